@@ -1,0 +1,134 @@
+/*
+ * halob200.h — C ABI of the B200-native Sylvie halo path (libhalob200.so).
+ *
+ * The reference (halobit, pure Python) has no FFI: the path sits behind
+ * Python call boundaries.  Each entry point below replaces one reference
+ * function (cited file:line under /root/reference/pkg/src/halobit); the Python
+ * host layer (paper_2303_01277_b200/) binds them with ctypes and keeps the
+ * reference's names, argument meaning and exceptions.  See INTEGRATION.md.
+ *
+ * Conventions
+ *   - All pointers are device pointers unless named h_*; sizes are element
+ *     counts; matrices are row-major with an explicit leading dimension (ld,
+ *     in elements).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *     and returns 0 on success or a negative HB_E* code; hb_last_error()
+ *     returns a thread-local message for the last failure.
+ *   - No call allocates persistent device memory; the caller (PyTorch) owns
+ *     every buffer.
+ */
+#ifndef HALOB200_H_
+#define HALOB200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_EINVAL (-1)     /* bad argument (maps to CodecError / ShapeError)   */
+#define HB_ECUDA (-2)      /* CUDA launch/runtime failure                        */
+#define HB_ENONFINITE (-3) /* reported via the device flag word, see hb_quantize_gather */
+
+/* Flag bits written (atomicOr) into the caller's device flag word. */
+#define HB_FLAG_NONFINITE 1u
+
+/* Wire block = the reference's QuantizedBlock.to_bytes() layout
+ * (codec.py:22-25, 71-76): 12-byte header <BBHII {1, bits, 0, rows, dim},
+ * rows x {f32 row_min, f32 row_scale}, rows x ceil(dim*bits/8) payload bytes.
+ * bits == 32 (passthrough): header + rows*dim fp32 (the accounting basis,
+ * codec.py:110-114).                                                         */
+#define HB_HEADER_BYTES 12
+
+/* One message = one (source partition -> destination partition) block of an
+ * exchange (transport.py:184-192).  40 bytes, 8-byte aligned. */
+typedef struct hb_segment {
+  uint64_t key0, key1;   /* Philox key of the sender's stream (rngstream.py:19-23)   */
+  uint64_t elem_offset;  /* stream index of element (row 0, col 0) of this block    */
+  uint64_t out;          /* device address of the block's wire image (header start) */
+  int32_t row_begin;     /* first row of this block in the flattened row list       */
+  int32_t num_rows;      /* rows in the block (> 0)                                  */
+} hb_segment_t;
+
+const char* hb_version(void);
+const char* hb_last_error(void);
+
+/* Replaces RngStream.uniforms (rngstream.py:38-39): out[i] = uniform of stream
+ * element start+i.  Used by parity tests to pin the device generator. */
+int hb_philox_uniforms(uint64_t key0, uint64_t key1, uint64_t start, int64_t n,
+                       double* out, void* stream);
+
+/* K1 — replaces the send half of exchange() (transport.py:184-192) fused with
+ * the gather of _fwd_outgoing/_bwd_outgoing (trainer.py:182,199) and
+ * quantize_rows + pack_code_matrix (codec.py:124-196):
+ *   for every segment s, row r of s:  x = src[row_idx[s.row_begin + r] * ld + 0..d)
+ *   writes the wire block of s at s.out (header written by the block's row 0).
+ * bits in {1..8, 16, 32}.  Non-finite input sets HB_FLAG_NONFINITE in *flags
+ * (the reference raises CodecError, codec.py:167-168; the host checks the flag
+ * at the exchange boundary).  `segs` is a device array of nseg descriptors
+ * sorted by row_begin. */
+int hb_quantize_gather(const float* src, int64_t ld, const int32_t* row_idx, int32_t total_rows,
+                       const hb_segment_t* segs, int32_t nseg, int32_t d, int32_t bits,
+                       uint32_t* flags, void* stream);
+
+/* K2 — replaces the receive half of exchange() (transport.py:195-204:
+ * dequantize_rows, codec.py:199-207) fused with _assemble_halo
+ * (trainer.py:208-212, accumulate = 0) or _integrate (trainer.py:214-216,
+ * accumulate = 1):
+ *   for i in [0, num_dst):  row t = dst_rows[i]
+ *     v = accumulate ? f64(dst[t]) : 0
+ *     for k in [src_ptr[i], src_ptr[i+1]):  v += dequant(received row src_rows[k])
+ *     dst[t] = f32(v)
+ * Received row q lives in the segment s with s.row_begin <= q < s.row_begin +
+ * s.num_rows (segs sorted by row_begin); sources are listed in ascending peer
+ * order, so the f64 sum follows the reference's ascending-peer integration. */
+int hb_dequant_gather(const hb_segment_t* segs, int32_t nseg, int32_t num_dst,
+                      const int32_t* dst_rows, const int32_t* src_ptr, const int32_t* src_rows,
+                      int32_t d, int32_t bits, float* dst, int64_t ld, int32_t accumulate,
+                      void* stream);
+
+/* K3/K4 — replaces linalg.spmm (linalg.py:71-75; called at trainer.py:291,293
+ * and, with the transposed block, trainer.py:318,321):
+ *   Y[i, 0:d) = sum_{k in [row_ptr[i], row_ptr[i+1])} vals[k] * X[col_idx[k], 0:d)
+ * (fp32, accumulated in index order). */
+int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+                const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream);
+
+/* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:
+ * grad rows outside the mask are zero, masked rows get (softmax - onehot)/norm;
+ * row_loss[i] = -log softmax[label] / norm (0 outside the mask) in f64.
+ * *loss_out = fixed-order sum of row_loss (deterministic, one CTA). */
+int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
+                    const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
+                    double* loss_out, void* stream);
+
+/* ReLU epilogue (linalg.py:78-80): y = max(z, 0), in place allowed. */
+int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream);
+
+/* relu_grad (linalg.py:83-84) fused with the product m = j * (h > 0)
+ * (trainer.py:312), where h = relu(z) of the same layer. */
+int hb_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, int32_t n, int32_t d,
+                     float* m, int64_t ldm, void* stream);
+
+/* adam_step (linalg.py:115-140), bias corrections bc1 = 1-b1^t, bc2 = 1-b2^t. */
+int hb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                 float b2, float eps, double bc1, double bc2, void* stream);
+
+/* Argmax accuracy counts for evaluate() (trainer.py:129-144):
+ * counts[2*k] = #rows with mask==k+1, counts[2*k+1] = #correct among them, k=0..2. */
+int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
+                       const uint8_t* mask, int64_t* counts, void* stream);
+
+/* Dropout on h~ (trainer.py:285-289, 322-323): keep = u >= p, drawn from the
+ * keyed stream (seed, "dropout", part, epoch, layer) over h~ of shape
+ * (nl+nh, d) in row-major order; out = keep ? x / (1-p) : 0.  Row r of this
+ * call is row (row0 + r) of the partition's h~, so the forward (on h~) and
+ * the backward (on j_full) regenerate the identical mask. */
+int hb_dropout(const float* x, int64_t ldx, int32_t nrows, int64_t row0, int32_t d, uint64_t key0,
+               uint64_t key1, float p, float* out, int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALOB200_H_ */

@@ -1,0 +1,135 @@
+// extern "C" entry points of libhalob200.so (declared in include/halob200.h).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include "common.cuh"
+
+namespace hb {
+cudaError_t launch_quantize_gather(const float*, int64_t, const int32_t*, int, const hb_segment_t*, int,
+                                   int, int, uint32_t*, cudaStream_t);
+cudaError_t launch_dequant_gather(const hb_segment_t*, int, int, const int32_t*, const int32_t*,
+                                  const int32_t*, int, int, float*, int64_t, int, cudaStream_t);
+cudaError_t launch_philox_uniforms(uint64_t, uint64_t, uint64_t, int64_t, double*, cudaStream_t);
+cudaError_t launch_spmm(int, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
+                        float*, int64_t, cudaStream_t);
+cudaError_t launch_xent(const float*, int64_t, int, int, const int32_t*, const uint8_t*, double, float*,
+                        int64_t, double*, double*, cudaStream_t);
+cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaStream_t);
+cudaError_t launch_relu_grad_mul(const float*, int64_t, const float*, int64_t, int, int, float*, int64_t,
+                                 cudaStream_t);
+cudaError_t launch_adam(float*, const float*, float*, float*, int64_t, float, float, float, float, double,
+                        double, cudaStream_t);
+cudaError_t launch_argmax_accuracy(const float*, int64_t, int, int, const int32_t*, const uint8_t*,
+                                   int64_t*, cudaStream_t);
+cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, uint64_t, float, float*,
+                           int64_t, cudaStream_t);
+
+int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n > 0 ? n : 148;
+  }
+  return cached;
+}
+}  // namespace hb
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(HB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HB_OK;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static bool valid_bits(int b) { return (b >= 1 && b <= 8) || b == 16 || b == 32; }
+
+extern "C" {
+
+const char* hb_version(void) { return "halob200 0.1 sm_100a"; }
+
+const char* hb_last_error(void) { return g_last_error.c_str(); }
+
+int hb_philox_uniforms(uint64_t key0, uint64_t key1, uint64_t start, int64_t n, double* out, void* stream) {
+  if (n < 0 || (n > 0 && !out)) return fail(HB_EINVAL, "hb_philox_uniforms: bad arguments");
+  return check(hb::launch_philox_uniforms(key0, key1, start, n, out, S(stream)), "hb_philox_uniforms");
+}
+
+int hb_quantize_gather(const float* src, int64_t ld, const int32_t* row_idx, int32_t total_rows,
+                       const hb_segment_t* segs, int32_t nseg, int32_t d, int32_t bits, uint32_t* flags,
+                       void* stream) {
+  if (!valid_bits(bits)) return fail(HB_EINVAL, "unsupported bit width " + std::to_string(bits));
+  if (total_rows < 0 || d <= 0 || ld < d || (total_rows > 0 && (!src || !row_idx || !segs || nseg <= 0)) ||
+      !flags)
+    return fail(HB_EINVAL, "hb_quantize_gather: bad arguments");
+  return check(hb::launch_quantize_gather(src, ld, row_idx, total_rows, segs, nseg, d, bits, flags, S(stream)),
+               "hb_quantize_gather");
+}
+
+int hb_dequant_gather(const hb_segment_t* segs, int32_t nseg, int32_t num_dst, const int32_t* dst_rows,
+                      const int32_t* src_ptr, const int32_t* src_rows, int32_t d, int32_t bits, float* dst,
+                      int64_t ld, int32_t accumulate, void* stream) {
+  if (!valid_bits(bits)) return fail(HB_EINVAL, "unsupported bit width " + std::to_string(bits));
+  if (num_dst < 0 || d <= 0 || ld < d || (num_dst > 0 && (!segs || nseg <= 0 || !dst_rows || !src_ptr || !dst)))
+    return fail(HB_EINVAL, "hb_dequant_gather: bad arguments");
+  return check(hb::launch_dequant_gather(segs, nseg, num_dst, dst_rows, src_ptr, src_rows, d, bits, dst, ld,
+                                         accumulate, S(stream)),
+               "hb_dequant_gather");
+}
+
+int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+                const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)))
+    return fail(HB_EINVAL, "hb_spmm_csr: bad arguments");
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, S(stream)), "hb_spmm_csr");
+}
+
+int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
+                    const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
+                    double* loss_out, void* stream) {
+  if (n < 0 || C <= 0 || norm <= 0 || !loss_out || (n > 0 && (!logits || !labels || !mask || !grad || !row_loss)))
+    return fail(HB_EINVAL, "hb_softmax_xent: bad arguments");
+  return check(hb::launch_xent(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss, loss_out, S(stream)),
+               "hb_softmax_xent");
+}
+
+int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream) {
+  if (n < 0 || d < 0) return fail(HB_EINVAL, "hb_relu: bad arguments");
+  return check(hb::launch_relu(z, ldz, n, d, y, ldy, S(stream)), "hb_relu");
+}
+
+int hb_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, int32_t n, int32_t d, float* m,
+                     int64_t ldm, void* stream) {
+  if (n < 0 || d < 0) return fail(HB_EINVAL, "hb_relu_grad_mul: bad arguments");
+  return check(hb::launch_relu_grad_mul(j, ldj, h, ldh, n, d, m, ldm, S(stream)), "hb_relu_grad_mul");
+}
+
+int hb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                 float eps, double bc1, double bc2, void* stream) {
+  if (n < 0 || bc1 <= 0 || bc2 <= 0) return fail(HB_EINVAL, "hb_adam_step: bad arguments");
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, S(stream)), "hb_adam_step");
+}
+
+int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
+                       const uint8_t* mask, int64_t* counts, void* stream) {
+  if (n < 0 || C <= 0 || !counts) return fail(HB_EINVAL, "hb_argmax_accuracy: bad arguments");
+  return check(hb::launch_argmax_accuracy(logits, ld, n, C, labels, mask, counts, S(stream)),
+               "hb_argmax_accuracy");
+}
+
+int hb_dropout(const float* x, int64_t ldx, int32_t nrows, int64_t row0, int32_t d, uint64_t key0, uint64_t key1,
+               float p, float* out, int64_t ldo, void* stream) {
+  if (nrows < 0 || d < 0 || row0 < 0 || !(p >= 0.f && p < 1.f)) return fail(HB_EINVAL, "hb_dropout: bad arguments");
+  return check(hb::launch_dropout(x, ldx, nrows, row0, d, key0, key1, p, out, ldo, S(stream)), "hb_dropout");
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+// Small fused elementwise/row kernels around the halo path (K8):
+// masked softmax-CE + grad (linalg.py:87-112), ReLU / relu' product
+// (linalg.py:78-84, trainer.py:295,312), Adam (linalg.py:115-140),
+// argmax accuracy (trainer.py:129-144) and keyed dropout (trainer.py:285-289).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace hb {
+
+// ---- masked softmax cross-entropy: warp per row ------------------------------
+__global__ void xent_rows_kernel(const float* __restrict__ logits, int64_t ld, int n, int C,
+                                 const int32_t* __restrict__ labels, const uint8_t* __restrict__ mask,
+                                 double norm, float* __restrict__ grad, int64_t ldg,
+                                 double* __restrict__ row_loss) {
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    float* g = grad + (int64_t)row * ldg;
+    if (!mask[row]) {
+      for (int c = lane; c < C; c += 32) g[c] = 0.f;
+      if (lane == 0) row_loss[row] = 0.0;
+      continue;
+    }
+    const float* z = logits + (int64_t)row * ld;
+    float m = -__int_as_float(0x7f800000);
+    for (int c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
+    m = warp_max(m);
+    double s = 0.0;
+    for (int c = lane; c < C; c += 32) s += exp((double)z[c] - (double)m);
+    s = warp_sum_d(s);
+    const int y = labels[row];
+    const double inv = 1.0 / s;
+    for (int c = lane; c < C; c += 32) {
+      const double p = exp((double)z[c] - (double)m) * inv;
+      g[c] = (float)((p - (c == y ? 1.0 : 0.0)) / norm);
+    }
+    if (lane == 0) row_loss[row] = -(((double)z[y] - (double)m) - log(s)) / norm;
+  }
+}
+
+// Deterministic fixed-order sum of row_loss: one CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) sum_f64_kernel(const double* __restrict__ x, int n,
+                                                       double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) acc += x[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 512; s; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ---- ReLU and relu' product ----------------------------------------------------
+__global__ void relu_kernel(const float* __restrict__ z, int64_t ldz, int n, int d,
+                            float* __restrict__ y, int64_t ldy) {
+  const int64_t total = (int64_t)n * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i - r * d;
+    const float v = z[r * ldz + c];
+    y[r * ldy + c] = (v > 0.f || v != v) ? v : 0.f;  // np.maximum propagates NaN
+  }
+}
+
+__global__ void relu_grad_mul_kernel(const float* __restrict__ j, int64_t ldj, const float* __restrict__ h,
+                                     int64_t ldh, int n, int d, float* __restrict__ m, int64_t ldm) {
+  const int64_t total = (int64_t)n * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i - r * d;
+    m[r * ldm + c] = h[r * ldh + c] > 0.f ? j[r * ldj + c] : 0.f;
+  }
+}
+
+// ---- Adam ------------------------------------------------------------------------
+__global__ void adam_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps,
+                            double bc1, double bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = g[i];
+    const double mi = (double)b1 * m[i] + (1.0 - (double)b1) * gi;
+    const double vi = (double)b2 * v[i] + (1.0 - (double)b2) * gi * gi;
+    m[i] = (float)mi;
+    v[i] = (float)vi;
+    const double upd = (double)lr * (mi / bc1) / (sqrt(vi / bc2) + (double)eps);
+    w[i] = (float)((double)w[i] - upd);
+  }
+}
+
+// ---- argmax accuracy ---------------------------------------------------------
+__global__ void argmax_acc_kernel(const float* __restrict__ logits, int64_t ld, int n, int C,
+                                  const int32_t* __restrict__ labels, const uint8_t* __restrict__ mask,
+                                  unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long local[6] = {0, 0, 0, 0, 0, 0};
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    const int mk = mask[row];
+    if (mk < 1 || mk > 3) continue;
+    const float* z = logits + (int64_t)row * ld;
+    float best = -__int_as_float(0x7f800000);
+    int arg = 0x7fffffff;
+    for (int c = lane; c < C; c += 32) {
+      const float v = z[c];
+      if (v > best || (v == best && c < arg)) { best = v; arg = c; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+    }
+    if (lane == 0) {
+      local[2 * (mk - 1)] += 1;
+      local[2 * (mk - 1) + 1] += (arg == labels[row]) ? 1 : 0;
+    }
+  }
+  if (lane == 0)
+    for (int k = 0; k < 6; ++k)
+      if (local[k]) atomicAdd(counts + k, local[k]);
+}
+
+// ---- keyed dropout -----------------------------------------------------------------
+__global__ void dropout_kernel(const float* __restrict__ x, int64_t ldx, int nrows, int64_t row0, int d,
+                               uint64_t k0, uint64_t k1, double p, float scale, float* __restrict__ out,
+                               int64_t ldo) {
+  const uint64_t e_begin = (uint64_t)row0 * d, e_end = (uint64_t)(row0 + nrows) * d;
+  const uint64_t b_first = e_begin >> 2, b_last = (e_end - 1) >> 2;
+  for (uint64_t b = b_first + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= b_last;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const U64x4 u = philox4x64_10(b + 1, k0, k1);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint64_t e = 4 * b + s;
+      if (e < e_begin || e >= e_end) continue;
+      const int64_t r = (int64_t)(e / d) - row0, c = (int64_t)(e % d);
+      const bool keep = u53_to_double(pick(u, s)) >= p;
+      out[r * ldo + c] = keep ? x[r * ldx + c] * scale : 0.f;
+    }
+  }
+}
+
+static int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t launch_xent(const float* logits, int64_t ld, int n, int C, const int32_t* labels,
+                        const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
+                        double* loss_out, cudaStream_t st) {
+  if (n > 0) xent_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss);
+  sum_f64_kernel<<<1, 1024, 0, st>>>(row_loss, n, loss_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relu(const float* z, int64_t ldz, int n, int d, float* y, int64_t ldy, cudaStream_t st) {
+  if ((int64_t)n * d <= 0) return cudaSuccess;
+  relu_kernel<<<grid_for((int64_t)n * d, 256), 256, 0, st>>>(z, ldz, n, d, y, ldy);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, int n, int d,
+                                 float* m, int64_t ldm, cudaStream_t st) {
+  if ((int64_t)n * d <= 0) return cudaSuccess;
+  relu_grad_mul_kernel<<<grid_for((int64_t)n * d, 256), 256, 0, st>>>(j, ldj, h, ldh, n, d, m, ldm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                        float b2, float eps, double bc1, double bc2, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  adam_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_accuracy(const float* logits, int64_t ld, int n, int C, const int32_t* labels,
+                                   const uint8_t* mask, int64_t* counts, cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, 6 * sizeof(int64_t), st);
+  if (n > 0)
+    argmax_acc_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask,
+                                                       reinterpret_cast<unsigned long long*>(counts));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dropout(const float* x, int64_t ldx, int nrows, int64_t row0, int d, uint64_t k0,
+                           uint64_t k1, float p, float* out, int64_t ldo, cudaStream_t st) {
+  if ((int64_t)nrows * d <= 0) return cudaSuccess;
+  const float scale = (float)(1.0 / (1.0 - (double)p));
+  dropout_kernel<<<grid_for(((int64_t)nrows * d) / 4 + 2, 256), 256, 0, st>>>(x, ldx, nrows, row0, d, k0, k1,
+                                                                              (double)p, scale, out, ldo);
+  return cudaGetLastError();
+}
+
+}  // namespace hb

@@ -1,0 +1,72 @@
+"""Thin torch-tensor wrappers over the C-ABI kernels (no host fallback).
+
+Each wrapper names the reference function it replaces.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from ._lib import ptr, stream_handle
+
+
+class DeviceCsr:
+    """CSR matrix resident in HBM: int64 row_ptr, int32 col_idx, fp32 values."""
+
+    def __init__(self, rows: int, cols: int, row_ptr, col_idx, values, device):
+        import torch
+        self.rows, self.cols = int(rows), int(cols)
+        self.row_ptr = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int64)).to(device)
+        self.col_idx = torch.from_numpy(np.ascontiguousarray(col_idx, dtype=np.int32)).to(device)
+        self.values = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(device)
+        self.nnz = int(self.col_idx.numel())
+
+    @classmethod
+    def from_csr(cls, m, device):
+        return cls(m.rows, m.cols, m.row_ptr, m.col_idx, m.values, device)
+
+
+def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None):
+    """``linalg.spmm`` (linalg.py:71-75): out[:rows, :d] = A @ x[:, :d]."""
+    d = x.shape[1] if d is None else d
+    _lib.call("hb_spmm_csr", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
+              x.stride(0), d, ptr(out), out.stride(0), stream_handle(stream))
+    return out
+
+
+def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None):
+    """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device."""
+    n = labels.numel()
+    _lib.call("hb_softmax_xent", ptr(logits), logits.stride(0), n, C, ptr(labels), ptr(mask),
+              float(norm), ptr(grad), grad.stride(0), ptr(row_loss), ptr(loss_out),
+              stream_handle(stream))
+
+
+def relu(z, y, n: int, d: int, stream=None):
+    """``linalg.relu`` (linalg.py:78-80)."""
+    _lib.call("hb_relu", ptr(z), z.stride(0), n, d, ptr(y), y.stride(0), stream_handle(stream))
+
+
+def relu_grad_mul(j, h, m, n: int, d: int, stream=None):
+    """``j * relu_grad(z)`` (trainer.py:312, linalg.py:83-84) with h = relu(z)."""
+    _lib.call("hb_relu_grad_mul", ptr(j), j.stride(0), ptr(h), h.stride(0), n, d, ptr(m),
+              m.stride(0), stream_handle(stream))
+
+
+def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None):
+    """``linalg.adam_step`` (linalg.py:127-140) in place on device tensors."""
+    _lib.call("hb_adam_step", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
+              float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, stream_handle(stream))
+
+
+def argmax_accuracy(logits, C: int, labels, mask, counts, stream=None):
+    """Counts for ``evaluate`` (trainer.py:129-144)."""
+    _lib.call("hb_argmax_accuracy", ptr(logits), logits.stride(0), labels.numel(), C,
+              ptr(labels), ptr(mask), ptr(counts), stream_handle(stream))
+
+
+def dropout(x, nrows: int, row0: int, d: int, key, p: float, out, stream=None):
+    """Keyed dropout of ``trainer.py:285-289`` (mask regenerated, never stored)."""
+    _lib.call("hb_dropout", ptr(x), x.stride(0), nrows, row0, d, int(key[0]), int(key[1]),
+              float(p), ptr(out), out.stride(0), stream_handle(stream))

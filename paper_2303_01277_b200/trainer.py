@@ -1,0 +1,530 @@
+"""Sylvie-S / Sylvie-A training on the B200: drop-in for ``halobit.trainer``.
+
+Public surface kept from the reference (``trainer.py:32-465``):
+``ModelConfig``, ``TrainMode``, ``staleness_adaptor``, ``MetricsRecord``,
+``TrainResult``, ``TrainingError``, ``init_weights``, ``train`` — same
+arguments, same semantics, same exceptions.  Underneath, each rank (one per
+GPU; a single rank hosts all partitions in the one-GPU case, exactly like the
+reference's one-process simulation) runs the epoch on device-resident buffers:
+
+  forward, layer l:   halo exchange (K1 -> [NCCL] -> K2)  |  Sylvie-A: consume
+                      epoch t-1 halo, ship epoch t halo for t+1
+                      p = A h~ (K3 SpMM)  [SAGE: p = [h~_local | M h~]]
+                      z = p W (GEMM);  h = relu(z)
+  loss:               masked softmax-CE with the global normaliser (K8)
+  backward, layer l:  m = j * relu'(z);  G = p^T m;  j_full = A^T (m W^T) (K4)
+                      halo gradient exchange, ascending-peer integration (K2)
+  all-reduce(G), NaN check, Adam.
+
+Numerics are fp32 (f64 in the reference); the codec decisions are bit-exact
+given identical fp32 inputs (see codec.py).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import ops
+from .codec import CodecError, QuantConfig, quantize_gather, dequant_gather
+from .graph import Graph, Partition
+from .rngstream import BACKWARD, FORWARD, derive_key, keyed_generator
+from .transport import ExchangeBuffers, ProtocolError, RankLayout, TransportStats, nccl_exchange
+
+MODELS = ("gcn", "sage")
+
+
+class TrainingError(RuntimeError):
+    pass
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    widths: tuple
+    model: str = "gcn"
+    dropout: float = 0.0
+
+    def __post_init__(self):
+        if len(self.widths) < 2 or any(w <= 0 for w in self.widths):
+            raise TrainingError("widths must list input, hidden(s), and output dims")
+        if self.model not in MODELS:
+            raise TrainingError(f"unknown model {self.model!r}")
+        if not (0.0 <= self.dropout < 1.0):
+            raise TrainingError("dropout must be in [0, 1)")
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.widths) - 1
+
+
+@dataclass(frozen=True)
+class TrainMode:
+    variant: str = "sync"
+    staleness: int = 0
+
+    def __post_init__(self):
+        if self.variant not in ("sync", "async"):
+            raise TrainingError(f"unknown mode {self.variant!r}")
+        if self.staleness < 0:
+            raise TrainingError("staleness interval must be >= 0")
+
+
+def staleness_adaptor(epoch: int, mode: TrainMode) -> str:
+    """Bounded Staleness Adaptor (trainer.py:70-76)."""
+    if mode.variant == "sync":
+        return "sync"
+    if mode.staleness > 0 and epoch % mode.staleness == 0:
+        return "sync"
+    return "async"
+
+
+@dataclass
+class MetricsRecord:
+    epoch: int
+    mode_this_epoch: str
+    train_loss: float
+    train_acc: float
+    val_acc: float
+    test_acc: float
+    main_bytes: int
+    meta_bytes: int
+    header_bytes: int
+    allreduce_bytes: int
+    messages: int
+    wall_ms: int = 0
+
+
+@dataclass
+class TrainResult:
+    metrics: list
+    final_weights: list
+    timings_ms: list = field(default_factory=list)
+
+
+def init_weights(cfg: ModelConfig, seed: int) -> list:
+    """Glorot-uniform from keyed Philox (trainer.py:102-112); float64 host arrays."""
+    out = []
+    for l in range(1, cfg.num_layers + 1):
+        fan_in = cfg.widths[l - 1] * (2 if cfg.model == "sage" else 1)
+        lim = np.sqrt(6.0 / (fan_in + cfg.widths[l]))
+        out.append(keyed_generator(seed, "init", l).uniform(-lim, lim, size=(fan_in, cfg.widths[l])))
+    return out
+
+
+def _ld(d: int) -> int:
+    return (d + 3) // 4 * 4
+
+
+def _stack_csr(layout: RankLayout, which: str):
+    """Block-diagonal CSR over all hosted partitions, columns remapped into the
+    rank's [local | halo] row space (graph.py:218-229 column order per part)."""
+    rps, cols, vals = [np.zeros(1, dtype=np.int64)], [], []
+    nnz = 0
+    for p in layout.parts:
+        m = p.adj_block if which == "adj" else p.mean_block
+        c = np.asarray(m.col_idx, dtype=np.int64)
+        nl = p.num_local
+        c = np.where(c < nl, layout.loc_base[p.id] + c,
+                     layout.NL + layout.halo_base[p.id] + (c - nl))
+        rps.append(np.asarray(m.row_ptr[1:], dtype=np.int64) + nnz)
+        nnz += int(m.row_ptr[-1])
+        cols.append(c)
+        vals.append(np.asarray(m.values))
+    rp = np.concatenate(rps)
+    ci = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    v = np.concatenate(vals) if vals else np.zeros(0)
+    return rp, ci, v
+
+
+def _transpose(rows, cols, rp, ci, v):
+    r = np.repeat(np.arange(rows, dtype=np.int64), np.diff(rp))
+    o = np.argsort(ci, kind="stable")
+    trp = np.zeros(cols + 1, dtype=np.int64)
+    np.cumsum(np.bincount(ci, minlength=cols), out=trp[1:])
+    return trp, r[o], v[o]
+
+
+class DeviceRank:
+    """One rank's share of the training: buffers, exchanges, epoch loop."""
+
+    def __init__(self, layout: RankLayout, cfg: ModelConfig, mode: TrainMode, quant: QuantConfig,
+                 seed: int, lr: float, global_norm: int, device=None, group=None, probe=None,
+                 features=None):
+        import torch
+        self.torch = torch
+        self.dev = torch.device(device or "cuda")
+        self.layout, self.cfg, self.mode, self.quant = layout, cfg, mode, quant
+        self.seed, self.lr, self.norm = seed, lr, float(global_norm)
+        self.group, self.probe = group, probe
+        self.world = 1
+        if group is not None or _dist_initialized():
+            import torch.distributed as dist
+            self.world = dist.get_world_size(group)
+        L, W = cfg.num_layers, cfg.widths
+        self.L = L
+        NL, NH = layout.NL, layout.NH
+        self.NL, self.NH = NL, NH
+        dev = self.dev
+        f32 = torch.float32
+        layout.to(dev)
+        # graph operators
+        which = "mean" if cfg.model == "sage" else "adj"
+        rp, ci, v = _stack_csr(layout, which)
+        self.A = ops.DeviceCsr(NL, NL + NH, rp, ci, v, dev)
+        trp, tci, tv = _transpose(NL, NL + NH, rp, ci, v)
+        self.At = ops.DeviceCsr(NL + NH, NL, trp, tci, tv, dev)
+        # activations: Ht[l] = [local ; halo] input of layer l (ld padded to 16 B)
+        self.Ht = {l: torch.zeros((NL + NH, _ld(W[l - 1])), dtype=f32, device=dev)
+                   for l in range(1, L + 1)}
+        feats = features if features is not None else \
+            np.concatenate([np.asarray(p.features, dtype=np.float32) for p in layout.parts])
+        self.Ht[1][:NL, :W[0]] = torch.from_numpy(np.ascontiguousarray(feats, dtype=np.float32)).to(dev)
+        self.drop = cfg.dropout > 0.0
+        self.Hd = {l: torch.zeros_like(self.Ht[l]) for l in range(1, L + 1)} if self.drop else self.Ht
+        self.AGG = {l: torch.zeros((NL, _ld(W[l - 1])), dtype=f32, device=dev) for l in range(1, L + 1)}
+        self.Z = {l: torch.zeros((NL, W[l]), dtype=f32, device=dev) for l in range(1, L + 1)}
+        self.JF = {l: torch.zeros((NL + NH, _ld(W[l - 1])), dtype=f32, device=dev) for l in range(2, L + 1)}
+        self.T = {l: torch.zeros((NL, W[l - 1]), dtype=f32, device=dev) for l in range(2, L + 1)}
+        self.JL = torch.zeros((NL, W[L]), dtype=f32, device=dev)
+        self.row_loss = torch.zeros(max(1, NL), dtype=torch.float64, device=dev)
+        self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(6, dtype=torch.int64, device=dev)
+        labels = np.concatenate([np.asarray(p.labels) for p in layout.parts]).astype(np.int32)
+        self.labels = torch.from_numpy(labels).to(dev)
+        tm = np.concatenate([np.asarray(p.train_mask, dtype=bool) for p in layout.parts])
+        self.train_mask = torch.from_numpy(tm.astype(np.uint8)).to(dev)
+        em = np.zeros(NL, dtype=np.uint8)
+        off = 0
+        for p in layout.parts:
+            n = p.num_local
+            em[off:off + n][np.asarray(p.train_mask, bool)] = 1
+            em[off:off + n][np.asarray(p.val_mask, bool)] = 2
+            em[off:off + n][np.asarray(p.test_mask, bool)] = 3
+            off += n
+        self.eval_mask = torch.from_numpy(em).to(dev)
+        # parameters (replicated; identical Glorot init on every rank, no broadcast)
+        w0 = init_weights(cfg, seed)
+        self.W = [torch.from_numpy(w.astype(np.float32)).to(dev) for w in w0]
+        self.gflat = torch.zeros(sum(w.numel() for w in self.W), dtype=f32, device=dev)
+        off = 0
+        self.G = []
+        for w in self.W:
+            self.G.append(self.gflat[off:off + w.numel()].view_as(w))
+            off += w.numel()
+        self.adam_m = [torch.zeros_like(w) for w in self.W]
+        self.adam_v = [torch.zeros_like(w) for w in self.W]
+        self.adam_t = 0
+        # exchange buffers
+        par = 2 if mode.variant == "async" else 1
+        self.xf = {l: ExchangeBuffers(layout, layout.fwd, W[l - 1], quant.bits, dev, par)
+                   for l in range(1, L + 1)}
+        self.xb = {l: ExchangeBuffers(layout, layout.bwd, W[l - 1], quant.bits, dev, par)
+                   for l in range(2, L + 1)}
+        self.xeval = None
+        self.slots = {}
+        self.stats = {p: TransportStats() for p in layout.ids}
+        self.epoch_loss = 0.0
+        self.comm_stream = torch.cuda.Stream(device=dev) if self.world > 1 else None
+        self.launches = 0
+
+    # -- exchange helpers -----------------------------------------------------
+    def _count(self, bufs: ExchangeBuffers):
+        for p, (mb, md, hd, ms) in bufs.stats_delta().items():
+            s = self.stats[p]
+            s.main_bytes_sent += mb
+            s.metadata_bytes_sent += md
+            s.header_bytes_sent += hd
+            s.messages_sent += ms
+
+    def _send(self, bufs: ExchangeBuffers, src, epoch: int, layer: int, parity: int, count=True):
+        """K1 for every hosted sender (+ NCCL for remote peers)."""
+        torch = self.torch
+        if bufs.n_send:
+            tab = bufs.send_table(self.seed, epoch, layer, parity)
+            segs = torch.from_numpy(tab.view(np.uint8).copy()).to(self.dev, non_blocking=False)
+            bufs._segs_keepalive = segs
+            quantize_gather(src, bufs.plan.dev["send_rows"], segs, bufs.n_send, bufs.d, bufs.bits,
+                            self.flags)
+            self.launches += 1
+            if self.probe:
+                self._probe_out(bufs, epoch, layer)
+        if self.world > 1:
+            ev = torch.cuda.current_stream().record_event()
+            with torch.cuda.stream(self.comm_stream):
+                self.comm_stream.wait_event(ev)
+                nccl_exchange(bufs, parity, self.group)
+            torch.cuda.current_stream().wait_stream(self.comm_stream)
+        if count:
+            self._count(bufs)
+
+    def _recv(self, bufs: ExchangeBuffers, parity: int, dst, accumulate: bool):
+        """K2: forward scatter into halo rows / backward ascending-peer integration."""
+        if bufs.n_recv == 0:
+            return
+        pd = bufs.plan.dev
+        dequant_gather(bufs.recv_segs[parity], bufs.n_recv, pd["dst_rows"], pd["src_ptr"],
+                       pd["src_rows"], bufs.d, bufs.bits, dst, accumulate)
+        self.launches += 1
+
+    def _probe_out(self, bufs, epoch, layer):
+        for m in bufs.plan.send_msgs:
+            p = self.layout.parts[self.layout.ids.index(m.src)]
+            if bufs.plan.phase == FORWARD:
+                gids = p.local_nodes[p.send_sets[m.dst]]
+            else:
+                gids = p.halo_nodes[p.recv_sets[m.dst]]
+            self.probe("exchange_out", part=m.src, peer=m.dst, epoch=epoch, layer=layer,
+                       phase=bufs.plan.phase, global_ids=gids)
+
+    def _consume(self, epoch: int, layer: int, phase: str) -> int:
+        """trainer.py:232-246 — tags are tracked on the host."""
+        tag = self.slots.get((layer, phase))
+        if tag is None:
+            if epoch > 1:
+                raise ProtocolError(f"buffer underflow: ({layer}, {phase}) never filled before epoch {epoch}")
+            return 0
+        if tag != epoch - 1:
+            raise ProtocolError(f"staleness violation on ({layer}, {phase}): buffer from epoch {tag}, "
+                                f"consuming at epoch {epoch}")
+        return tag
+
+    def _dropout(self, src, dst, epoch: int, layer: int, d: int):
+        lay = self.layout
+        for p in lay.parts:
+            key = derive_key((self.seed, "dropout", p.id, epoch, layer))
+            lb, hb = lay.loc_base[p.id], lay.NL + lay.halo_base[p.id]
+            if p.num_local:
+                ops.dropout(src[lb:], p.num_local, 0, d, key, self.cfg.dropout, dst[lb:])
+            if p.num_halo:
+                ops.dropout(src[hb:], p.num_halo, p.num_local, d, key, self.cfg.dropout, dst[hb:])
+            self.launches += 2
+
+    # -- forward / backward -----------------------------------------------------
+    def forward(self, epoch: int, epoch_mode: str, training: bool = True):
+        torch = self.torch
+        W, L, NL = self.cfg.widths, self.L, self.NL
+        sync_variant = self.mode.variant == "sync"
+        for l in range(1, L + 1):
+            d = W[l - 1]
+            H = self.Ht[l]
+            if not training:
+                bufs = self.xeval[l]
+                self._send(bufs, H, epoch, l, 0, count=False)
+                self._recv(bufs, 0, H, False)
+            elif sync_variant:
+                bufs = self.xf[l]
+                self._send(bufs, H, epoch, l, 0)
+                self._recv(bufs, 0, H, False)
+            elif epoch_mode == "sync":
+                bufs = self.xf[l]
+                if epoch > 1:
+                    self._consume(epoch, l, FORWARD)
+                self._send(bufs, H, epoch, l, epoch % 2)
+                self._recv(bufs, epoch % 2, H, False)
+                self.slots[(l, FORWARD)] = epoch
+            else:
+                bufs = self.xf[l]
+                tag = self._consume(epoch, l, FORWARD)
+                if tag == 0:
+                    H[NL:].zero_()
+                else:
+                    self._recv(bufs, (epoch - 1) % 2, H, False)
+                if self.probe:
+                    self._probe_halo(epoch, l, tag, H, d)
+                self._send(bufs, H, epoch, l, epoch % 2)
+                self.slots[(l, FORWARD)] = epoch
+            Hd = H
+            if training and self.drop:
+                Hd = self.Hd[l]
+                self._dropout(H, Hd, epoch, l, d)
+            agg = self.AGG[l]
+            ops.spmm(self.A, Hd, agg, d)
+            self.launches += 1
+            Z = self.Z[l]
+            if self.cfg.model == "sage":
+                torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
+                Z.addmm_(agg[:, :d], self.W[l - 1][d:])
+            else:
+                torch.mm(agg[:, :d], self.W[l - 1], out=Z)
+            if l < L:
+                ops.relu(Z, self.Ht[l + 1], NL, W[l])
+                self.launches += 1
+        return self.Z[L]
+
+    def _probe_halo(self, epoch, layer, tag, H, d):
+        lay = self.layout
+        for p in lay.parts:
+            hb = lay.NL + lay.halo_base[p.id]
+            data = H[hb:hb + p.num_halo, :d].double().cpu().numpy()
+            self.probe("halo_consumed", part=p.id, epoch=epoch, layer=layer, phase=FORWARD,
+                       tag=tag, data=data)
+
+    def backward(self, epoch: int, epoch_mode: str, logits):
+        torch = self.torch
+        W, L, NL = self.cfg.widths, self.L, self.NL
+        sync_variant = self.mode.variant == "sync"
+        C = W[L]
+        ops.softmax_xent(logits, C, self.labels, self.train_mask, self.norm, self.JL,
+                         self.row_loss, self.loss_dev)
+        self.launches += 2
+        J = self.JL
+        for l in range(L, 0, -1):
+            d, dout = W[l - 1], W[l]
+            if l < L:
+                ops.relu_grad_mul(J, self.Ht[l + 1], J, NL, dout)
+                self.launches += 1
+            m = J[:, :dout]
+            Hd = self.Hd[l] if self.drop else self.Ht[l]
+            agg = self.AGG[l]
+            G = self.G[l - 1]
+            if self.cfg.model == "sage":
+                torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
+                torch.mm(agg[:, :d].t(), m, out=G[d:])
+            else:
+                torch.mm(agg[:, :d].t(), m, out=G)
+            if l == 1:
+                break
+            T, JF = self.T[l], self.JF[l]
+            Wl = self.W[l - 1]
+            if self.cfg.model == "sage":
+                torch.mm(m, Wl[d:].t(), out=T)
+                ops.spmm(self.At, T, JF, d)
+                JF[:NL, :d].addmm_(m, Wl[:d].t())
+            else:
+                torch.mm(m, Wl.t(), out=T)
+                ops.spmm(self.At, T, JF, d)
+            self.launches += 1
+            if self.drop:
+                self._dropout(JF, JF, epoch, l, d)
+            bufs = self.xb[l]
+            if sync_variant:
+                self._send(bufs, JF, epoch, l, 0)
+                self._recv(bufs, 0, JF, True)
+            elif epoch_mode == "sync":
+                if epoch > 1:
+                    self._consume(epoch, l, BACKWARD)
+                self._send(bufs, JF, epoch, l, epoch % 2)
+                self._recv(bufs, epoch % 2, JF, True)
+                self.slots[(l, BACKWARD)] = epoch
+            else:
+                if epoch > 1:
+                    self._consume(epoch, l, BACKWARD)
+                    self._recv(bufs, (epoch - 1) % 2, JF, True)
+                self._send(bufs, JF, epoch, l, epoch % 2)
+                self.slots[(l, BACKWARD)] = epoch
+            J = JF[:NL]
+        return self.loss_dev
+
+    def step(self, epoch: int):
+        """All-reduce, Adam (trainer.py:358-366); returns nothing, loss stays on device."""
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.gflat, group=self.group)
+            dist.all_reduce(self.loss_dev, group=self.group)
+        self.adam_t += 1
+        for w, g, m, v in zip(self.W, self.G, self.adam_m, self.adam_v):
+            ops.adam_step(w, g, m, v, self.lr, self.adam_t)
+            self.launches += 1
+
+    def run_epoch(self, epoch: int, check: bool = True) -> str:
+        epoch_mode = staleness_adaptor(epoch, self.mode)
+        logits = self.forward(epoch, epoch_mode)
+        self.backward(epoch, epoch_mode, logits)
+        if check:
+            self.check_epoch(epoch)
+        self.step(epoch)
+        return epoch_mode
+
+    def check_epoch(self, epoch: int):
+        """Host checks of the reference (codec.py:167-168, trainer.py:361-363)."""
+        flags = int(self.flags.item())
+        if flags & 1:
+            raise TrainingError(f"worker {self.layout.ids[0]} aborted: "
+                                f"{CodecError('non-finite values in quantizer input')}")
+        loss = float(self.loss_dev.item())
+        if not math.isfinite(loss):
+            raise TrainingError(f"worker {self.layout.ids[0]} aborted: NaN/inf loss at epoch {epoch}: "
+                                "learning rate too high or codec error")
+        self.epoch_loss = loss
+
+    def evaluate(self) -> dict:
+        """Full-precision forward (no dropout, passthrough halos) + argmax
+        accuracy on every mask (trainer.py:115-144), on device."""
+        if self.xeval is None:
+            self.xeval = {l: ExchangeBuffers(self.layout, self.layout.fwd, self.cfg.widths[l - 1], 32,
+                                             self.dev, 1) for l in range(1, self.L + 1)}
+        logits = self.forward(0, "sync", training=False)
+        ops.argmax_accuracy(logits, self.cfg.widths[-1], self.labels, self.eval_mask, self.counts)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.counts, group=self.group)
+        c = self.counts.cpu().numpy()
+        names = ("train_acc", "val_acc", "test_acc")
+        return {n: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0)
+                for k, n in enumerate(names)}
+
+    def weights_host(self) -> list:
+        return [w.double().cpu().numpy() for w in self.W]
+
+    def total_stats(self) -> dict:
+        t = TransportStats()
+        for s in self.stats.values():
+            t.main_bytes_sent += s.main_bytes_sent
+            t.metadata_bytes_sent += s.metadata_bytes_sent
+            t.header_bytes_sent += s.header_bytes_sent
+            t.messages_sent += s.messages_sent
+            t.allreduce_bytes += s.allreduce_bytes
+        return t.snapshot()
+
+
+def _dist_initialized() -> bool:
+    try:
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized()
+    except Exception:
+        return False
+
+
+def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMode,
+          quant_cfg: QuantConfig, epochs: int, seed: int, lr: float = 0.01, probe=None,
+          timeout: float = 60.0, device=None, evaluate_each_epoch: bool = True) -> TrainResult:
+    """Drop-in for ``halobit.train`` (trainer.py:386-465) on one GPU: every
+    partition is hosted by this process's device (the reference's one-process
+    simulation, with device-resident halo traffic)."""
+    import time
+    n = len(partitions)
+    global_norm = max(1, int(np.asarray(graph.train_mask).sum()))
+    layout = RankLayout({p.id: p for p in partitions}, [0] * n, 0)
+    eng = DeviceRank(layout, model_cfg, mode, quant_cfg, seed, lr, global_norm, device=device,
+                     probe=probe)
+    if epochs == 0:
+        return TrainResult([], init_weights(model_cfg, seed))
+    ar_per_epoch = (4 * sum(int(w.numel()) for w in eng.W)) if n > 1 else 0
+    metrics, timings = [], []
+    prev = eng.total_stats()
+    for epoch in range(1, epochs + 1):
+        t0 = time.perf_counter()
+        try:
+            epoch_mode = eng.run_epoch(epoch)
+        except ProtocolError as e:
+            raise TrainingError(f"worker {layout.ids[0]} aborted: {e}") from e
+        for p in layout.ids:
+            eng.stats[p].allreduce_bytes += ar_per_epoch
+        stats = eng.total_stats()
+        accs = eng.evaluate() if evaluate_each_epoch else dict(train_acc=0.0, val_acc=0.0, test_acc=0.0)
+        if probe:
+            wts = eng.weights_host()
+            probe("weights", epoch=epoch, weights=[[w.copy() for w in wts] for _ in range(n)])
+        metrics.append(MetricsRecord(
+            epoch=epoch, mode_this_epoch=epoch_mode, train_loss=eng.epoch_loss,
+            main_bytes=stats["main_bytes_sent"] - prev["main_bytes_sent"],
+            meta_bytes=stats["metadata_bytes_sent"] - prev["metadata_bytes_sent"],
+            header_bytes=stats["header_bytes_sent"] - prev["header_bytes_sent"],
+            allreduce_bytes=stats["allreduce_bytes"] - prev["allreduce_bytes"],
+            messages=stats["messages_sent"] - prev["messages_sent"], **accs))
+        prev = stats
+        timings.append((time.perf_counter() - t0) * 1000.0)
+    return TrainResult(metrics, eng.weights_host(), timings)

@@ -1,0 +1,304 @@
+"""Halo exchange on device buffers: drop-in for ``halobit.transport``'s
+``exchange`` + ``Fabric`` on the B200.
+
+Reference (``transport.py:90-205``, driven by ``trainer.py:175-223``): for each
+(partition, epoch, layer, phase) the sender gathers its boundary rows per peer,
+quantizes them peer-by-peer (ascending) from one keyed stream, ships one
+message per non-empty peer; the receiver dequantizes and scatters
+(forward: into its halo slots) or accumulates (backward: into its local rows,
+ascending peer order).
+
+B200 design:
+* A rank hosts one or more partitions (one per GPU in production; the
+  single-GPU case hosts all of them, which is exactly the reference's
+  one-process simulation).  Its rows live in HBM as one contiguous
+  ``[local rows of all hosted partitions ; halo rows of all hosted partitions]``
+  matrix per layer, so one SpMM, one GEMM and one K1/K2 launch cover every
+  hosted partition.
+* K1 (``hb_quantize_gather``) gathers, quantizes, packs and writes each
+  message's wire block straight into its destination: the receiver's slot in
+  the local receive buffer (same-rank peer) or the send buffer for the peer
+  rank.  Messages to one rank are contiguous, so one NCCL send/recv pair per
+  peer rank moves them (``torch.distributed`` over NCCL/NVLink, on a side
+  stream).
+* K2 (``hb_dequant_gather``) consumes the receive buffer: forward writes halo
+  rows, backward accumulates into local rows with sources in ascending peer
+  order (f64 sum, one fp32 rounding).
+* Receive buffers are double-buffered by epoch parity for the Sylvie-A
+  pipeline: epoch t consumes parity (t-1)%2 while its fresh sends land in
+  parity t%2 (``trainer.py:232-246``).
+* Byte meters are exact functions of the plan (``transport.py:105-114``):
+  they count what the device actually moves.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .codec import HEADER_BYTES, metadata_bytes, payload_bytes, wire_bytes
+from .rngstream import BACKWARD, FORWARD, derive_key
+
+DEFAULT_TIMEOUT = 60.0
+
+
+class ProtocolError(RuntimeError):
+    pass
+
+
+@dataclass
+class TransportStats:
+    """``transport.py:62-71``."""
+
+    main_bytes_sent: int = 0
+    metadata_bytes_sent: int = 0
+    header_bytes_sent: int = 0
+    messages_sent: int = 0
+    allreduce_bytes: int = 0
+
+    def snapshot(self) -> dict:
+        return dict(self.__dict__)
+
+
+class PoisonableBarrier:
+    """``transport.py:74-87`` (host-side epoch barrier for probes/eval)."""
+
+    def __init__(self, parties: int):
+        self._barrier = threading.Barrier(parties)
+
+    def wait(self, timeout: float = DEFAULT_TIMEOUT):
+        try:
+            self._barrier.wait(timeout)
+        except threading.BrokenBarrierError:
+            raise ProtocolError("barrier poisoned: a worker aborted") from None
+
+    def poison(self):
+        self._barrier.abort()
+
+
+def _align16(n: int) -> int:
+    return (n + 15) & ~15
+
+
+@dataclass
+class _Msg:
+    src: int          # sending partition
+    dst: int          # receiving partition
+    rows: int
+    row_begin: int    # position in the flattened send (or receive) row list
+
+
+class PhasePlan:
+    """Static (layer-independent) index maps of one phase on one rank."""
+
+    def __init__(self, phase, send_msgs, send_rows, recv_msgs, dst_rows, src_ptr, src_rows):
+        self.phase = phase
+        self.send_msgs = send_msgs      # list[_Msg], sorted by (src, dst)
+        self.send_rows = send_rows      # int32 numpy, source row per flattened send row
+        self.recv_msgs = recv_msgs      # list[_Msg], sorted by (src, dst)
+        self.dst_rows = dst_rows        # int32 numpy, K2 destination rows
+        self.src_ptr = src_ptr          # int32 numpy CSR over dst_rows
+        self.src_rows = src_rows        # int32 numpy, flattened receive indices
+        self.dev = None
+
+    def to(self, device):
+        import torch
+
+        def t(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+        self.dev = dict(send_rows=t(self.send_rows), dst_rows=t(self.dst_rows),
+                        src_ptr=t(self.src_ptr), src_rows=t(self.src_rows))
+        return self
+
+
+class RankLayout:
+    """Row layout of the partitions one rank hosts.
+
+    ``owner[p]`` is the rank of partition p; ``parts`` maps hosted partition
+    id → Partition (each with ``send_sets``/``recv_sets`` per peer,
+    ``graph.py:70-100``).
+    """
+
+    def __init__(self, parts: dict, owner, rank: int):
+        self.rank = rank
+        self.owner = list(owner)
+        self.num_partitions = len(self.owner)
+        self.ids = sorted(parts)
+        self.parts = [parts[i] for i in self.ids]
+        self.nl = {p.id: p.num_local for p in self.parts}
+        self.nh = {p.id: p.num_halo for p in self.parts}
+        self.loc_base, self.halo_base = {}, {}
+        a = b = 0
+        for p in self.parts:
+            self.loc_base[p.id], self.halo_base[p.id] = a, b
+            a += p.num_local
+            b += p.num_halo
+        self.NL, self.NH = a, b
+        self.ranks = sorted(set(self.owner))
+        self.fwd = self._phase_plan(FORWARD)
+        self.bwd = self._phase_plan(BACKWARD)
+
+    def _phase_plan(self, phase) -> PhasePlan:
+        fwd = phase == FORWARD
+        send_msgs, send_rows = [], []
+        pos = 0
+        for p in self.parts:
+            for q in range(self.num_partitions):
+                if q == p.id:
+                    continue
+                idx = p.send_sets[q] if fwd else p.recv_sets[q]
+                if len(idx) == 0:
+                    continue
+                send_msgs.append(_Msg(p.id, q, len(idx), pos))
+                pos += len(idx)
+                if fwd:
+                    send_rows.append(self.loc_base[p.id] + np.asarray(idx))
+                else:
+                    send_rows.append(self.NL + self.halo_base[p.id] + np.asarray(idx))
+        # receive side: messages (p -> q) for hosted q, sorted by (p, q)
+        recv = []
+        for q in self.parts:
+            for p in range(self.num_partitions):
+                if p == q.id:
+                    continue
+                idx = q.recv_sets[p] if fwd else q.send_sets[p]
+                if len(idx):
+                    recv.append((p, q.id, np.asarray(idx)))
+        recv.sort(key=lambda m: (m[0], m[1]))
+        recv_msgs, dst, srcp = [], [], []
+        pos = 0
+        for p, qid, idx in recv:
+            recv_msgs.append(_Msg(p, qid, len(idx), pos))
+            if fwd:
+                dst.append(self.NL + self.halo_base[qid] + idx)
+            else:
+                dst.append(self.loc_base[qid] + idx)
+            srcp.append(np.full(len(idx), p, dtype=np.int64))
+            pos += len(idx)
+        cat = (lambda xs: np.concatenate(xs).astype(np.int64)) if recv else \
+            (lambda xs: np.zeros(0, dtype=np.int64))
+        dst_all, src_part = cat(dst), cat(srcp)
+        flat = np.arange(len(dst_all), dtype=np.int64)
+        if fwd:
+            dst_rows, src_ptr, src_rows = dst_all, np.arange(len(dst_all) + 1), flat
+        else:
+            # integrate j[S_k] += recv_k in ascending peer order (trainer.py:214-216):
+            # destination-major CSR, sources sorted by (dst row, peer)
+            o = np.lexsort((src_part, dst_all))
+            d_sorted = dst_all[o]
+            dst_rows, starts = np.unique(d_sorted, return_index=True)
+            src_ptr = np.append(starts, len(d_sorted))
+            src_rows = flat[o]
+        srows = np.concatenate(send_rows).astype(np.int64) if send_rows else np.zeros(0, np.int64)
+        return PhasePlan(phase, send_msgs, srows, recv_msgs, dst_rows, src_ptr, src_rows)
+
+    def to(self, device):
+        self.fwd.to(device)
+        self.bwd.to(device)
+        return self
+
+
+class ExchangeBuffers:
+    """Wire buffers + descriptor tables for one (layer, phase, d, bits)."""
+
+    def __init__(self, layout: RankLayout, plan: PhasePlan, d: int, bits: int, device,
+                 parities: int = 1):
+        import torch
+        self.layout, self.plan, self.d, self.bits = layout, plan, d, bits
+        me = layout.rank
+        size = [_align16(wire_bytes(m.rows, d, bits)) for m in plan.recv_msgs]
+        # receive buffer: groups by source rank, (src, dst) order inside a group
+        self.recv_off, self.recv_group = {}, {}
+        off = 0
+        for r in layout.ranks:
+            g0 = off
+            for m, sz in zip(plan.recv_msgs, size):
+                if layout.owner[m.src] == r:
+                    self.recv_off[(m.src, m.dst)] = off
+                    off += sz
+            if off > g0:
+                self.recv_group[r] = (g0, off - g0)
+        self.recv_bytes = off
+        # send buffer: messages to remote ranks, grouped by destination rank
+        self.send_off, self.send_group = {}, {}
+        off = 0
+        for r in layout.ranks:
+            if r == me:
+                continue
+            g0 = off
+            for m in plan.send_msgs:
+                if layout.owner[m.dst] == r:
+                    self.send_off[(m.src, m.dst)] = off
+                    off += _align16(wire_bytes(m.rows, d, bits))
+            if off > g0:
+                self.send_group[r] = (g0, off - g0)
+        self.send_bytes = off
+        self.recv = [torch.zeros(max(16, self.recv_bytes), dtype=torch.uint8, device=device)
+                     for _ in range(parities)]
+        self.send = torch.zeros(max(16, self.send_bytes), dtype=torch.uint8, device=device)
+        # element offsets of each sender's stream: peers ascending, empty skipped
+        self.elem_off = {}
+        acc = {}
+        for m in plan.send_msgs:
+            self.elem_off[(m.src, m.dst)] = acc.get(m.src, 0)
+            acc[m.src] = acc.get(m.src, 0) + m.rows * d
+        # static receive-side descriptors per parity
+        self.recv_segs = []
+        for par in range(parities):
+            seg = np.zeros(len(plan.recv_msgs), dtype=_lib.SEGMENT_DTYPE)
+            base = self.recv[par].data_ptr()
+            for i, m in enumerate(plan.recv_msgs):
+                seg[i] = (0, 0, 0, base + self.recv_off[(m.src, m.dst)], m.row_begin, m.rows)
+            self.recv_segs.append(torch.from_numpy(seg.view(np.uint8).copy()).to(device))
+        self.n_send = len(plan.send_msgs)
+        self.n_recv = len(plan.recv_msgs)
+
+    def send_table(self, seed: int, epoch: int, layer: int, parity: int) -> np.ndarray:
+        """hb_segment_t rows for this exchange (keys depend on the epoch)."""
+        me = self.layout.rank
+        seg = np.zeros(self.n_send, dtype=_lib.SEGMENT_DTYPE)
+        keys = {}
+        for i, m in enumerate(self.plan.send_msgs):
+            if m.src not in keys:
+                keys[m.src] = derive_key((seed, m.src, epoch, layer, self.plan.phase)) \
+                    if self.bits != 32 else (0, 0)
+            if self.layout.owner[m.dst] == me:
+                out = self.recv[parity].data_ptr() + self.recv_off[(m.src, m.dst)]
+            else:
+                out = self.send.data_ptr() + self.send_off[(m.src, m.dst)]
+            k = keys[m.src]
+            seg[i] = (k[0], k[1], self.elem_off[(m.src, m.dst)], out, m.row_begin, m.rows)
+        return seg
+
+    def stats_delta(self) -> dict:
+        """Per sending partition byte meters of one exchange (transport.py:105-114)."""
+        out = {}
+        for m in self.plan.send_msgs:
+            s = out.setdefault(m.src, [0, 0, 0, 0])
+            s[0] += payload_bytes(m.rows, self.d, self.bits)
+            s[1] += metadata_bytes(m.rows, self.bits)
+            s[2] += HEADER_BYTES
+            s[3] += 1
+        return out
+
+    def wire_bytes_total(self) -> int:
+        return sum(wire_bytes(m.rows, self.d, self.bits) for m in self.plan.send_msgs)
+
+
+def nccl_exchange(bufs: ExchangeBuffers, parity: int, group=None):
+    """Move the remote groups with NCCL send/recv (one pair per peer rank).
+    Called on the comm stream; a no-op on a single rank."""
+    import torch.distributed as dist
+    ops = []
+    for r, (o, n) in bufs.send_group.items():
+        ops.append(dist.P2POp(dist.isend, bufs.send[o:o + n], r, group=group))
+    for r, (o, n) in bufs.recv_group.items():
+        if r == bufs.layout.rank:
+            continue
+        ops.append(dist.P2POp(dist.irecv, bufs.recv[parity][o:o + n], r, group=group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()

@@ -1,0 +1,208 @@
+"""Device training loop vs the CPU oracle / the reference's golden traces.
+
+Tolerances (fp32 device vs f64 reference):
+* passthrough (bits=32) trajectories: per-epoch loss rel 5e-5 (measured fp32
+  drift ~1.2e-6 per epoch), final weights max-abs diff / max-abs weight < 1e-4
+  after 10 epochs (measured ~2.4e-6);
+* byte meters: exact;
+* first exchange of a run (fp32 features on both sides): wire bytes exact;
+* 1-bit training: mean final test accuracy within 0.5 points of the
+  reference's, seeds {1, 2, 3}, BASELINE config 1.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+def _graph(seed=4, npc=25, comms=4, d=32):
+    from paper_2303_01277_b200.datasets import SbmSpec, generate_sbm
+    return generate_sbm(SbmSpec(nodes_per_community=npc, communities=comms, feature_dim=d, seed=seed))
+
+
+def _parts(g, n, model="gcn", strategy="contiguous"):
+    from paper_2303_01277_b200.graph import build_partitions
+    return build_partitions(g, n, strategy, 0, model)[2]
+
+
+def _f32(parts):
+    return [np.asarray(p.features, dtype=np.float32).astype(np.float64) for p in parts]
+
+
+def _run_both(g, n, widths, model, variant, st, bits, epochs, seed, dropout=0.0, strategy="contiguous"):
+    from oracle.epoch import OracleTrainer
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    parts = _parts(g, n, model, strategy)
+    res = train(g, parts, ModelConfig(widths, model, dropout), TrainMode(variant, st),
+                QuantConfig(bits), epochs, seed)
+    o = OracleTrainer(parts, widths, model, variant, st, bits, seed, dropout=dropout,
+                      features=_f32(parts))
+    losses, bytes_ = [], []
+    prev = o.totals()
+    for e in range(1, epochs + 1):
+        o.run_epoch(e)
+        t = o.totals()
+        bytes_.append(tuple(t[k] - prev[k] for k in ("main", "meta", "header", "messages", "allreduce")))
+        prev = t
+        losses.append(o.loss)
+    return res, o, losses, bytes_
+
+
+def _wdiff(a, b):
+    scale = max(np.abs(w).max() for w in b)
+    return max(np.abs(x - y).max() for x, y in zip(a, b)) / scale
+
+
+@pytest.mark.parametrize("model", ["gcn", "sage"])
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_passthrough_trajectory_matches_oracle(model, n):
+    g = _graph()
+    res, o, losses, bytes_ = _run_both(g, n, (32, 16, 4), model, "sync", 0, 32, 10, 2)
+    for m, lo, by in zip(res.metrics, losses, bytes_):
+        assert m.train_loss == pytest.approx(lo, rel=5e-5)
+        assert (m.main_bytes, m.meta_bytes, m.header_bytes, m.messages, m.allreduce_bytes) == by
+    assert _wdiff(res.final_weights, o.weights) < 1e-4
+
+
+@pytest.mark.parametrize("variant,st", [("sync", 0), ("async", 0), ("async", 2), ("async", 3)])
+def test_modes_bytes_and_schedule_match_oracle(variant, st):
+    g = _graph(seed=5, npc=30)
+    res, o, losses, bytes_ = _run_both(g, 3, (32, 16, 8, 4), "sage", variant, st, 32, 6, 3)
+    for m, lo, by in zip(res.metrics, losses, bytes_):
+        assert (m.main_bytes, m.meta_bytes, m.header_bytes, m.messages, m.allreduce_bytes) == by
+        assert m.train_loss == pytest.approx(lo, rel=5e-5)
+    assert _wdiff(res.final_weights, o.weights) < 1e-4
+
+
+def test_dropout_trajectory_matches_oracle():
+    g = _graph(seed=9, npc=20)
+    res, o, losses, _ = _run_both(g, 2, (32, 16, 4), "gcn", "sync", 0, 32, 5, 7, dropout=0.3)
+    for m, lo in zip(res.metrics, losses):
+        assert m.train_loss == pytest.approx(lo, rel=5e-5)
+    assert _wdiff(res.final_weights, o.weights) < 1e-4
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_first_exchange_wire_bytes_exact(bits):
+    """Epoch 1 / layer 1: every message's wire block equals the oracle's."""
+    from oracle.epoch import OracleTrainer
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
+    from paper_2303_01277_b200.transport import RankLayout
+    g = _graph(seed=6, npc=40)
+    parts = _parts(g, 4, "gcn", "hash")
+    lay = RankLayout({p.id: p for p in parts}, [0] * 4, 0)
+    eng = DeviceRank(lay, ModelConfig((32, 16, 4)), TrainMode(), QuantConfig(bits), 11, 0.01,
+                     int(g.train_mask.sum()))
+    eng.run_epoch(1)
+    torch.cuda.synchronize()
+    o = OracleTrainer(parts, (32, 16, 4), "gcn", "sync", 0, bits, 11, features=_f32(parts))
+    o.wire_log = []
+    o.run_epoch(1)
+    want = {(s, d): raw for s, d, e, l, ph, raw in o.wire_log if l == 1 and ph == "forward"}
+    bufs = eng.xf[1]
+    got_all = bufs.recv[0].cpu().numpy().tobytes()
+    assert len(want) == bufs.n_recv > 0
+    for (s, d), raw in want.items():
+        off = bufs.recv_off[(s, d)]
+        assert got_all[off:off + len(raw)] == raw, (s, d)
+
+
+def test_config1_bytes_and_accuracy_vs_reference(traces):
+    """BASELINE config 1 (2-layer GCN 64-32-4, 2 partitions, sync): byte meters
+    identical to the reference every epoch; 1-bit mean final test accuracy
+    within 0.5 points of the reference's over seeds 1-3."""
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.datasets import CONFIG1, generate_sbm
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    g = generate_sbm(CONFIG1)
+    parts = _parts(g, 2)
+    accs = {1: [], 32: []}
+    ref_accs = {1: [], 32: []}
+    for seed in (1, 2, 3):
+        for bits in (1, 32):
+            res = train(g, parts, ModelConfig((64, 32, 4)), TrainMode("sync", 0), QuantConfig(bits),
+                        20, seed)
+            ref = traces[f"config1_seed{seed}_b{bits}"]["metrics"]
+            for m, r in zip(res.metrics, ref):
+                assert (m.main_bytes, m.meta_bytes, m.header_bytes, m.messages, m.allreduce_bytes) == \
+                    (r["main_bytes"], r["meta_bytes"], r["header_bytes"], r["messages"],
+                     r["allreduce_bytes"])
+                if bits == 32:
+                    assert m.train_loss == pytest.approx(r["train_loss"], rel=1e-4)
+            accs[bits].append(res.metrics[-1].test_acc)
+            ref_accs[bits].append(ref[-1]["test_acc"])
+    for bits in (1, 32):
+        assert abs(np.mean(accs[bits]) - np.mean(ref_accs[bits])) <= 0.005, (bits, accs, ref_accs)
+
+
+def test_async_epoch_one_zero_halo_and_tags():
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    g = _graph(seed=12, npc=15)
+    parts = _parts(g, 4)
+    consumed = []
+
+    def probe(event, **kw):
+        if event == "halo_consumed":
+            consumed.append(kw)
+    train(g, parts, ModelConfig((32, 8, 4)), TrainMode("async", 0), QuantConfig(1), 5, 10, probe=probe)
+    assert consumed
+    for e in consumed:
+        if e["epoch"] == 1:
+            assert e["tag"] == 0
+            np.testing.assert_array_equal(e["data"], 0.0)
+        else:
+            assert e["tag"] == e["epoch"] - 1
+
+
+def test_unit_staleness_collapses_to_sync():
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    g = _graph(seed=11, npc=15)
+    parts = _parts(g, 4)
+    a = train(g, parts, ModelConfig((32, 8, 4)), TrainMode("sync", 0), QuantConfig(32), 8, 9)
+    b = train(g, parts, ModelConfig((32, 8, 4)), TrainMode("async", 1), QuantConfig(32), 8, 9)
+    assert _wdiff(b.final_weights, a.final_weights) == 0.0
+    c = train(g, parts, ModelConfig((32, 8, 4)), TrainMode("async", 2), QuantConfig(1), 6, 11)
+    assert [m.mode_this_epoch for m in c.metrics] == ["async", "sync"] * 3
+
+
+def test_replay_bit_identical():
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    g = _graph(seed=13, npc=20)
+    parts = _parts(g, 3)
+    r1 = train(g, parts, ModelConfig((32, 8, 4), dropout=0.2), TrainMode("async", 2), QuantConfig(2), 4, 7)
+    r2 = train(g, parts, ModelConfig((32, 8, 4), dropout=0.2), TrainMode("async", 2), QuantConfig(2), 4, 7)
+    assert _wdiff(r1.final_weights, r2.final_weights) == 0.0
+    assert [m.train_loss for m in r1.metrics] == [m.train_loss for m in r2.metrics]
+
+
+def test_nan_feature_aborts():
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, TrainingError, train
+    g = _graph(seed=7, npc=10)
+    g.features[0, 0] = np.nan
+    parts = _parts(g, 2)
+    with pytest.raises(TrainingError, match="aborted"):
+        train(g, parts, ModelConfig((32, 8, 2)), TrainMode(), QuantConfig(1), 3, 5)
+
+
+def test_zero_epochs_and_empty_mask():
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, init_weights, train
+    g = _graph(seed=3, npc=10)
+    parts = _parts(g, 2)
+    res = train(g, parts, ModelConfig((32, 8, 2)), TrainMode(), QuantConfig(1), 0, 1)
+    assert res.metrics == []
+    assert _wdiff(res.final_weights, init_weights(ModelConfig((32, 8, 2)), 1)) == 0.0
