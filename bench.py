@@ -1,0 +1,338 @@
+"""Benchmark: full-graph epoch time of the Sylvie halo path on B200.
+
+Workload (BASELINE.json configs[1]): 3-layer GraphSAGE (602-256-256-41) on a
+Reddit-shaped synthetic planted-partition graph (232,965 nodes, 114,615,892
+directed edges, 41 classes), 8 partitions (contiguous), 1-bit halos, Sylvie-S
+(sync).  The 8 partitions are spread over the N GPUs (N=1: all 8 on one GPU —
+the reference's one-process simulation with device-resident halo traffic;
+N=8: one subgraph per GPU, halos over NVLink via NCCL).  Total work is fixed
+as N grows ("strong" scaling).
+
+A "step" is one training epoch (forward + loss + backward + gradient
+all-reduce + Adam), the centralized evaluation excluded.
+
+  python bench.py [--gpus N --steps K --warmup W]          # B200 arm
+  python bench.py --impl reference [--steps K --warmup W]  # CPU oracle arm
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (300, 512, 512, 512, 100)}
+MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn"}
+PARTITIONS = 8
+CPU_SAMPLE_SCALE = 0.125       # the CPU oracle runs the same shape at 1/8 of the nodes/edges
+
+
+def _spec(name: str, scale: float = 1.0):
+    from paper_2303_01277_b200 import datasets as ds
+    spec = {"reddit": ds.REDDIT, "ogbn": ds.OGBN_PRODUCTS, "yelp": ds.YELP}[name]
+    return spec if scale == 1.0 else ds.scaled(spec, scale)
+
+
+def build_graph(name: str, scale: float = 1.0, parts_needed=None):
+    from paper_2303_01277_b200.datasets import generate_planted
+    from paper_2303_01277_b200.graph import build_partition, mean_adjacency, normalize_adjacency, \
+        partition_nodes
+    g = generate_planted(_spec(name, scale))
+    a = normalize_adjacency(g)
+    m = mean_adjacency(g) if MODEL[name] == "sage" else None
+    plan = partition_nodes(g, PARTITIONS)
+    ids = range(PARTITIONS) if parts_needed is None else parts_needed
+    return g, {k: build_partition(g, a, plan, k, m) for k in ids}
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm_gbs=float(d["hbm_gbs"]), bf16_tflops=float(d["bf16_tflops"]), source="measured")
+    return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, source="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def result(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9 and f[1].isdigit():
+                    rows.append(f)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        sm = [int(r[1]) for r in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
+
+
+def cpu_epoch_sample(name: str, threads: int, epochs: int = 1, warmup: int = 0):
+    """Oracle epochs on the same-shape graph at CPU_SAMPLE_SCALE; returns
+    (seconds per full-scale epoch, sample description, cores)."""
+    from oracle.epoch import OracleTrainer
+    g, parts = build_graph(name, CPU_SAMPLE_SCALE)
+    o = OracleTrainer([parts[k] for k in sorted(parts)], WIDTHS[name], MODEL[name], "sync", 0, 1, 0,
+                      threads=threads)
+    for e in range(1, warmup + 1):
+        o.run_epoch(e)
+    times = []
+    for e in range(warmup + 1, warmup + epochs + 1):
+        t0 = time.perf_counter()
+        o.run_epoch(e)
+        times.append(time.perf_counter() - t0)
+    nnz = sum(p.mean_block.nnz if p.mean_block is not None else p.adj_block.nnz for p in parts.values())
+    per = statistics.mean(times) / CPU_SAMPLE_SCALE
+    sample = (f"{epochs} oracle epoch(s) (numpy/scipy f64, {threads} worker threads) of the {name}-shaped "
+              f"graph at {CPU_SAMPLE_SCALE:g} scale ({g.num_nodes} nodes, {len(g.edges)} edges, "
+              f"{nnz} aggregation nnz, same widths/partitions/cut), time x {1 / CPU_SAMPLE_SCALE:g}")
+    return per, sample, times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    per, sample, times = cpu_epoch_sample(args.config, threads, epochs=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": "full-graph epoch time", "value": per, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args),
+        "cpu_baseline": {"value": per, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": per, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args) -> dict:
+    spec = _spec(args.config)
+    return {"workload": f"{args.config}-shaped {len(WIDTHS[args.config]) - 1}-layer "
+                        f"{MODEL[args.config].upper()} {'-'.join(map(str, WIDTHS[args.config]))}, "
+                        f"{PARTITIONS} partitions over {args.gpus} GPU(s), {args.bits}-bit halos, "
+                        f"Sylvie-{'S' if args.mode == 'sync' else 'A'}",
+            "nodes": spec.num_nodes, "edges": spec.num_edges, "partitions": PARTITIONS,
+            "bits": args.bits, "mode": args.mode, "staleness": args.staleness,
+            "model": MODEL[args.config], "widths": list(WIDTHS[args.config]),
+            "l2": "inputs larger than L2 (features 561 MB, aggregation CSR 0.9 GB)"}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.profiling import KernelTimer
+    from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
+    from paper_2303_01277_b200.transport import RankLayout
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    owner = [p * world // PARTITIONS for p in range(PARTITIONS)]
+    mine = [p for p in range(PARTITIONS) if owner[p] == rank]
+    t0 = time.perf_counter()
+    g, parts = build_graph(args.config, 1.0, mine)
+    gnorm = int(g.train_mask.sum())
+    layout = RankLayout(parts, owner, rank)
+    eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config]),
+                     TrainMode(args.mode, args.staleness), QuantConfig(args.bits), args.seed, 0.01, gnorm,
+                     device=torch.device("cuda", local))
+    feats_host = torch.from_numpy(np.concatenate([np.asarray(p.features, dtype=np.float32)
+                                                  for p in layout.parts])).pin_memory()
+    del g
+    setup_s = time.perf_counter() - t0
+    epoch = 0
+    for _ in range(args.warmup):
+        epoch += 1
+        eng.run_epoch(epoch)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-timed region: K epochs, no host syncs inside ------------------
+    timer = KernelTimer()
+    eng.timer = timer
+    launches0 = eng.launches
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            epoch += 1
+            eng.run_epoch(epoch, check=False)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = eng.launches - launches0
+    eng.timer = KernelTimer()
+    eng.timer.enabled = False
+    eng.check_epoch(epoch)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ksum = timer.summary()
+    clocks = clk.result()
+
+    # ---- end-to-end through the public epoch call with host buffers ----------
+    h2d = int(feats_host.numel() * 4)
+    e2e_times = []
+    for _ in range(max(1, args.steps // 2)):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        epoch += 1
+        eng.Ht[1][:eng.NL, :WIDTHS[args.config][0]].copy_(feats_host, non_blocking=True)
+        eng.run_epoch(epoch, check=True)            # reads loss + codec flag back (D2H)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+
+    if rank == 0:
+        peaks = load_peaks()
+        dom = max(ksum, key=lambda k: ksum[k]["ms"]) if ksum else None
+        roof = None
+        if "spmm" in ksum:
+            s = ksum["spmm"]
+            traffic = _ncu_traffic("spmm")
+            roof = {"kernel": "hb_spmm_csr (K3/K4)", "bound": "hbm",
+                    "achieved": s["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": traffic,
+                    "algorithmic_bytes_per_launch": s["bytes"] / s["launches"],
+                    "avg_launch_ms": s["ms"] / s["launches"], "peak_source": peaks["source"],
+                    "fp32_simt_tflops": s["tflops"]}
+        wire = sum(b.wire_bytes_total() for b in list(eng.xf.values()) + list(eng.xb.values()))
+        halo_ms = sum(ksum.get(k, {}).get("ms", 0.0) for k in ("quantize_gather", "dequant_gather"))
+        line = {
+            "metric": "full-graph epoch time", "value": ms / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (planted-partition reddit-shaped graph, random-init Glorot weights)",
+            "config": workload_config(args),
+            "roofline": roof,
+            "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                        for k, v in ksum.items()},
+            "dominant_kernel": dom,
+            "halo": {"wire_bytes_per_epoch": wire,
+                     "k1_k2_ms_per_epoch": halo_ms / args.steps,
+                     "fp32_equiv_bytes_per_epoch": _fp32_equiv(eng),
+                     "note": "N=1: the 8 partitions share one GPU, so halo messages move HBM->HBM; "
+                             "K1 writes each wire block straight into its receiver's buffer"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": {"value": float(e2e.item()), "unit": "s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 12},
+            "setup_s": round(setup_s, 1),
+            "final_loss": eng.epoch_loss,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            per, sample, _ = cpu_epoch_sample(args.config, threads)
+            line["cpu_baseline"] = {"value": per, "unit": "s", "cores": threads, "kind": "port",
+                                    "sample": sample}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _fp32_equiv(eng) -> int:
+    tot = 0
+    for b in list(eng.xf.values()) + list(eng.xb.values()):
+        tot += int(b.plan.send_rows.size) * b.d * 4
+    return tot
+
+
+def _ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="reddit", choices=sorted(WIDTHS))
+    ap.add_argument("--bits", type=int, default=1)
+    ap.add_argument("--mode", default="sync", choices=["sync", "async"])
+    ap.add_argument("--staleness", type=int, default=0)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

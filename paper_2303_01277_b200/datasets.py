@@ -20,6 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._np import setdiff_sorted, sorted_unique
 from .graph import Graph
 from .rngstream import keyed_generator
 
@@ -95,43 +96,71 @@ class PlantedSpec:
             raise DatasetError("bad planted-partition spec")
 
 
+def _tri_decode(t: np.ndarray):
+    """Index t of the strict lower triangle (row-major) -> (a, b), a > b."""
+    a = ((1.0 + np.sqrt(1.0 + 8.0 * t.astype(np.float64))) // 2).astype(np.int64)
+    a -= (a * (a - 1) // 2 > t)           # guard float rounding at the boundaries
+    a += ((a + 1) * a // 2 <= t)
+    return a, t - a * (a - 1) // 2
+
+
 def generate_planted(spec: PlantedSpec) -> Graph:
+    """O(E) planted-partition graph.  Intra-community edges are sampled without
+    replacement from each community's pair set (so there are no duplicates to
+    discard); cut edges join uniform node pairs; the union is deduplicated once."""
     n = spec.num_nodes
     C = spec.communities or spec.num_classes
     bounds = np.linspace(0, n, C + 1).astype(np.int64)
-    comm = np.repeat(np.arange(C), np.diff(bounds))
+    sizes = np.diff(bounds)
+    comm = np.repeat(np.arange(C), sizes)
     target_und = spec.num_edges // 2
+    n_cut = int(round(target_und * spec.cut))
+    n_intra = target_und - n_cut
+    pairs = sizes * (sizes - 1) // 2
+    if n_intra > pairs.sum():
+        raise DatasetError("communities too small for the requested intra-community degree")
+    share = n_intra * pairs / max(1, pairs.sum())
+    k = np.floor(share).astype(np.int64)
+    k[np.argsort(-(share - k))[: n_intra - k.sum()]] += 1
     rng = keyed_generator(spec.seed, "planted-edges")
-    keys = np.empty(0, dtype=np.int64)
-    over = 1.03
-    while len(keys) < target_und:
-        need = int((target_und - len(keys)) * over) + 1024
-        src = rng.integers(0, n, size=need, dtype=np.int64)
-        intra = rng.random(need) >= spec.cut
-        c = comm[src]
-        lo, sz = bounds[c], bounds[c + 1] - bounds[c]
-        dst = np.where(intra, lo + (rng.random(need) * sz).astype(np.int64),
-                       rng.integers(0, n, size=need, dtype=np.int64))
-        ok = src != dst
-        a, b = np.minimum(src[ok], dst[ok]), np.maximum(src[ok], dst[ok])
-        keys = np.unique(np.concatenate([keys, a * n + b]))
-        over *= 1.5
-    if len(keys) > target_und:
-        keys = np.sort(rng.choice(keys, size=target_und, replace=False))
-    a, b = keys // n, keys % n
-    both = np.concatenate([a * n + b, b * n + a])
+    keys = []
+    for c in range(C):
+        if k[c] == 0:
+            continue
+        t = rng.choice(pairs[c], size=k[c], replace=False)
+        a, b = _tri_decode(t)
+        keys.append((bounds[c] + b) * n + (bounds[c] + a))      # (min, max) pair key
+    intra = np.concatenate(keys) if keys else np.empty(0, dtype=np.int64)
+    und = np.sort(intra)              # distinct by construction (disjoint communities)
+    cut_keys = np.empty(0, dtype=np.int64)
+    while len(cut_keys) < n_cut:
+        need = n_cut - len(cut_keys)
+        u = rng.integers(0, n, size=int(need * 1.05) + 16, dtype=np.int64)
+        v = rng.integers(0, n, size=len(u), dtype=np.int64)
+        ok = u != v
+        ck = sorted_unique(np.minimum(u[ok], v[ok]) * n + np.maximum(u[ok], v[ok]))
+        ck = setdiff_sorted(setdiff_sorted(ck, und), cut_keys)
+        if len(ck) > need:
+            ck = np.sort(rng.choice(ck, size=need, replace=False))
+        cut_keys = np.sort(np.concatenate([cut_keys, ck]))
+    und = np.sort(np.concatenate([und, cut_keys]))
+    lo, hi = und // n, und % n
+    both = np.concatenate([lo * n + hi, hi * n + lo])
     both.sort()
-    edges = np.stack([both // n, both % n], axis=1)
+    edges = np.empty((len(both), 2), dtype=np.int64)
+    np.floor_divide(both, n, out=edges[:, 0])
+    np.remainder(both, n, out=edges[:, 1])
+    del both
     labels = comm % spec.num_classes
     d = spec.feature_dim
     frng = keyed_generator(spec.seed, "planted-features")
     feats = frng.standard_normal((n, d), dtype=np.float32)
     feats *= np.float32(spec.feature_noise)
-    cols = np.arange(d)
+    cls_of_col = np.arange(d) % spec.num_classes
     # tiled one-hot: column j carries the signal of class j % num_classes
-    for start in range(0, n, 1 << 16):
-        blk = slice(start, min(n, start + (1 << 16)))
-        feats[blk] += (labels[blk, None] == (cols[None, :] % spec.num_classes)).astype(np.float32)
+    for start in range(0, n, 1 << 15):
+        blk = slice(start, min(n, start + (1 << 15)))
+        feats[blk] += labels[blk, None] == cls_of_col[None, :]
     perm = keyed_generator(spec.seed, "planted-masks").permutation(n)
     tr, va, te = _split_masks(n, perm, (spec.train_frac, spec.val_frac))
     return Graph(num_nodes=n, edges=edges, features=feats, labels=labels.astype(np.int64),

@@ -23,6 +23,7 @@ import numpy as np
 import scipy.sparse as sp
 from scipy.sparse import csgraph
 
+from ._np import sorted_unique
 from .linalg import CsrMatrix
 
 STRATEGIES = ("contiguous", "bfs_blocks", "hash")
@@ -117,8 +118,11 @@ def clean_edges(g: Graph) -> np.ndarray:
     e = np.asarray(g.edges, dtype=np.int64).reshape(-1, 2)
     if e.size == 0:
         return e.reshape(0, 2)
+    key = e[:, 0] * np.int64(g.num_nodes) + e[:, 1]
+    if len(key) > 1 and np.all(key[1:] > key[:-1]) and not np.any(e[:, 0] == e[:, 1]):
+        return e  # already sorted, unique and loop-free (the generators emit this form)
     e = e[e[:, 0] != e[:, 1]]
-    key = np.unique(e[:, 0] * np.int64(g.num_nodes) + e[:, 1])
+    key = sorted_unique(e[:, 0] * np.int64(g.num_nodes) + e[:, 1])
     return np.stack([key // g.num_nodes, key % g.num_nodes], axis=1)
 
 
@@ -136,20 +140,28 @@ def normalize_adjacency(g: Graph, degree_with_self_loops: bool = True) -> CsrMat
     diagonal scalings produce."""
     a = _adjacency_csr(g)
     n = g.num_nodes
-    deg = np.diff(a.indptr).astype(np.float64)
+    cnt = np.diff(a.indptr)
+    deg = cnt.astype(np.float64)
     if degree_with_self_loops:
         deg = deg + 1.0
     deg[deg == 0] = 1.0
     dinv = 1.0 / np.sqrt(deg)
-    # insert the diagonal into every row, keeping columns sorted
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(a.indptr))
+    # insert the diagonal into every (column-sorted) row in O(nnz)
+    rows = np.repeat(np.arange(n, dtype=np.int64), cnt)
     cols = a.indices.astype(np.int64)
-    key = np.concatenate([rows * n + cols, np.arange(n, dtype=np.int64) * (n + 1)])
-    key.sort()
-    r, c = key // n, key % n
-    rp = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.bincount(r, minlength=n), out=rp[1:])
-    return CsrMatrix(n, n, rp, c, dinv[r] * dinv[c], validate=False)
+    after = cols > rows
+    pos = np.arange(len(cols), dtype=np.int64) + rows + after
+    below = np.bincount(rows, weights=~after, minlength=n).astype(np.int64)
+    dpos = a.indptr[:-1].astype(np.int64) + np.arange(n, dtype=np.int64) + below
+    nnz = len(cols) + n
+    ci = np.empty(nnz, dtype=np.int64)
+    v = np.empty(nnz, dtype=np.float64)
+    ci[pos] = cols
+    v[pos] = dinv[rows] * dinv[cols]
+    ci[dpos] = np.arange(n)
+    v[dpos] = dinv * dinv
+    rp = a.indptr.astype(np.int64) + np.arange(n + 1, dtype=np.int64)
+    return CsrMatrix(n, n, rp, ci, v, validate=False)
 
 
 def mean_adjacency(g: Graph) -> CsrMatrix:
@@ -232,39 +244,76 @@ def build_partition(g: Graph, a_hat: CsrMatrix, plan: PartitionPlan, n: int,
     """
     local = np.sort(plan.nodes_of(n))
     owner = plan.assignment
-    r, c, v = _row_slice(a_hat, local)
-    is_local = owner[c] == n
-    halo = np.unique(c[~is_local])
-    col_map = np.full(g.num_nodes, -1, dtype=np.int64)
-    col_map[local] = np.arange(len(local))
-    col_map[halo] = len(local) + np.arange(len(halo))
-    ncols = len(local) + len(halo)
+    nl = len(local)
+    contiguous = nl > 0 and local[-1] - local[0] + 1 == nl
+    if contiguous:
+        lo = int(local[0])
+        k0, k1 = int(a_hat.row_ptr[lo]), int(a_hat.row_ptr[lo + nl])
+        rp_loc = a_hat.row_ptr[lo:lo + nl + 1] - k0
+        r = np.repeat(np.arange(nl, dtype=np.int64), np.diff(rp_loc))
+        c, v = a_hat.col_idx[k0:k1], a_hat.values[k0:k1]
+        is_local = (c >= lo) & (c < lo + nl)
+    else:
+        r, c, v = _row_slice(a_hat, local)
+        is_local = owner[c] == n
+    halo = sorted_unique(c[~is_local])
+    ncols = nl + len(halo)
 
-    def block(rr, cc, vv):
-        newc = col_map[cc]
-        key = rr * ncols + newc
-        o = np.argsort(key, kind="stable")
-        rp = np.zeros(len(local) + 1, dtype=np.int64)
-        np.cumsum(np.bincount(rr, minlength=len(local)), out=rp[1:])
-        return CsrMatrix(len(local), ncols, rp, newc[o], vv[o], validate=False)
+    def block(rr, cc, vv, loc):
+        """Columns local-first then halo, each sorted by global id: within a
+        row of a column-sorted matrix that is a stable local/halo partition."""
+        if contiguous:
+            newc = np.where(loc, cc - lo, nl + np.searchsorted(halo, cc))
+        else:
+            cmap = np.full(g.num_nodes, -1, dtype=np.int64)
+            cmap[local] = np.arange(nl)
+            cmap[halo] = nl + np.arange(len(halo))
+            newc = cmap[cc]
+        cnt = np.bincount(rr, minlength=nl)
+        rp = np.zeros(nl + 1, dtype=np.int64)
+        np.cumsum(cnt, out=rp[1:])
+        nloc = np.bincount(rr, weights=loc, minlength=nl).astype(np.int64)
+        cl = np.cumsum(loc) - loc                       # locals before this entry (global)
+        ch = np.cumsum(~loc) - (~loc)                   # halos before this entry (global)
+        start = rp[:-1][rr]
+        cl0 = np.concatenate([[0], np.cumsum(nloc)])[rr]
+        ch0 = (rp[:-1] - np.concatenate([[0], np.cumsum(nloc)[:-1]]))[rr]
+        pos = np.where(loc, start + (cl - cl0), start + nloc[rr] + (ch - ch0))
+        ci = np.empty(len(cc), dtype=np.int64)
+        vo = np.empty(len(cc), dtype=np.float64)
+        ci[pos] = newc
+        vo[pos] = vv
+        return CsrMatrix(nl, ncols, rp, ci, vo, validate=False)
 
-    adj_block = block(r, c, v)
+    adj_block = block(r, c, v, is_local)
     mean_block = None
     if mean_hat is not None:
-        mr, mc, mv = _row_slice(mean_hat, local)
-        keep = col_map[mc] >= 0
-        mean_block = block(mr[keep], mc[keep], mv[keep])
+        if contiguous:
+            m0, m1 = int(mean_hat.row_ptr[lo]), int(mean_hat.row_ptr[lo + nl])
+            mrp = mean_hat.row_ptr[lo:lo + nl + 1] - m0
+            mr = np.repeat(np.arange(nl, dtype=np.int64), np.diff(mrp))
+            mc, mv = mean_hat.col_idx[m0:m1], mean_hat.values[m0:m1]
+            mloc = (mc >= lo) & (mc < lo + nl)
+        else:
+            mr, mc, mv = _row_slice(mean_hat, local)
+            mloc = owner[mc] == n
+        mean_block = block(mr, mc, mv, mloc)
 
     recv_sets, send_sets = [], []
     halo_owner = owner[halo]
-    c_owner = owner[c]
+    # S_k: local rows with >= 1 neighbour owned by k (graph.py:238-247), from the
+    # halo entries only: unique (owner, row) keys, already ordered by row per owner
+    hr, hc = r[~is_local], c[~is_local]
+    keys = sorted_unique(owner[hc] * np.int64(max(nl, 1)) + hr)
+    kown, krow = keys // max(nl, 1), keys % max(nl, 1)
+    bounds = np.searchsorted(kown, np.arange(plan.num_partitions + 1))
     for k in range(plan.num_partitions):
         if k == n:
             recv_sets.append(np.empty(0, dtype=np.int64))
             send_sets.append(np.empty(0, dtype=np.int64))
             continue
         recv_sets.append(np.flatnonzero(halo_owner == k).astype(np.int64))
-        send_sets.append(np.unique(r[c_owner == k]).astype(np.int64))
+        send_sets.append(krow[bounds[k]:bounds[k + 1]].astype(np.int64))
 
     return Partition(
         id=n, num_partitions=plan.num_partitions, local_nodes=local, halo_nodes=halo,

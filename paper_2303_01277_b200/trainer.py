@@ -30,6 +30,7 @@ import numpy as np
 from . import ops
 from .codec import CodecError, QuantConfig, quantize_gather, dequant_gather
 from .graph import Graph, Partition
+from .profiling import null_timer
 from .rngstream import BACKWARD, FORWARD, derive_key, keyed_generator
 from .transport import ExchangeBuffers, ProtocolError, RankLayout, TransportStats, nccl_exchange
 
@@ -146,6 +147,25 @@ def _transpose(rows, cols, rp, ci, v):
     return trp, r[o], v[o]
 
 
+def _transpose_device(a: "ops.DeviceCsr") -> "ops.DeviceCsr":
+    """CSR of A^T built on the device (stable by row, so each row of A^T keeps
+    ascending columns) — the reference precomputes the same transpose on the
+    host (trainer.py:164-165)."""
+    import torch
+    dev = a.row_ptr.device
+    counts = a.row_ptr[1:] - a.row_ptr[:-1]
+    rows = torch.repeat_interleave(torch.arange(a.rows, device=dev, dtype=torch.int32), counts)
+    order = torch.sort(a.col_idx.long(), stable=True).indices
+    t = ops.DeviceCsr.__new__(ops.DeviceCsr)
+    t.rows, t.cols, t.nnz = a.cols, a.rows, a.nnz
+    t.col_idx = rows[order].contiguous()
+    t.values = a.values[order].contiguous()
+    rp = torch.zeros(a.cols + 1, dtype=torch.int64, device=dev)
+    rp[1:] = torch.cumsum(torch.bincount(a.col_idx.long(), minlength=a.cols), 0)
+    t.row_ptr = rp
+    return t
+
+
 class DeviceRank:
     """One rank's share of the training: buffers, exchanges, epoch loop."""
 
@@ -173,8 +193,7 @@ class DeviceRank:
         which = "mean" if cfg.model == "sage" else "adj"
         rp, ci, v = _stack_csr(layout, which)
         self.A = ops.DeviceCsr(NL, NL + NH, rp, ci, v, dev)
-        trp, tci, tv = _transpose(NL, NL + NH, rp, ci, v)
-        self.At = ops.DeviceCsr(NL + NH, NL, trp, tci, tv, dev)
+        self.At = _transpose_device(self.A)
         # activations: Ht[l] = [local ; halo] input of layer l (ld padded to 16 B)
         self.Ht = {l: torch.zeros((NL + NH, _ld(W[l - 1])), dtype=f32, device=dev)
                    for l in range(1, L + 1)}
@@ -229,6 +248,7 @@ class DeviceRank:
         self.epoch_loss = 0.0
         self.comm_stream = torch.cuda.Stream(device=dev) if self.world > 1 else None
         self.launches = 0
+        self.timer = null_timer
 
     # -- exchange helpers -----------------------------------------------------
     def _count(self, bufs: ExchangeBuffers):
@@ -246,8 +266,11 @@ class DeviceRank:
             tab = bufs.send_table(self.seed, epoch, layer, parity)
             segs = torch.from_numpy(tab.view(np.uint8).copy()).to(self.dev, non_blocking=False)
             bufs._segs_keepalive = segs
-            quantize_gather(src, bufs.plan.dev["send_rows"], segs, bufs.n_send, bufs.d, bufs.bits,
-                            self.flags)
+            R = int(bufs.plan.send_rows.size)
+            nbytes = R * bufs.d * 4 + R * 4 + bufs.wire_bytes_total()
+            with self.timer("quantize_gather", nbytes):
+                quantize_gather(src, bufs.plan.dev["send_rows"], segs, bufs.n_send, bufs.d,
+                                bufs.bits, self.flags)
             self.launches += 1
             if self.probe:
                 self._probe_out(bufs, epoch, layer)
@@ -265,8 +288,11 @@ class DeviceRank:
         if bufs.n_recv == 0:
             return
         pd = bufs.plan.dev
-        dequant_gather(bufs.recv_segs[parity], bufs.n_recv, pd["dst_rows"], pd["src_ptr"],
-                       pd["src_rows"], bufs.d, bufs.bits, dst, accumulate)
+        nd, ns = int(bufs.plan.dst_rows.size), int(bufs.plan.src_rows.size)
+        nbytes = bufs.wire_bytes_total() + nd * bufs.d * 4 * (2 if accumulate else 1) + 4 * (2 * nd + ns)
+        with self.timer("dequant_gather", nbytes):
+            dequant_gather(bufs.recv_segs[parity], bufs.n_recv, pd["dst_rows"], pd["src_ptr"],
+                           pd["src_rows"], bufs.d, bufs.bits, dst, accumulate)
         self.launches += 1
 
     def _probe_out(self, bufs, epoch, layer):
@@ -341,16 +367,19 @@ class DeviceRank:
                 Hd = self.Hd[l]
                 self._dropout(H, Hd, epoch, l, d)
             agg = self.AGG[l]
-            ops.spmm(self.A, Hd, agg, d)
+            with self.timer("spmm", *_spmm_cost(self.A, d)):
+                ops.spmm(self.A, Hd, agg, d)
             self.launches += 1
             Z = self.Z[l]
-            if self.cfg.model == "sage":
-                torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
-                Z.addmm_(agg[:, :d], self.W[l - 1][d:])
-            else:
-                torch.mm(agg[:, :d], self.W[l - 1], out=Z)
+            with self.timer("gemm", 0, 2 * NL * self.W[l - 1].shape[0] * W[l]):
+                if self.cfg.model == "sage":
+                    torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
+                    Z.addmm_(agg[:, :d], self.W[l - 1][d:])
+                else:
+                    torch.mm(agg[:, :d], self.W[l - 1], out=Z)
             if l < L:
-                ops.relu(Z, self.Ht[l + 1], NL, W[l])
+                with self.timer("elementwise", 8 * NL * W[l]):
+                    ops.relu(Z, self.Ht[l + 1], NL, W[l])
                 self.launches += 1
         return self.Z[L]
 
@@ -374,28 +403,30 @@ class DeviceRank:
         for l in range(L, 0, -1):
             d, dout = W[l - 1], W[l]
             if l < L:
-                ops.relu_grad_mul(J, self.Ht[l + 1], J, NL, dout)
+                with self.timer("elementwise", 12 * NL * dout):
+                    ops.relu_grad_mul(J, self.Ht[l + 1], J, NL, dout)
                 self.launches += 1
             m = J[:, :dout]
             Hd = self.Hd[l] if self.drop else self.Ht[l]
             agg = self.AGG[l]
             G = self.G[l - 1]
-            if self.cfg.model == "sage":
-                torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
-                torch.mm(agg[:, :d].t(), m, out=G[d:])
-            else:
-                torch.mm(agg[:, :d].t(), m, out=G)
+            with self.timer("gemm", 0, 2 * NL * G.shape[0] * dout):
+                if self.cfg.model == "sage":
+                    torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
+                    torch.mm(agg[:, :d].t(), m, out=G[d:])
+                else:
+                    torch.mm(agg[:, :d].t(), m, out=G)
             if l == 1:
                 break
             T, JF = self.T[l], self.JF[l]
             Wl = self.W[l - 1]
+            with self.timer("gemm", 0, 2 * NL * d * dout):
+                torch.mm(m, (Wl[d:] if self.cfg.model == "sage" else Wl).t(), out=T)
+            with self.timer("spmm", *_spmm_cost(self.At, d)):
+                ops.spmm(self.At, T, JF, d)
             if self.cfg.model == "sage":
-                torch.mm(m, Wl[d:].t(), out=T)
-                ops.spmm(self.At, T, JF, d)
-                JF[:NL, :d].addmm_(m, Wl[:d].t())
-            else:
-                torch.mm(m, Wl.t(), out=T)
-                ops.spmm(self.At, T, JF, d)
+                with self.timer("gemm", 0, 2 * NL * d * dout):
+                    JF[:NL, :d].addmm_(m, Wl[:d].t())
             self.launches += 1
             if self.drop:
                 self._dropout(JF, JF, epoch, l, d)
@@ -478,6 +509,13 @@ class DeviceRank:
             t.messages_sent += s.messages_sent
             t.allreduce_bytes += s.allreduce_bytes
         return t.snapshot()
+
+
+def _spmm_cost(a, d: int):
+    """(compulsory HBM bytes, flops) of one SpMM launch: CSR arrays + every X
+    row read once + Y written once; 2 flops per nonzero per column."""
+    nbytes = 8 * (a.rows + 1) + 8 * a.nnz + 4 * a.cols * d + 4 * a.rows * d
+    return nbytes, 2 * a.nnz * d
 
 
 def _dist_initialized() -> bool:

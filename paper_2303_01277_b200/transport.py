@@ -39,6 +39,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._np import sorted_unique_index
 from .codec import HEADER_BYTES, metadata_bytes, payload_bytes, wire_bytes
 from .rngstream import BACKWARD, FORWARD, derive_key
 
@@ -189,7 +190,7 @@ class RankLayout:
             # destination-major CSR, sources sorted by (dst row, peer)
             o = np.lexsort((src_part, dst_all))
             d_sorted = dst_all[o]
-            dst_rows, starts = np.unique(d_sorted, return_index=True)
+            dst_rows, starts = sorted_unique_index(d_sorted)
             src_ptr = np.append(starts, len(d_sorted))
             src_rows = flat[o]
         srows = np.concatenate(send_rows).astype(np.int64) if send_rows else np.zeros(0, np.int64)
