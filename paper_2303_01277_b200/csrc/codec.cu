@@ -23,6 +23,7 @@
 //    any row alignment), then written to the wire block with coalesced stores.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -30,50 +31,75 @@ namespace hb {
 
 constexpr int kQWarps = 8;                 // warps per CTA in K1/K2
 constexpr int kMaxSmemSegs = 128;          // segment table cached in smem
-constexpr int kMaxChunks = 9;              // d <= 9*128 - 3 keeps the row in registers
-constexpr int kRowBufWords = 2 + (kMaxChunks * 128 * 16) / 32 + 4;  // b <= 16, 64-bit lead
+constexpr int kK1SmallWords = 320;         // per-warp row image: pow2 b<=8 up to d=1149, b=16 up to d~600
+constexpr int kK1LargeWords = 1160;        // b <= 16 up to d = 2300
+
+__device__ __forceinline__ int find_segment_smem(const int32_t* begin, int nseg, int row) {
+  int lo = 0, hi = nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (begin[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
 struct QuantRowCtx {
-  float mn, s, inv_s, E;
+  float mn, s, inv_s, E, Eu;
   int B, bits;
   bool live, fast;
 };
 
-// Exact fp64 reference decision (codec.py:185-193).
-__device__ __forceinline__ int quant_exact(float x, const QuantRowCtx& q, uint64_t w) {
-  const double D = __dsub_rn((double)x, (double)q.mn);
-  const double h = __ddiv_rn(D, (double)q.s);
+// Exact fp64 reference decision (codec.py:185-193); rarely executed.
+__device__ __noinline__ int quant_exact(float x, float mn, float s, int B, uint64_t w) {
+  const double D = __dsub_rn((double)x, (double)mn);
+  const double h = __ddiv_rn(D, (double)s);
   const double f = floor(h);
   const double fr = __dsub_rn(h, f);
   const double u = u53_to_double(w);
-  int code = (int)f + (u < fr ? 1 : 0);
-  return min(max(code, 0), q.B);
+  const int code = (int)f + (u < fr ? 1 : 0);
+  return min(max(code, 0), B);
 }
 
-// fp32 filter: returns the code, or -1 when the decision needs fp64.
-__device__ __forceinline__ int quant_fast(float x, const QuantRowCtx& q, uint64_t w) {
-  if (x == q.mn) return 0;                       // h == 0 exactly on both paths
+// fp32 decision + "ambiguous" flag.  With |h32 - h64| <= E (rigorous bound for
+// the fp32 evaluation) and u in [ut, ut + 2^-23):
+//   * floor(h) is certain unless frac(h32) is within E of an integer;
+//   * (u < frac) is certain unless |frac32 - ut| < E + 2^-22.
+// Ambiguous elements are recomputed with the exact fp64 path.
+__device__ __forceinline__ int quant_fast(float x, const QuantRowCtx& q, uint64_t w, bool& amb) {
   const float xm = __fsub_rn(x, q.mn);
   const float h = __fmul_rn(xm, q.inv_s);
-  if (!(h < 8388608.0f)) return -1;
   const float fl = floorf(h);
-  const float fr = __fsub_rn(h, fl);             // exact
-  if (fr < q.E || fr > 1.0f - q.E) return -1;    // floor(h) itself is uncertain
-  const float ut = __uint2float_rn((uint32_t)(w >> 40)) * 5.9604644775390625e-08f;  // top 24 bits
-  int up;
-  if (ut + 5.9604644775390625e-08f + q.E <= fr) up = 1;   // u < ut + 2^-24 <= frac
-  else if (ut >= fr + q.E) up = 0;                         // u >= ut >= frac
-  else return -1;
-  const int code = (int)fl + up;
+  const float fr = __fsub_rn(h, fl);
+  const float ut = __fsub_rn(__uint_as_float(((uint32_t)(w >> 32) >> 9) | 0x3f800000u), 1.0f);
+  amb = (x != q.mn) & ((fr <= q.E) | (fr >= 1.0f - q.E) | (fabsf(__fsub_rn(fr, ut)) <= q.Eu) |
+                        !(h < 8388608.0f));
+  const int code = (int)fl + (ut < fr ? 1 : 0);
   return min(max(code, 0), q.B);
 }
 
-__device__ __forceinline__ int quant_one(float x, const QuantRowCtx& q, uint64_t w) {
-  if (q.fast) {
-    const int c = quant_fast(x, q, w);
-    if (c >= 0) return c;
-  }
-  return quant_exact(x, q, w);
+// b = 1: h in [0, 1 + eps]; a non-ambiguous element has floor(h) = 0, so the
+// code is just (u < h).
+__device__ __forceinline__ uint32_t quant_fast_b1(float x, const QuantRowCtx& q, uint64_t w, bool& amb) {
+  const float h = __fmul_rn(__fsub_rn(x, q.mn), q.inv_s);
+  const float ut = __fsub_rn(__uint_as_float(((uint32_t)(w >> 32) >> 9) | 0x3f800000u), 1.0f);
+  amb = (x != q.mn) & ((h <= q.E) | (h >= 1.0f - q.E) | (fabsf(__fsub_rn(h, ut)) <= q.Eu));
+  return ut < h ? 1u : 0u;
+}
+
+// General b, no clamp needed: a non-ambiguous element has floor(h) <= B - 1.
+__device__ __forceinline__ uint32_t quant_fast_nc(float x, const QuantRowCtx& q, uint64_t w, bool& amb) {
+  const float h = __fmul_rn(__fsub_rn(x, q.mn), q.inv_s);
+  const float fl = floorf(h);
+  const float fr = __fsub_rn(h, fl);
+  const float ut = __fsub_rn(__uint_as_float(((uint32_t)(w >> 32) >> 9) | 0x3f800000u), 1.0f);
+  amb = (x != q.mn) & ((fr <= q.E) | (fr >= 1.0f - q.E) | (fabsf(__fsub_rn(fr, ut)) <= q.Eu) |
+                        !(h < 8388608.0f));
+  const float cf = __fadd_rn(fl, ut < fr ? 1.0f : 0.0f);
+  return __float_as_uint(__fadd_rn(cf, 8388608.0f)) & 0x7fffffu;   // exact small integer
+}
+
+__device__ __forceinline__ float sel4(const float (&a)[4], int k) {
+  return k == 0 ? a[0] : (k == 1 ? a[1] : (k == 2 ? a[2] : a[3]));
 }
 
 __device__ __forceinline__ void write_header(uint8_t* out, int bits, int rows, int d) {
@@ -85,69 +111,77 @@ __device__ __forceinline__ void write_header(uint8_t* out, int bits, int rows, i
   for (int k = 0; k < 4; ++k) out[8 + k] = (uint8_t)((uint32_t)d >> (8 * k));
 }
 
-__device__ __forceinline__ void store_f32_unaligned4(uint8_t* p, float v) {
-  // p is 4-byte aligned by construction (12 + 8r offsets from a 16B-aligned block)
-  *reinterpret_cast<float*>(p) = v;
-}
-
-// NCH > 0: the row is held in registers (NCH chunks of 128 columns, Philox frame).
-// NCH == 0: generic path for very wide rows (re-reads x in the second pass).
-template <int NCH>
-__global__ void __launch_bounds__(kQWarps * 32)
+// K1, register-lean layout (occupancy matters: Philox4x64-10 is a chain of
+// dependent 64-bit multiplies, so the SM needs many warps in flight).
+//   pass 1: stream the row once (128-bit loads) for min / max / finiteness;
+//   pass 2: per 128-column chunk, each lane computes one Philox block (4
+//           uniforms), re-reads its 4 columns (L1 hits) in the Philox frame,
+//           quantizes and packs.
+// MAXW: row-image words per warp in shared memory (bounds d).
+//
+// Packing: for bits in {1, 2, 4, 8} each lane's 4 codes form a 4b-bit field;
+// a shuffle-OR over 8/b lanes assembles 32-bit words of the chunk image
+// (chunk bit q = 4b*lane + b*i + j), stored to a per-warp smem array; the row
+// image is then the chunk stream shifted right by delta*b bits (the Philox
+// frame starts delta columns before the row).  Other widths OR codes into the
+// smem row image with shared-memory atomics.
+template <bool B1, int MAXW>
+__global__ void __launch_bounds__(kQWarps * 32, 4)
 quantize_gather_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
                        int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
                        int bits, uint32_t* __restrict__ flags) {
   __shared__ hb_segment_t segs_s[kMaxSmemSegs];
-  __shared__ uint32_t rowbuf[kQWarps][NCH > 0 ? kRowBufWords : 2];
+  __shared__ int32_t seg_begin[kMaxSmemSegs];
+  __shared__ uint32_t rowbuf[kQWarps][MAXW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool smem_segs = nseg <= kMaxSmemSegs;
   if (smem_segs) {
-    for (int i = threadIdx.x; i < nseg; i += blockDim.x) segs_s[i] = segs_g[i];
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+      segs_s[i] = segs_g[i];
+      seg_begin[i] = segs_g[i].row_begin;
+    }
     __syncthreads();
   }
-  const hb_segment_t* segs = smem_segs ? segs_s : segs_g;
   const int B = (1 << bits) - 1;
   const int rb = (d * bits + 7) >> 3;
-  const int nchunks_max = (d + 3 + 127) >> 7;
+  const bool pow2 = bits <= 8 && (bits & (bits - 1)) == 0;
+  const bool vec = ((ld & 3) == 0) && ((((uintptr_t)src) & 15) == 0);
   uint32_t* buf = rowbuf[warp];
-  const int buf_words = (NCH > 0) ? ((64 + bits * (nchunks_max * 128)) >> 5) + 3 : 0;
 
   for (int row = blockIdx.x * kQWarps + warp; row < total_rows; row += gridDim.x * kQWarps) {
-    const hb_segment_t sg = segs[find_segment(segs, nseg, row)];
+    const int si = smem_segs ? find_segment_smem(seg_begin, nseg, row) : find_segment(segs_g, nseg, row);
+    const hb_segment_t sg = smem_segs ? segs_s[si] : segs_g[si];
     const int r = row - sg.row_begin;
-    const float* x = src + (int64_t)row_idx[row] * ld;
+    const float* __restrict__ x = src + (int64_t)row_idx[row] * ld;
     const uint64_t e_row = sg.elem_offset + (uint64_t)r * (uint64_t)d;
     const int delta = (int)(e_row & 3ull);
     const uint64_t blk0 = e_row >> 2;
     const int nchunks = (d + delta + 127) >> 7;
     uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
 
-    // ---- pass 1: load (Philox frame) + row min/max + finiteness -------------
-    float v[NCH > 0 ? NCH : 1][4];
+    // ---- pass 1: min / max / finiteness ---------------------------------------
     float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
     bool bad = false;
-    if (NCH > 0) {
-#pragma unroll
-      for (int t = 0; t < (NCH > 0 ? NCH : 1); ++t) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int c = 128 * t + 4 * lane + i - delta;
-          float xv = 0.f;
-          if (t < nchunks && c >= 0 && c < d) {
-            xv = __ldg(x + c);
-            mn = fminf(mn, xv);
-            mx = fmaxf(mx, xv);
-            bad |= !isfinite(xv);
-          }
-          v[t][i] = xv;
-        }
+    if (vec) {
+      const int d4 = d >> 2;
+      for (int k = lane; k < d4; k += 32) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(x) + k);
+        mn = fminf(fminf(mn, a.x), fminf(a.y, fminf(a.z, a.w)));
+        mx = fmaxf(fmaxf(mx, a.x), fmaxf(a.y, fmaxf(a.z, a.w)));
+        bad |= !(isfinite(a.x) & isfinite(a.y) & isfinite(a.z) & isfinite(a.w));
+      }
+      for (int c = 4 * d4 + lane; c < d; c += 32) {
+        const float a = __ldg(x + c);
+        mn = fminf(mn, a);
+        mx = fmaxf(mx, a);
+        bad |= !isfinite(a);
       }
     } else {
       for (int c = lane; c < d; c += 32) {
-        const float xv = __ldg(x + c);
-        mn = fminf(mn, xv);
-        mx = fmaxf(mx, xv);
-        bad |= !isfinite(xv);
+        const float a = __ldg(x + c);
+        mn = fminf(mn, a);
+        mx = fmaxf(mx, a);
+        bad |= !isfinite(a);
       }
     }
     mn = warp_min(mn);
@@ -172,75 +206,368 @@ quantize_gather_kernel(const float* __restrict__ src, int64_t ld, const int32_t*
     q.live = q.s > 0.0f;
     q.inv_s = q.live ? __frcp_rn(q.s) : 0.f;
     q.fast = q.live && q.s >= 7.888609052210118e-31f /* 2^-100 */ &&
-             fabsf(mn) <= 1.2676506002282294e30f && fabsf(mx) <= 1.2676506002282294e30f &&
-             bits <= 16;
+             fabsf(mn) <= 1.2676506002282294e30f && fabsf(mx) <= 1.2676506002282294e30f;
     q.E = (float)(B + 2) * 2.384185791015625e-07f;  // (B+2) * 2^-22
+    q.Eu = q.E + 2.384185791015625e-07f;
     if (lane == 0) {
-      store_f32_unaligned4(out + HB_HEADER_BYTES + 8 * (int64_t)r, q.mn);
-      store_f32_unaligned4(out + HB_HEADER_BYTES + 8 * (int64_t)r + 4, q.s);
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r) = q.mn;
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r + 4) = q.s;
     }
     uint8_t* pay = out + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
 
-    if (NCH == 0) {
-      // generic wide-row path: direct byte-wise OR is impossible without atomics on
-      // global memory, so each lane assembles whole payload bytes itself.
-      for (int byte = lane; byte < rb; byte += 32) {
-        uint32_t acc = 0;
-        const int c_first = (byte * 8) / bits, c_last = min(d - 1, (byte * 8 + 7) / bits);
-        for (int c = c_first; c <= c_last; ++c) {
-          int code = 0;
-          if (q.live) {
-            const uint64_t e = e_row + (uint64_t)c;
-            const U64x4 u = philox4x64_10((e >> 2) + 1, sg.key0, sg.key1);
-            code = quant_one(__ldg(x + c), q, pick(u, (int)(e & 3)));
-          }
-          const int pos = c * bits - byte * 8;  // may be negative for straddling codes
-          acc |= pos >= 0 ? ((uint32_t)code << pos) : ((uint32_t)code >> (-pos));
-        }
-        pay[byte] = (uint8_t)(acc & 0xffu);
-      }
-      continue;
+    // ---- pass 2: Philox + quantize + pack --------------------------------------
+    const int nw_chunk = 4 * bits;                          // chunk image words (pow2 path)
+    if (!pow2) {
+      const int buf_words = ((64 + bits * (nchunks * 128)) >> 5) + 3;
+      for (int k = lane; k < buf_words; k += 32) buf[k] = 0u;
+      __syncwarp();
     }
-
-    // ---- pass 2: Philox + quantize + pack into the smem row image ------------
-    for (int k = lane; k < buf_words; k += 32) buf[k] = 0u;
-    __syncwarp();
-    if (q.live) {
+    for (int t = 0; t < nchunks; ++t) {
+      uint32_t field = 0, field_hi = 0;
+      if (q.live) {
+        const U64x4 u = philox4x64_10(blk0 + (uint64_t)(32 * t + lane) + 1ull, sg.key0, sg.key1);
+        const int c0 = 128 * t + 4 * lane - delta;
+        const bool full = q.fast && (128 * t - delta >= 0) && (128 * t - delta + 128 <= d);
+        uint32_t code[4];
+        bool amb[4];
+        if (full) {
+          const float xv[4] = {__ldg(x + c0), __ldg(x + c0 + 1), __ldg(x + c0 + 2), __ldg(x + c0 + 3)};
+          const uint64_t ws[4] = {u.w0, u.w1, u.w2, u.w3};
 #pragma unroll
-      for (int t = 0; t < (NCH > 0 ? NCH : 1); ++t) {
-        if (t < nchunks) {
-          const U64x4 u = philox4x64_10(blk0 + (uint64_t)(32 * t + lane) + 1ull, sg.key0, sg.key1);
-          const int c0 = 128 * t + 4 * lane - delta;
-          uint64_t field = 0;
+          for (int i = 0; i < 4; ++i)
+            code[i] = B1 ? quant_fast_b1(xv[i], q, ws[i], amb[i]) : quant_fast_nc(xv[i], q, ws[i], amb[i]);
+        } else {
+          const uint64_t ws[4] = {u.w0, u.w1, u.w2, u.w3};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int c = c0 + i;
+            amb[i] = false;
+            code[i] = 0;
             if (c >= 0 && c < d) {
-              const uint64_t w = i == 0 ? u.w0 : (i == 1 ? u.w1 : (i == 2 ? u.w2 : u.w3));
-              field |= (uint64_t)quant_one(v[t][i], q, w) << (i * bits);
+              const float xv = __ldg(x + c);
+              if (q.fast) code[i] = B1 ? quant_fast_b1(xv, q, ws[i], amb[i]) : quant_fast_nc(xv, q, ws[i], amb[i]);
+              else amb[i] = true;
             }
           }
-          if (field) {
-            const int pos = 64 + bits * c0;           // >= 16 for bits <= 16
-            const int wd = pos >> 5, sh = pos & 31;
-            const uint64_t lo = field << sh;
-            atomicOr(&buf[wd], (uint32_t)lo);
-            if ((uint32_t)(lo >> 32)) atomicOr(&buf[wd + 1], (uint32_t)(lo >> 32));
-            if (sh && (field >> (64 - sh))) atomicOr(&buf[wd + 2], (uint32_t)(field >> (64 - sh)));
-          }
         }
+        if (__any_sync(0xffffffffu, amb[0] | amb[1] | amb[2] | amb[3])) {
+          const uint64_t ws[4] = {u.w0, u.w1, u.w2, u.w3};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (amb[i]) code[i] = (uint32_t)quant_exact(__ldg(x + c0 + i), q.mn, q.s, q.B, ws[i]);
+        }
+        if (bits <= 8) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) field |= code[i] << (i * bits);
+        } else {  // bits == 16
+          field = code[0] | (code[1] << 16);
+          field_hi = code[2] | (code[3] << 16);
+        }
+      }
+      if (pow2) {
+        // chunk image word k = OR of fields of lanes [k*L, (k+1)*L), L = 8/bits
+        const int L = 8 / bits;
+        uint32_t w = field << ((4 * bits) * (lane & (L - 1)));
+        if (L >= 2) w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        if (L >= 4) w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        if (L >= 8) w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + lane / L] = w;
+      } else if (field | field_hi) {
+        const int c0 = 128 * t + 4 * lane - delta;
+        const int pos = 64 + bits * c0;                     // >= 16 for bits <= 16
+        const int wd = pos >> 5, sh = pos & 31;
+        const uint64_t f64v = (uint64_t)field | ((uint64_t)field_hi << 32);
+        const uint64_t lo = f64v << sh;
+        atomicOr(&buf[wd], (uint32_t)lo);
+        if ((uint32_t)(lo >> 32)) atomicOr(&buf[wd + 1], (uint32_t)(lo >> 32));
+        if (sh && (f64v >> (64 - sh))) atomicOr(&buf[wd + 2], (uint32_t)(f64v >> (64 - sh)));
       }
     }
     __syncwarp();
-    const uint8_t* img = reinterpret_cast<const uint8_t*>(buf) + 8;
-    if ((((uintptr_t)pay) & 3) == 0 && (rb & 3) == 0) {
-      uint32_t* pw = reinterpret_cast<uint32_t*>(pay);
-      const uint32_t* iw = buf + 2;
-      for (int k = lane; k < (rb >> 2); k += 32) pw[k] = iw[k];
+    // ---- emit the row image ------------------------------------------------------
+    const int nrw = (rb + 3) >> 2;                            // row words
+    const bool wordstore = ((((uintptr_t)pay) & 3) == 0) && ((rb & 3) == 0);
+    if (pow2) {
+      const int sh = delta * bits;                            // 0..24
+      const int total_w = nw_chunk * nchunks;
+      for (int m = lane; m < nrw; m += 32) {
+        const uint32_t lo = buf[m];
+        const uint32_t hi = (m + 1 < total_w) ? buf[m + 1] : 0u;
+        const uint32_t rw = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
+        if (wordstore) {
+          reinterpret_cast<uint32_t*>(pay)[m] = rw;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * m + k < rb) pay[4 * m + k] = (uint8_t)(rw >> (8 * k));
+        }
+      }
     } else {
-      for (int k = lane; k < rb; k += 32) pay[k] = img[k];
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(buf) + 8;
+      if (wordstore) {
+        const uint32_t* iw = buf + 2;
+        for (int k = lane; k < nrw; k += 32) reinterpret_cast<uint32_t*>(pay)[k] = iw[k];
+      } else {
+        for (int k = lane; k < rb; k += 32) pay[k] = img[k];
+      }
     }
     __syncwarp();
+  }
+}
+
+// K1 with TMA staging: each warp streams its rows through two shared-memory
+// row buffers filled by 1-D bulk async copies (cp.async.bulk + mbarrier), one
+// row ahead, so HBM latency hides behind the Philox work of the current row
+// and the row is read from HBM exactly once (128-bit bulk transfers).
+// Requires ld % 4 == 0 and a 16-byte aligned source.
+template <bool B1, int MINB>
+__global__ void __launch_bounds__(kQWarps * 32, MINB)
+quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
+                           int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
+                           int bits, uint32_t* __restrict__ flags, int ldr, int imgw) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs];
+  __shared__ __align__(8) uint64_t bars[kQWarps][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool smem_segs = nseg <= kMaxSmemSegs;
+  if (smem_segs) {
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+      segs_s[i] = segs_g[i];
+      seg_begin[i] = segs_g[i].row_begin;
+    }
+  }
+  float* rows_s = reinterpret_cast<float*>(dsm + (size_t)warp * (2 * ldr * 4 + imgw * 4));
+  uint32_t* buf = reinterpret_cast<uint32_t*>(rows_s + 2 * ldr);
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int B = (1 << bits) - 1;
+  const int rb = (d * bits + 7) >> 3;
+  const bool pow2 = bits <= 8 && (bits & (bits - 1)) == 0;
+  const uint32_t bytes = (uint32_t)(((d + 3) & ~3) * 4);
+  const int stride = gridDim.x * kQWarps;
+  uint32_t phase[2] = {0u, 0u};
+
+  int row = blockIdx.x * kQWarps + warp;
+  if (row < total_rows && lane == 0) {
+    mbar_expect_tx(&bars[warp][0], bytes);
+    tma_load_1d(rows_s, src + (int64_t)__ldg(row_idx + row) * ld, bytes, &bars[warp][0]);
+  }
+  for (int k = 0; row < total_rows; row += stride, ++k) {
+    const int cur = k & 1;
+    const int nxt = row + stride;
+    if (nxt < total_rows && lane == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bars[warp][cur ^ 1], bytes);
+      tma_load_1d(rows_s + (cur ^ 1) * ldr, src + (int64_t)__ldg(row_idx + nxt) * ld, bytes,
+                  &bars[warp][cur ^ 1]);
+    }
+    const int si = smem_segs ? find_segment_smem(seg_begin, nseg, row) : find_segment(segs_g, nseg, row);
+    const hb_segment_t sg = smem_segs ? segs_s[si] : segs_g[si];
+    const int r = row - sg.row_begin;
+    const uint64_t e_row = sg.elem_offset + (uint64_t)r * (uint64_t)d;
+    const int delta = (int)(e_row & 3ull);
+    const uint64_t blk0 = e_row >> 2;
+    const int nchunks = (d + delta + 127) >> 7;
+    uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
+    const float* xs = rows_s + cur * ldr;
+    mbar_wait(&bars[warp][cur], phase[cur]);
+    phase[cur] ^= 1u;
+
+    // ---- pass 1 (smem): min / max / finiteness ----------------------------------
+    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+    bool bad = false;
+    const int d4 = d >> 2;
+    for (int c4 = lane; c4 < d4; c4 += 32) {
+      const float4 a = reinterpret_cast<const float4*>(xs)[c4];
+      mn = fminf(fminf(mn, a.x), fminf(a.y, fminf(a.z, a.w)));
+      mx = fmaxf(fmaxf(mx, a.x), fmaxf(a.y, fmaxf(a.z, a.w)));
+      bad |= !(isfinite(a.x) & isfinite(a.y) & isfinite(a.z) & isfinite(a.w));
+    }
+    for (int c = 4 * d4 + lane; c < d; c += 32) {
+      const float a = xs[c];
+      mn = fminf(mn, a);
+      mx = fmaxf(mx, a);
+      bad |= !isfinite(a);
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicOr(flags, HB_FLAG_NONFINITE);
+      __syncwarp();
+      continue;  // the host raises CodecError; the block contents are undefined
+    }
+    if (r == 0 && lane == 0) write_header(out, bits, sg.num_rows, d);
+    QuantRowCtx q;
+    q.bits = bits;
+    q.B = B;
+    q.mn = mn;
+    q.s = __double2float_rn(__ddiv_rn(__dsub_rn((double)mx, (double)mn), (double)B));
+    q.live = q.s > 0.0f;
+    q.inv_s = q.live ? __frcp_rn(q.s) : 0.f;
+    q.fast = q.live && q.s >= 7.888609052210118e-31f /* 2^-100 */ &&
+             fabsf(mn) <= 1.2676506002282294e30f && fabsf(mx) <= 1.2676506002282294e30f;
+    q.E = (float)(B + 2) * 2.384185791015625e-07f;  // (B+2) * 2^-22
+    q.Eu = q.E + 2.384185791015625e-07f;
+    if (lane == 0) {
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r) = q.mn;
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r + 4) = q.s;
+    }
+    uint8_t* pay = out + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+
+    // ---- pass 2: Philox + quantize + pack --------------------------------------
+    const int nw_chunk = 4 * bits;
+    if (!pow2) {
+      const int buf_words = ((64 + bits * (nchunks * 128)) >> 5) + 3;
+      for (int w = lane; w < buf_words; w += 32) buf[w] = 0u;
+      __syncwarp();
+    }
+    for (int t = 0; t < nchunks; ++t) {
+      uint32_t field = 0, field_hi = 0;
+      if (q.live) {
+        const U64x4 u = philox4x64_10(blk0 + (uint64_t)(32 * t + lane) + 1ull, sg.key0, sg.key1);
+        const uint64_t ws[4] = {u.w0, u.w1, u.w2, u.w3};
+        const int c0 = 128 * t + 4 * lane - delta;
+        const bool full = q.fast && (128 * t - delta >= 0) && (128 * t - delta + 128 <= d);
+        uint32_t code[4];
+        bool amb[4];
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            code[i] = B1 ? quant_fast_b1(xs[c0 + i], q, ws[i], amb[i]) : quant_fast_nc(xs[c0 + i], q, ws[i], amb[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = c0 + i;
+            amb[i] = false;
+            code[i] = 0;
+            if (c >= 0 && c < d) {
+              if (q.fast) code[i] = B1 ? quant_fast_b1(xs[c], q, ws[i], amb[i]) : quant_fast_nc(xs[c], q, ws[i], amb[i]);
+              else amb[i] = true;
+            }
+          }
+        }
+        if (__any_sync(0xffffffffu, amb[0] | amb[1] | amb[2] | amb[3])) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (amb[i]) code[i] = (uint32_t)quant_exact(xs[c0 + i], q.mn, q.s, q.B, ws[i]);
+        }
+        if (bits <= 8) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) field |= code[i] << (i * bits);
+        } else {  // bits == 16
+          field = code[0] | (code[1] << 16);
+          field_hi = code[2] | (code[3] << 16);
+        }
+      }
+      if (pow2) {
+        const int L = 8 / bits;
+        uint32_t w = field << ((4 * bits) * (lane & (L - 1)));
+        if (L >= 2) w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        if (L >= 4) w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        if (L >= 8) w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + lane / L] = w;
+      } else if (field | field_hi) {
+        const int c0 = 128 * t + 4 * lane - delta;
+        const int pos = 64 + bits * c0;
+        const int wd = pos >> 5, sh = pos & 31;
+        const uint64_t f64v = (uint64_t)field | ((uint64_t)field_hi << 32);
+        const uint64_t lo = f64v << sh;
+        atomicOr(&buf[wd], (uint32_t)lo);
+        if ((uint32_t)(lo >> 32)) atomicOr(&buf[wd + 1], (uint32_t)(lo >> 32));
+        if (sh && (f64v >> (64 - sh))) atomicOr(&buf[wd + 2], (uint32_t)(f64v >> (64 - sh)));
+      }
+    }
+    __syncwarp();
+    const int nrw = (rb + 3) >> 2;
+    const bool wordstore = ((((uintptr_t)pay) & 3) == 0) && ((rb & 3) == 0);
+    if (pow2) {
+      const int sh = delta * bits;
+      const int total_w = nw_chunk * nchunks;
+      for (int m = lane; m < nrw; m += 32) {
+        const uint32_t lo = buf[m];
+        const uint32_t hi = (m + 1 < total_w) ? buf[m + 1] : 0u;
+        const uint32_t rw = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
+        if (wordstore) {
+          reinterpret_cast<uint32_t*>(pay)[m] = rw;
+        } else {
+#pragma unroll
+          for (int b4 = 0; b4 < 4; ++b4)
+            if (4 * m + b4 < rb) pay[4 * m + b4] = (uint8_t)(rw >> (8 * b4));
+        }
+      }
+    } else {
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(buf) + 8;
+      if (wordstore) {
+        const uint32_t* iw = buf + 2;
+        for (int w = lane; w < nrw; w += 32) reinterpret_cast<uint32_t*>(pay)[w] = iw[w];
+      } else {
+        for (int w = lane; w < rb; w += 32) pay[w] = img[w];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Generic per-element path (rows wider than the smem row image).
+__global__ void __launch_bounds__(kQWarps * 32)
+quantize_gather_wide_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
+                            int total_rows, const hb_segment_t* __restrict__ segs, int nseg, int d,
+                            int bits, uint32_t* __restrict__ flags) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = (1 << bits) - 1;
+  const int rb = (d * bits + 7) >> 3;
+  for (int row = blockIdx.x * kQWarps + warp; row < total_rows; row += gridDim.x * kQWarps) {
+    const hb_segment_t sg = segs[find_segment(segs, nseg, row)];
+    const int r = row - sg.row_begin;
+    const float* x = src + (int64_t)row_idx[row] * ld;
+    const uint64_t e_row = sg.elem_offset + (uint64_t)r * (uint64_t)d;
+    uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
+    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+    bool bad = false;
+    for (int c = lane; c < d; c += 32) {
+      const float a = __ldg(x + c);
+      mn = fminf(mn, a);
+      mx = fmaxf(mx, a);
+      bad |= !isfinite(a);
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicOr(flags, HB_FLAG_NONFINITE);
+      continue;
+    }
+    if (r == 0 && lane == 0) write_header(out, bits, sg.num_rows, d);
+    if (bits == 32) {
+      float* prow = reinterpret_cast<float*>(out + HB_HEADER_BYTES) + (int64_t)r * d;
+      for (int c = lane; c < d; c += 32) prow[c] = __ldg(x + c);
+      continue;
+    }
+    const float s = __double2float_rn(__ddiv_rn(__dsub_rn((double)mx, (double)mn), (double)B));
+    if (lane == 0) {
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r) = mn;
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r + 4) = s;
+    }
+    uint8_t* pay = out + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+    for (int byte = lane; byte < rb; byte += 32) {
+      uint32_t acc = 0;
+      const int c_first = (byte * 8) / bits, c_last = min(d - 1, (byte * 8 + 7) / bits);
+      for (int c = c_first; c <= c_last; ++c) {
+        int code = 0;
+        if (s > 0.0f) {
+          const uint64_t e = e_row + (uint64_t)c;
+          const U64x4 u = philox4x64_10((e >> 2) + 1, sg.key0, sg.key1);
+          code = quant_exact(__ldg(x + c), mn, s, B, pick(u, (int)(e & 3)));
+        }
+        const int pos = c * bits - byte * 8;  // may be negative for straddling codes
+        acc |= pos >= 0 ? ((uint32_t)code << pos) : ((uint32_t)code >> (-pos));
+      }
+      pay[byte] = (uint8_t)(acc & 0xffu);
+    }
   }
 }
 
@@ -359,23 +686,39 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
                                    int bits, uint32_t* flags, cudaStream_t st) {
   if (total_rows <= 0) return cudaSuccess;
   const int nch = (d + 3 + 127) / 128;
+  const bool pow2 = bits <= 8 && (bits & (bits - 1)) == 0;
+  const int need = pow2 ? 4 * bits * nch + 1 : ((64 + (bits == 32 ? 0 : bits) * nch * 128) >> 5) + 3;
   const int want = (total_rows + kQWarps - 1) / kQWarps;
-  const int grid = want < num_sms() * 8 ? want : num_sms() * 8;
+  const int grid = want < num_sms() * 16 ? want : num_sms() * 16;
   const dim3 blk(kQWarps * 32);
-#define HB_Q(N) quantize_gather_kernel<N><<<grid, blk, 0, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, bits, flags)
-  switch (nch) {
-    case 1: HB_Q(1); break;
-    case 2: HB_Q(2); break;
-    case 3: HB_Q(3); break;
-    case 4: HB_Q(4); break;
-    case 5: HB_Q(5); break;
-    case 6: HB_Q(6); break;
-    case 7: HB_Q(7); break;
-    case 8: HB_Q(8); break;
-    case 9: HB_Q(9); break;
-    default: HB_Q(0); break;
+#define ARGS src, ld, row_idx, total_rows, segs, nseg, d, bits, flags
+  static const bool no_tma = getenv("HB_K1_NO_TMA") != nullptr;
+  const bool aligned = (ld % 4 == 0) && ((((uintptr_t)src) & 15) == 0);
+  if (!no_tma && aligned && bits != 32 && d <= 4096) {
+    const int ldr = (d + 3) & ~3;
+    const int imgw = ((pow2 ? 4 * bits * nch + 2 : ((64 + bits * nch * 128) >> 5) + 4) + 3) & ~3;  // 16B multiple
+    const size_t dyn = (size_t)kQWarps * (2 * ldr * 4 + imgw * 4);
+    if (dyn <= 200 * 1024) {
+      static const int minb = getenv("HB_K1_MINB") ? atoi(getenv("HB_K1_MINB")) : 3;
+      auto kern = bits == 1 ? (minb == 4 ? quantize_gather_tma_kernel<true, 4> : quantize_gather_tma_kernel<true, 3>)
+                            : (minb == 4 ? quantize_gather_tma_kernel<false, 4> : quantize_gather_tma_kernel<false, 3>);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      kern<<<grid, blk, dyn, st>>>(ARGS, ldr, imgw);
+#undef ARGS
+      return cudaGetLastError();
+    }
   }
-#undef HB_Q
+#define ARGS src, ld, row_idx, total_rows, segs, nseg, d, bits, flags
+  if (bits == 32 || need <= kK1SmallWords) {
+    if (bits == 1) quantize_gather_kernel<true, kK1SmallWords><<<grid, blk, 0, st>>>(ARGS);
+    else quantize_gather_kernel<false, kK1SmallWords><<<grid, blk, 0, st>>>(ARGS);
+  } else if (need <= kK1LargeWords) {
+    if (bits == 1) quantize_gather_kernel<true, kK1LargeWords><<<grid, blk, 0, st>>>(ARGS);
+    else quantize_gather_kernel<false, kK1LargeWords><<<grid, blk, 0, st>>>(ARGS);
+  } else {
+    quantize_gather_wide_kernel<<<grid, blk, 0, st>>>(ARGS);
+  }
+#undef ARGS
   return cudaGetLastError();
 }
 

@@ -43,6 +43,35 @@ __device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t k0, uint64_
   return {x0, x1, x2, x3};
 }
 
+// Two independent blocks with interleaved rounds: doubles the ILP of the
+// (latency-bound) 64-bit multiply chains.
+__device__ __forceinline__ void philox4x64_10_x2(uint64_t ca, uint64_t cb, uint64_t k0, uint64_t k1,
+                                                 U64x4& ra, U64x4& rb) {
+  constexpr uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  constexpr uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+  uint64_t a0, a1, a2, a3, b0, b1, b2, b3;
+  uint64_t ah0, al0, ah1, al1, bh0, bl0, bh1, bl1;
+  mulhilo64(M0, ca, ah0, al0);
+  mulhilo64(M0, cb, bh0, bl0);
+  a0 = k0; a1 = 0; a2 = ah0 ^ k1; a3 = al0;
+  b0 = k0; b1 = 0; b2 = bh0 ^ k1; b3 = bl0;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    k0 += W0;
+    k1 += W1;
+    mulhilo64(M0, a0, ah0, al0);
+    mulhilo64(M0, b0, bh0, bl0);
+    mulhilo64(M1, a2, ah1, al1);
+    mulhilo64(M1, b2, bh1, bl1);
+    const uint64_t na0 = ah1 ^ a1 ^ k0, na2 = ah0 ^ a3 ^ k1;
+    const uint64_t nb0 = bh1 ^ b1 ^ k0, nb2 = bh0 ^ b3 ^ k1;
+    a1 = al1; a3 = al0; a0 = na0; a2 = na2;
+    b1 = bl1; b3 = bl0; b0 = nb0; b2 = nb2;
+  }
+  ra = {a0, a1, a2, a3};
+  rb = {b0, b1, b2, b3};
+}
+
 __device__ __forceinline__ double u53_to_double(uint64_t w) {
   return (double)(w >> 11) * (1.0 / 9007199254740992.0);
 }

@@ -1,0 +1,110 @@
+"""Microbenchmarks of the halo-path kernels on synthetic inputs (GPU box).
+
+  python tools/kbench.py codec [--rows R --d D --bits B --segs S]
+  python tools/kbench.py spmm  [--config reddit]      (real planted graph, all SpMM shapes)
+
+Times each kernel with CUDA events over several launches (inputs > L2), prints
+one JSON line per case with achieved algorithmic GB/s.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def _time(fn, reps=10, warm=3):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def codec(args):
+    import torch
+    from paper_2303_01277_b200 import codec as C
+    from paper_2303_01277_b200.rngstream import derive_key
+    rng = np.random.default_rng(0)
+    R, d, b, S = args.rows, args.d, args.bits, args.segs
+    ld = (d + 3) // 4 * 4
+    nsrc = int(R * 1.5)
+    src = torch.randn(nsrc, ld, device="cuda") * torch.rand(nsrc, 1, device="cuda") * 3
+    idx = np.sort(rng.choice(nsrc, size=R, replace=False)).astype(np.int32)
+    bounds = np.linspace(0, R, S + 1).astype(int)
+    rows = np.diff(bounds)
+    sizes = [(C.wire_bytes(int(r), d, b) + 15) // 16 * 16 for r in rows]
+    out = torch.zeros(sum(sizes), dtype=torch.uint8, device="cuda")
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    keys = [derive_key((0, s // 7, 1, 1, "forward")) for s in range(S)]
+    eoff = [int((bounds[s] - bounds[(s // 7) * 7]) * d) for s in range(S)]
+    segs = C.segments_tensor([int(r) for r in rows], keys, eoff,
+                             [out.data_ptr() + int(o) for o in offs], "cuda")
+    ridx = torch.from_numpy(idx).cuda()
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ms = _time(lambda: C.quantize_gather(src, ridx, segs, S, d, b, flags))
+    nbytes = R * d * 4 + R * 4 + sum(C.wire_bytes(int(r), d, b) for r in rows)
+    print(json.dumps({"kernel": "quantize_gather", "rows": R, "d": d, "bits": b, "ms": ms,
+                      "gbps": nbytes / ms / 1e6, "gelem_s": R * d / ms / 1e6}), flush=True)
+    # K2 forward scatter into a halo region
+    dst = torch.zeros(nsrc, ld, device="cuda")
+    drow = torch.from_numpy(rng.permutation(nsrc)[:R].astype(np.int32)).cuda()
+    ptr = torch.arange(R + 1, dtype=torch.int32, device="cuda")
+    srows = torch.arange(R, dtype=torch.int32, device="cuda")
+    ms2 = _time(lambda: C.dequant_gather(segs, S, drow, ptr, srows, d, b, dst, False))
+    nb2 = sum(C.wire_bytes(int(r), d, b) for r in rows) + R * d * 4 + 12 * R
+    print(json.dumps({"kernel": "dequant_gather", "rows": R, "d": d, "bits": b, "ms": ms2,
+                      "gbps": nb2 / ms2 / 1e6}), flush=True)
+
+
+def spmm(args):
+    import torch
+    sys.path.insert(0, str(ROOT))
+    from bench import build_graph
+    from paper_2303_01277_b200 import ops
+    from paper_2303_01277_b200.trainer import _stack_csr, _transpose_device
+    from paper_2303_01277_b200.transport import RankLayout
+    t0 = time.time()
+    g, parts = build_graph(args.config)
+    lay = RankLayout(parts, [0] * len(parts), 0)
+    which = "mean" if args.config != "yelp" else "adj"
+    rp, ci, v = _stack_csr(lay, which)
+    A = ops.DeviceCsr(lay.NL, lay.NL + lay.NH, rp, ci, v, "cuda")
+    At = _transpose_device(A)
+    print(json.dumps({"setup_s": time.time() - t0, "NL": lay.NL, "NH": lay.NH, "nnz": A.nnz}), flush=True)
+    for name, M, d in (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("A", A, 64)):
+        ld = (d + 3) // 4 * 4
+        X = torch.randn(M.cols, ld, device="cuda")
+        Y = torch.zeros(M.rows, ld, device="cuda")
+        ms = _time(lambda: ops.spmm(M, X, Y, d), reps=5)
+        comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
+        print(json.dumps({"kernel": "spmm", "mat": name, "d": d, "ms": ms,
+                          "compulsory_gbps": comp / ms / 1e6,
+                          "gather_gbps": (8 * M.nnz + 4 * M.nnz * d) / ms / 1e6,
+                          "tflops": 2 * M.nnz * d / ms / 1e9}), flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["codec", "spmm"])
+    ap.add_argument("--rows", type=int, default=461_644)
+    ap.add_argument("--d", type=int, default=602)
+    ap.add_argument("--bits", type=int, default=1)
+    ap.add_argument("--segs", type=int, default=56)
+    ap.add_argument("--config", default="reddit")
+    a = ap.parse_args()
+    {"codec": codec, "spmm": spmm}[a.what](a)
