@@ -95,6 +95,17 @@ int hb_dequant_gather(const hb_segment_t* segs, int32_t nseg, int32_t num_dst,
 int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream);
 
+/* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
+ * tensor cores with the 3xTF32 split (fp32 accuracy):
+ *   C[m, n] = sum_k A(m, k) B(k, n) (+ beta * C[m, n])
+ *   A(m, k) = A[m*lda_m + k*lda_k],  B(k, n) = B[k*ldb_k + n*ldb_n]  (any strides)
+ * relu_out (optional, not with split-K): relu_out[m*ldr + n] = max(C[m, n], 0).
+ * ws (optional, ws_floats capacity): enables a deterministic split-K for
+ * small M*N with long K (the weight gradient G = P^T m). */
+int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k,
+                const float* B, int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta,
+                float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream);
+
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:
  * grad rows outside the mask are zero, masked rows get (softmax - onehot)/norm;
  * row_loss[i] = -log softmax[label] / norm (0 outside the mask) in f64.

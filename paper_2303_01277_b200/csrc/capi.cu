@@ -25,6 +25,9 @@ cudaError_t launch_argmax_accuracy(const float*, int64_t, int, int, const int32_
 cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, uint64_t, float, float*,
                            int64_t, cudaStream_t);
 
+cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
+                               float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+
 int num_sms() {
   static int cached = 0;
   if (!cached) {
@@ -91,6 +94,16 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)))
     return fail(HB_EINVAL, "hb_spmm_csr: bad arguments");
   return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, S(stream)), "hb_spmm_csr");
+}
+
+int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
+                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr,
+                float* ws, int64_t ws_floats, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || (M > 0 && N > 0 && (!A || !B || !C || K == 0)) || ldc < N)
+    return fail(HB_EINVAL, "hb_gemm_f32: bad arguments");
+  return check(hb::launch_gemm_tf32x3(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
+                                      ws_floats, S(stream)),
+               "hb_gemm_f32");
 }
 
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

@@ -35,6 +35,19 @@ def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None):
     return out
 
 
+def gemm(A, B, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
+    """C (+)= A @ B on tcgen05 (3xTF32), A/B any 2-D strided fp32 views
+    (trainer.py:294,313,318-321).  Returns C."""
+    M, K = A.shape
+    K2, N = B.shape
+    assert K == K2 and C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
+    _lib.call("hb_gemm_f32", M, N, K, ptr(A), A.stride(0), A.stride(1), ptr(B), B.stride(0),
+              B.stride(1), ptr(C), C.stride(0), float(beta), ptr(relu_out),
+              relu_out.stride(0) if relu_out is not None else 0, ptr(ws),
+              ws.numel() if ws is not None else 0, stream_handle(stream))
+    return C
+
+
 def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None):
     """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device."""
     n = labels.numel()

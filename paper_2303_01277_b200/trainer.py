@@ -23,6 +23,7 @@ given identical fp32 inputs (see codec.py).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -233,6 +234,10 @@ class DeviceRank:
         for w in self.W:
             self.G.append(self.gflat[off:off + w.numel()].view_as(w))
             off += w.numel()
+        # split-K workspace for the weight-gradient GEMM (G = P^T m, K = rows)
+        self.gemm_impl = os.environ.get("HB_GEMM", "cublas")
+        gmax = max(w.numel() for w in self.W)
+        self.gemm_ws = torch.empty(64 * gmax, dtype=f32, device=dev)
         self.adam_m = [torch.zeros_like(w) for w in self.W]
         self.adam_v = [torch.zeros_like(w) for w in self.W]
         self.adam_t = 0
@@ -371,16 +376,24 @@ class DeviceRank:
                 ops.spmm(self.A, Hd, agg, d)
             self.launches += 1
             Z = self.Z[l]
+            hout = self.Ht[l + 1][:NL, :W[l]] if l < L else None
             with self.timer("gemm", 0, 2 * NL * self.W[l - 1].shape[0] * W[l]):
-                if self.cfg.model == "sage":
-                    torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
-                    Z.addmm_(agg[:, :d], self.W[l - 1][d:])
+                if self.gemm_impl == "cublas":
+                    if self.cfg.model == "sage":
+                        torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
+                        Z.addmm_(agg[:, :d], self.W[l - 1][d:])
+                    else:
+                        torch.mm(agg[:, :d], self.W[l - 1], out=Z)
+                    if hout is not None:
+                        ops.relu(Z, self.Ht[l + 1], NL, W[l])
+                        self.launches += 1
+                elif self.cfg.model == "sage":
+                    ops.gemm(Hd[:NL, :d], self.W[l - 1][:d], Z)
+                    ops.gemm(agg[:, :d], self.W[l - 1][d:], Z, beta=1.0, relu_out=hout)
+                    self.launches += 2
                 else:
-                    torch.mm(agg[:, :d], self.W[l - 1], out=Z)
-            if l < L:
-                with self.timer("elementwise", 8 * NL * W[l]):
-                    ops.relu(Z, self.Ht[l + 1], NL, W[l])
-                self.launches += 1
+                    ops.gemm(agg[:, :d], self.W[l - 1], Z, relu_out=hout)
+                    self.launches += 1
         return self.Z[L]
 
     def _probe_halo(self, epoch, layer, tag, H, d):
@@ -411,22 +424,39 @@ class DeviceRank:
             agg = self.AGG[l]
             G = self.G[l - 1]
             with self.timer("gemm", 0, 2 * NL * G.shape[0] * dout):
-                if self.cfg.model == "sage":
-                    torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
-                    torch.mm(agg[:, :d].t(), m, out=G[d:])
+                if self.gemm_impl == "cublas":
+                    if self.cfg.model == "sage":
+                        torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
+                        torch.mm(agg[:, :d].t(), m, out=G[d:])
+                    else:
+                        torch.mm(agg[:, :d].t(), m, out=G)
+                elif self.cfg.model == "sage":
+                    ops.gemm(Hd[:NL, :d].t(), m, G[:d], ws=self.gemm_ws)
+                    ops.gemm(agg[:, :d].t(), m, G[d:], ws=self.gemm_ws)
+                    self.launches += 4
                 else:
-                    torch.mm(agg[:, :d].t(), m, out=G)
+                    ops.gemm(agg[:, :d].t(), m, G, ws=self.gemm_ws)
+                    self.launches += 2
             if l == 1:
                 break
             T, JF = self.T[l], self.JF[l]
             Wl = self.W[l - 1]
             with self.timer("gemm", 0, 2 * NL * d * dout):
-                torch.mm(m, (Wl[d:] if self.cfg.model == "sage" else Wl).t(), out=T)
+                Wb = (Wl[d:] if self.cfg.model == "sage" else Wl).t()
+                if self.gemm_impl == "cublas":
+                    torch.mm(m, Wb, out=T)
+                else:
+                    ops.gemm(m, Wb, T)
+                    self.launches += 1
             with self.timer("spmm", *_spmm_cost(self.At, d)):
                 ops.spmm(self.At, T, JF, d)
             if self.cfg.model == "sage":
                 with self.timer("gemm", 0, 2 * NL * d * dout):
-                    JF[:NL, :d].addmm_(m, Wl[:d].t())
+                    if self.gemm_impl == "cublas":
+                        JF[:NL, :d].addmm_(m, Wl[:d].t())
+                    else:
+                        ops.gemm(m, Wl[:d].t(), JF[:NL, :d], beta=1.0)
+                        self.launches += 1
             self.launches += 1
             if self.drop:
                 self._dropout(JF, JF, epoch, l, d)

@@ -98,13 +98,38 @@ def spmm(args):
                           "tflops": 2 * M.nnz * d / ms / 1e9}), flush=True)
 
 
+def gemm(args):
+    import torch
+    from paper_2303_01277_b200 import ops
+    NL = 232_965
+    g = torch.Generator(device="cuda").manual_seed(0)
+    cases = [("Z=P W   (l1 half)", NL, 256, 602, "nn"), ("Z=P W   (l2 half)", NL, 256, 256, "nn"),
+             ("Z=P W   (l3 half)", NL, 41, 256, "nn"), ("G=P^T m (l1 half)", 602, 256, NL, "tn"),
+             ("G=P^T m (l3 half)", 256, 41, NL, "tn"), ("T=m W^T (l2)", NL, 256, 256, "nt"),
+             ("T=m W^T (l3)", NL, 256, 41, "nt")]
+    ws = torch.empty(64 * 602 * 256, device="cuda")
+    for name, M, N, K, kind in cases:
+        if kind == "nn":
+            A = torch.randn(M, K, device="cuda", generator=g); B = torch.randn(K, N, device="cuda", generator=g)
+        elif kind == "tn":
+            A = torch.randn(K, M, device="cuda", generator=g).t(); B = torch.randn(K, N, device="cuda", generator=g)
+        else:
+            A = torch.randn(M, K, device="cuda", generator=g); B = torch.randn(N, K, device="cuda", generator=g).t()
+        C = torch.empty(M, N, device="cuda")
+        ms = _time(lambda: ops.gemm(A, B, C, ws=ws), reps=5)
+        ms_cb = _time(lambda: torch.mm(A, B, out=C), reps=5)
+        fl = 2.0 * M * N * K
+        print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_ms": ms, "cublas_fp32_ms": ms_cb,
+                          "tcgen05_tflops": fl / ms / 1e9, "cublas_tflops": fl / ms_cb / 1e9}), flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["codec", "spmm"])
+    ap.add_argument("what", choices=["codec", "spmm", "gemm"])
     ap.add_argument("--rows", type=int, default=461_644)
     ap.add_argument("--d", type=int, default=602)
     ap.add_argument("--bits", type=int, default=1)
     ap.add_argument("--segs", type=int, default=56)
     ap.add_argument("--config", default="reddit")
     a = ap.parse_args()
-    {"codec": codec, "spmm": spmm}[a.what](a)
+    {"codec": codec, "spmm": spmm, "gemm": gemm}[a.what](a)
