@@ -172,7 +172,7 @@ class DeviceRank:
 
     def __init__(self, layout: RankLayout, cfg: ModelConfig, mode: TrainMode, quant: QuantConfig,
                  seed: int, lr: float, global_norm: int, device=None, group=None, probe=None,
-                 features=None):
+                 features=None, agg_order=None):
         import torch
         self.torch = torch
         self.dev = torch.device(device or "cuda")
@@ -203,11 +203,28 @@ class DeviceRank:
         self.Ht[1][:NL, :W[0]] = torch.from_numpy(np.ascontiguousarray(feats, dtype=np.float32)).to(dev)
         self.drop = cfg.dropout > 0.0
         self.Hd = {l: torch.zeros_like(self.Ht[l]) for l in range(1, L + 1)} if self.drop else self.Ht
-        self.AGG = {l: torch.zeros((NL, _ld(W[l - 1])), dtype=f32, device=dev) for l in range(1, L + 1)}
+        self.gemm_impl = os.environ.get("HB_GEMM", "cublas")
+        # aggregation order per layer (see choose_agg_order)
+        order = agg_order or os.environ.get("HB_AGG_ORDER", "auto")
+        if order not in AGG_ORDERS:
+            raise TrainingError(f"unknown aggregation order {order!r}")
+        self.post = {}
+        for l in range(1, L + 1):
+            o = order if order != "auto" else choose_agg_order(
+                l, W[l - 1], W[l], self.A.nnz, NL, NL + NH, cfg.model, self.gemm_impl)
+            self.post[l] = o == "post"
+        # pre: AGG = A h~ (width d_in); post: Y = h~ W_bot, AGG = A Y (width d_out)
+        self.AGG = {l: torch.zeros((NL, _ld(W[l] if self.post[l] else W[l - 1])), dtype=f32, device=dev)
+                    for l in range(1, L + 1)}
+        self.Y = {l: torch.zeros((NL + NH, _ld(W[l])), dtype=f32, device=dev)
+                  for l in range(1, L + 1) if self.post[l]}
+        self.S = {l: torch.zeros((NL + NH, _ld(W[l])), dtype=f32, device=dev)
+                  for l in range(1, L + 1) if self.post[l]}
         self.Z = {l: torch.zeros((NL, W[l]), dtype=f32, device=dev) for l in range(1, L + 1)}
         self.JF = {l: torch.zeros((NL + NH, _ld(W[l - 1])), dtype=f32, device=dev) for l in range(2, L + 1)}
-        self.T = {l: torch.zeros((NL, W[l - 1]), dtype=f32, device=dev) for l in range(2, L + 1)}
-        self.JL = torch.zeros((NL, W[L]), dtype=f32, device=dev)
+        self.T = {l: torch.zeros((NL, _ld(W[l - 1])), dtype=f32, device=dev)
+                  for l in range(2, L + 1) if not self.post[l]}
+        self.JL = torch.zeros((NL, _ld(W[L])), dtype=f32, device=dev)
         self.row_loss = torch.zeros(max(1, NL), dtype=torch.float64, device=dev)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -235,7 +252,6 @@ class DeviceRank:
             self.G.append(self.gflat[off:off + w.numel()].view_as(w))
             off += w.numel()
         # split-K workspace for the weight-gradient GEMM (G = P^T m, K = rows)
-        self.gemm_impl = os.environ.get("HB_GEMM", "cublas")
         gmax = max(w.numel() for w in self.W)
         self.gemm_ws = torch.empty(64 * gmax, dtype=f32, device=dev)
         self.adam_m = [torch.zeros_like(w) for w in self.W]
@@ -371,30 +387,97 @@ class DeviceRank:
             if training and self.drop:
                 Hd = self.Hd[l]
                 self._dropout(H, Hd, epoch, l, d)
-            agg = self.AGG[l]
-            with self.timer("spmm", *_spmm_cost(self.A, d)):
-                ops.spmm(self.A, Hd, agg, d)
-            self.launches += 1
-            Z = self.Z[l]
-            hout = self.Ht[l + 1][:NL, :W[l]] if l < L else None
-            with self.timer("gemm", 0, 2 * NL * self.W[l - 1].shape[0] * W[l]):
-                if self.gemm_impl == "cublas":
-                    if self.cfg.model == "sage":
-                        torch.mm(Hd[:NL, :d], self.W[l - 1][:d], out=Z)
-                        Z.addmm_(agg[:, :d], self.W[l - 1][d:])
-                    else:
-                        torch.mm(agg[:, :d], self.W[l - 1], out=Z)
-                    if hout is not None:
-                        ops.relu(Z, self.Ht[l + 1], NL, W[l])
-                        self.launches += 1
-                elif self.cfg.model == "sage":
-                    ops.gemm(Hd[:NL, :d], self.W[l - 1][:d], Z)
-                    ops.gemm(agg[:, :d], self.W[l - 1][d:], Z, beta=1.0, relu_out=hout)
-                    self.launches += 2
-                else:
-                    ops.gemm(agg[:, :d], self.W[l - 1], Z, relu_out=hout)
-                    self.launches += 1
+            self._layer_forward(l, Hd)
         return self.Z[L]
+
+    # -- dense combine + aggregation of one layer --------------------------------
+    def _mm(self, a, b, out, accumulate: bool = False, relu_out=None):
+        """out (+)= a @ b (trainer.py:294,313,318-321)."""
+        nl, nc = out.shape
+        with self.timer("gemm", 0, 2 * a.shape[0] * a.shape[1] * b.shape[1]):
+            if self.gemm_impl == "cublas":
+                if accumulate:
+                    out.addmm_(a, b)
+                else:
+                    self.torch.mm(a, b, out=out)
+                if relu_out is not None:
+                    ops.relu(out, relu_out, nl, nc)
+                    self.launches += 1
+            else:
+                ops.gemm(a, b, out, beta=1.0 if accumulate else 0.0, relu_out=relu_out, ws=self.gemm_ws)
+                self.launches += 1
+
+    def _spmm(self, a, x, y, d: int):
+        with self.timer("spmm", *_spmm_cost(a, d)):
+            ops.spmm(a, x, y, d)
+        self.launches += 1
+
+    def _layer_forward(self, l: int, Hd):
+        """p = A h~ (SAGE: [h~_local | M h~]); z = p W; h = relu(z) (trainer.py:290-295).
+
+        pre order (the reference's): AGG = A h~ at width d_in, then the GEMM.
+        post order: Y = h~ W_bot over local+halo rows, AGG = A Y at width d_out,
+        z = h~_local W_top + AGG — the same z up to fp32 summation order, with
+        the SpMM at the narrower width (DGL applies the same reordering)."""
+        W, NL = self.cfg.widths, self.NL
+        d, dout = W[l - 1], W[l]
+        sage = self.cfg.model == "sage"
+        Wl = self.W[l - 1]
+        Wtop, Wbot = (Wl[:d], Wl[d:]) if sage else (None, Wl)
+        Z, agg = self.Z[l], self.AGG[l]
+        hout = self.Ht[l + 1][:NL, :dout] if l < self.L else None
+        if not self.post[l]:
+            self._spmm(self.A, Hd, agg, d)
+            if sage:
+                self._mm(Hd[:NL, :d], Wtop, Z)
+                self._mm(agg[:, :d], Wbot, Z, accumulate=True, relu_out=hout)
+            else:
+                self._mm(agg[:, :d], Wbot, Z, relu_out=hout)
+            return
+        Y = self.Y[l]
+        self._mm(Hd[:, :d], Wbot, Y[:, :dout])
+        if sage:
+            self._spmm(self.A, Y, agg, dout)
+            Z.copy_(agg[:, :dout])
+            self._mm(Hd[:NL, :d], Wtop, Z, accumulate=True, relu_out=hout)
+        else:
+            self._spmm(self.A, Y, agg, dout)
+            if hout is not None:
+                ops.relu(agg, self.Ht[l + 1], NL, dout)
+                self.launches += 1
+            else:
+                Z.copy_(agg[:, :dout])
+
+    def _layer_backward(self, l: int, m, JF):
+        """G = p^T m; j_full = A^T (m W_bot^T) (+ SAGE local m W_top^T)
+        (trainer.py:313-321).  post order: S = A^T m at width d_out, then
+        G_bot = h~^T S and j_full = S W_bot^T."""
+        W, NL = self.cfg.widths, self.NL
+        d, dout = W[l - 1], W[l]
+        sage = self.cfg.model == "sage"
+        Hd = self.Hd[l] if self.drop else self.Ht[l]
+        Wl, G = self.W[l - 1], self.G[l - 1]
+        Gtop, Gbot = (G[:d], G[d:]) if sage else (None, G)
+        Wtop, Wbot = (Wl[:d], Wl[d:]) if sage else (None, Wl)
+        if sage:
+            self._mm(Hd[:NL, :d].t(), m, Gtop)
+        if not self.post[l]:
+            agg = self.AGG[l]
+            self._mm(agg[:, :d].t(), m, Gbot)
+            if JF is None:
+                return
+            T = self.T[l]
+            self._mm(m, Wbot.t(), T[:, :d])
+            self._spmm(self.At, T, JF, d)
+        else:
+            S = self.S[l]
+            self._spmm(self.At, m, S, dout)
+            self._mm(Hd[:, :d].t(), S[:, :dout], Gbot)
+            if JF is None:
+                return
+            self._mm(S[:, :dout], Wbot.t(), JF[:, :d])
+        if sage:
+            self._mm(m, Wtop.t(), JF[:NL, :d], accumulate=True)
 
     def _probe_halo(self, epoch, layer, tag, H, d):
         lay = self.layout
@@ -420,44 +503,11 @@ class DeviceRank:
                     ops.relu_grad_mul(J, self.Ht[l + 1], J, NL, dout)
                 self.launches += 1
             m = J[:, :dout]
-            Hd = self.Hd[l] if self.drop else self.Ht[l]
-            agg = self.AGG[l]
-            G = self.G[l - 1]
-            with self.timer("gemm", 0, 2 * NL * G.shape[0] * dout):
-                if self.gemm_impl == "cublas":
-                    if self.cfg.model == "sage":
-                        torch.mm(Hd[:NL, :d].t(), m, out=G[:d])
-                        torch.mm(agg[:, :d].t(), m, out=G[d:])
-                    else:
-                        torch.mm(agg[:, :d].t(), m, out=G)
-                elif self.cfg.model == "sage":
-                    ops.gemm(Hd[:NL, :d].t(), m, G[:d], ws=self.gemm_ws)
-                    ops.gemm(agg[:, :d].t(), m, G[d:], ws=self.gemm_ws)
-                    self.launches += 4
-                else:
-                    ops.gemm(agg[:, :d].t(), m, G, ws=self.gemm_ws)
-                    self.launches += 2
             if l == 1:
+                self._layer_backward(l, m, None)
                 break
-            T, JF = self.T[l], self.JF[l]
-            Wl = self.W[l - 1]
-            with self.timer("gemm", 0, 2 * NL * d * dout):
-                Wb = (Wl[d:] if self.cfg.model == "sage" else Wl).t()
-                if self.gemm_impl == "cublas":
-                    torch.mm(m, Wb, out=T)
-                else:
-                    ops.gemm(m, Wb, T)
-                    self.launches += 1
-            with self.timer("spmm", *_spmm_cost(self.At, d)):
-                ops.spmm(self.At, T, JF, d)
-            if self.cfg.model == "sage":
-                with self.timer("gemm", 0, 2 * NL * d * dout):
-                    if self.gemm_impl == "cublas":
-                        JF[:NL, :d].addmm_(m, Wl[:d].t())
-                    else:
-                        ops.gemm(m, Wl[:d].t(), JF[:NL, :d], beta=1.0)
-                        self.launches += 1
-            self.launches += 1
+            JF = self.JF[l]
+            self._layer_backward(l, m, JF)
             if self.drop:
                 self._dropout(JF, JF, epoch, l, d)
             bufs = self.xb[l]
@@ -541,6 +591,30 @@ class DeviceRank:
         return t.snapshot()
 
 
+AGG_ORDERS = ("pre", "post", "auto")
+# Effective rates behind the per-layer aggregation-order choice, measured on
+# the B200 (bench r1): the SpMM moves ~17 TB/s of gathered X rows out of L2;
+# the GEMM rate depends on the implementation.
+SPMM_GATHER_BPS = 17e12
+GEMM_FLOPS = {"cublas": 40e12, "tcgen05": 250e12}
+
+
+def choose_agg_order(layer: int, d_in: int, d_out: int, nnz: int, nl: int, nrows: int, model: str,
+                     gemm_impl: str = "cublas") -> str:
+    """'pre' (aggregate the d_in-wide input, the reference's order) or 'post'
+    (project to d_out first, aggregate the d_out-wide product), whichever
+    moves fewer bytes/flops under the measured rates.  Layer 1 has no
+    backward SpMM in 'pre' order (no j_full), but always has one in 'post'
+    (for G_bot = h~^T A^T m)."""
+    fan = 2 if model == "sage" else 1
+    bwd = 1 if layer > 1 else 0
+    rate = GEMM_FLOPS.get(gemm_impl, GEMM_FLOPS["cublas"])
+    spmm = lambda w: 4.0 * nnz * w / SPMM_GATHER_BPS  # noqa: E731
+    pre = spmm(d_in) * (1 + bwd) + 2.0 * nl * fan * d_in * d_out * (2 + bwd) / rate
+    post = 2 * spmm(d_out) + 2.0 * d_in * d_out * (nrows + (fan - 1) * nl) * (2 + bwd) / rate
+    return "post" if post < pre else "pre"
+
+
 def _spmm_cost(a, d: int):
     """(compulsory HBM bytes, flops) of one SpMM launch: CSR arrays + every X
     row read once + Y written once; 2 flops per nonzero per column."""
@@ -558,7 +632,8 @@ def _dist_initialized() -> bool:
 
 def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMode,
           quant_cfg: QuantConfig, epochs: int, seed: int, lr: float = 0.01, probe=None,
-          timeout: float = 60.0, device=None, evaluate_each_epoch: bool = True) -> TrainResult:
+          timeout: float = 60.0, device=None, evaluate_each_epoch: bool = True,
+          agg_order: str | None = None) -> TrainResult:
     """Drop-in for ``halobit.train`` (trainer.py:386-465) on one GPU: every
     partition is hosted by this process's device (the reference's one-process
     simulation, with device-resident halo traffic)."""
@@ -567,7 +642,7 @@ def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMod
     global_norm = max(1, int(np.asarray(graph.train_mask).sum()))
     layout = RankLayout({p.id: p for p in partitions}, [0] * n, 0)
     eng = DeviceRank(layout, model_cfg, mode, quant_cfg, seed, lr, global_norm, device=device,
-                     probe=probe)
+                     probe=probe, agg_order=agg_order)
     if epochs == 0:
         return TrainResult([], init_weights(model_cfg, seed))
     ar_per_epoch = (4 * sum(int(w.numel()) for w in eng.W)) if n > 1 else 0

@@ -37,13 +37,14 @@ def _f32(parts):
     return [np.asarray(p.features, dtype=np.float32).astype(np.float64) for p in parts]
 
 
-def _run_both(g, n, widths, model, variant, st, bits, epochs, seed, dropout=0.0, strategy="contiguous"):
+def _run_both(g, n, widths, model, variant, st, bits, epochs, seed, dropout=0.0, strategy="contiguous",
+              agg_order=None):
     from oracle.epoch import OracleTrainer
     from paper_2303_01277_b200.codec import QuantConfig
     from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
     parts = _parts(g, n, model, strategy)
     res = train(g, parts, ModelConfig(widths, model, dropout), TrainMode(variant, st),
-                QuantConfig(bits), epochs, seed)
+                QuantConfig(bits), epochs, seed, agg_order=agg_order)
     o = OracleTrainer(parts, widths, model, variant, st, bits, seed, dropout=dropout,
                       features=_f32(parts))
     losses, bytes_ = [], []
@@ -62,30 +63,36 @@ def _wdiff(a, b):
     return max(np.abs(x - y).max() for x, y in zip(a, b)) / scale
 
 
+@pytest.mark.parametrize("order", ["pre", "post"])
 @pytest.mark.parametrize("model", ["gcn", "sage"])
 @pytest.mark.parametrize("n", [1, 2, 4])
-def test_passthrough_trajectory_matches_oracle(model, n):
+def test_passthrough_trajectory_matches_oracle(model, n, order):
+    """Both aggregation orders (reference order A(hW) vs (Ah)W) track the oracle."""
     g = _graph()
-    res, o, losses, bytes_ = _run_both(g, n, (32, 16, 4), model, "sync", 0, 32, 10, 2)
+    res, o, losses, bytes_ = _run_both(g, n, (32, 16, 4), model, "sync", 0, 32, 10, 2, agg_order=order)
     for m, lo, by in zip(res.metrics, losses, bytes_):
         assert m.train_loss == pytest.approx(lo, rel=5e-5)
         assert (m.main_bytes, m.meta_bytes, m.header_bytes, m.messages, m.allreduce_bytes) == by
     assert _wdiff(res.final_weights, o.weights) < 1e-4
 
 
+@pytest.mark.parametrize("order", ["pre", "post"])
 @pytest.mark.parametrize("variant,st", [("sync", 0), ("async", 0), ("async", 2), ("async", 3)])
-def test_modes_bytes_and_schedule_match_oracle(variant, st):
+def test_modes_bytes_and_schedule_match_oracle(variant, st, order):
     g = _graph(seed=5, npc=30)
-    res, o, losses, bytes_ = _run_both(g, 3, (32, 16, 8, 4), "sage", variant, st, 32, 6, 3)
+    res, o, losses, bytes_ = _run_both(g, 3, (32, 16, 8, 4), "sage", variant, st, 32, 6, 3,
+                                       agg_order=order)
     for m, lo, by in zip(res.metrics, losses, bytes_):
         assert (m.main_bytes, m.meta_bytes, m.header_bytes, m.messages, m.allreduce_bytes) == by
         assert m.train_loss == pytest.approx(lo, rel=5e-5)
     assert _wdiff(res.final_weights, o.weights) < 1e-4
 
 
-def test_dropout_trajectory_matches_oracle():
+@pytest.mark.parametrize("order", ["pre", "post"])
+def test_dropout_trajectory_matches_oracle(order):
     g = _graph(seed=9, npc=20)
-    res, o, losses, _ = _run_both(g, 2, (32, 16, 4), "gcn", "sync", 0, 32, 5, 7, dropout=0.3)
+    res, o, losses, _ = _run_both(g, 2, (32, 16, 4), "gcn", "sync", 0, 32, 5, 7, dropout=0.3,
+                                  agg_order=order)
     for m, lo in zip(res.metrics, losses):
         assert m.train_loss == pytest.approx(lo, rel=5e-5)
     assert _wdiff(res.final_weights, o.weights) < 1e-4
