@@ -106,6 +106,12 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
                 const float* B, int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta,
                 float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream);
 
+/* Selects the K5-K7 kernel: 0 = TMA-fed warp-specialised tcgen05 kernel
+ * whenever both operands are TMA-describable (16-byte aligned, unit stride on
+ * one axis, 16-byte row stride), else the SIMT-staged tcgen05 kernel;
+ * 1 = SIMT-staged kernel only (tests compare the two). */
+int hb_gemm_set_path(int32_t path);
+
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:
  * grad rows outside the mask are zero, masked rows get (softmax - onehot)/norm;
  * row_loss[i] = -log softmax[label] / norm (0 outside the mask) in f64.

@@ -27,6 +27,7 @@ cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, u
 
 cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
                                float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+extern int g_gemm_path;
 
 int num_sms() {
   static int cached = 0;
@@ -104,6 +105,12 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
   return check(hb::launch_gemm_tf32x3(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                       ws_floats, S(stream)),
                "hb_gemm_f32");
+}
+
+int hb_gemm_set_path(int32_t path) {
+  if (path < 0 || path > 1) return fail(HB_EINVAL, "hb_gemm_set_path: path must be 0 (auto) or 1 (SIMT-staged)");
+  hb::g_gemm_path = path;
+  return HB_OK;
 }
 
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

@@ -208,11 +208,12 @@ gemm_tf32x3_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda
   for (int c0 = 0; c0 < BN; c0 += 8) {
     uint32_t r[8];
     const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+                 "tcgen05.wait::ld.sync.aligned;"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                    "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
+                 : "r"(taddr)
+                 : "memory");
     if (row < M) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -288,11 +289,21 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
   return cudaSuccess;
 }
 
+cudaError_t launch_gemm_tma(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
+                            int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+
+int g_gemm_path = 0;   // 0: TMA warp-specialised kernel when operands allow; 1: SIMT-staged kernel only
+
 cudaError_t launch_gemm_tf32x3(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
                                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
                                int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K <= 0) return cudaErrorInvalidValue;
+  if (g_gemm_path == 0) {
+    const cudaError_t e = launch_gemm_tma(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr,
+                                          ws, ws_floats, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (N <= 32) return launch_bn<32>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   if (N <= 64) return launch_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   if (N <= 128) return launch_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);

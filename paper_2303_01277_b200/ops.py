@@ -48,6 +48,11 @@ def gemm(A, B, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
     return C
 
 
+def gemm_set_path(path: int):
+    """0: TMA warp-specialised tcgen05 kernel where operands allow; 1: SIMT-staged kernel."""
+    _lib.call("hb_gemm_set_path", int(path))
+
+
 def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None):
     """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device."""
     n = labels.numel()

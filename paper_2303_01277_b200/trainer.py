@@ -203,7 +203,9 @@ class DeviceRank:
         self.Ht[1][:NL, :W[0]] = torch.from_numpy(np.ascontiguousarray(feats, dtype=np.float32)).to(dev)
         self.drop = cfg.dropout > 0.0
         self.Hd = {l: torch.zeros_like(self.Ht[l]) for l in range(1, L + 1)} if self.drop else self.Ht
-        self.gemm_impl = os.environ.get("HB_GEMM", "cublas")
+        self.gemm_impl = os.environ.get("HB_GEMM", "tcgen05")
+        if self.gemm_impl not in GEMM_FLOPS:
+            raise TrainingError(f"unknown GEMM implementation {self.gemm_impl!r}")
         # aggregation order per layer (see choose_agg_order)
         order = agg_order or os.environ.get("HB_AGG_ORDER", "auto")
         if order not in AGG_ORDERS:
@@ -243,19 +245,28 @@ class DeviceRank:
             off += n
         self.eval_mask = torch.from_numpy(em).to(dev)
         # parameters (replicated; identical Glorot init on every rank, no broadcast)
+        # Stored with 16-byte row strides (columns padded to a multiple of 4, pad
+        # entries stay exactly 0 through Adam) so every GEMM operand is
+        # TMA-describable; W / G are the logical (fan_in x d_out) views.
         w0 = init_weights(cfg, seed)
-        self.W = [torch.from_numpy(w.astype(np.float32)).to(dev) for w in w0]
-        self.gflat = torch.zeros(sum(w.numel() for w in self.W), dtype=f32, device=dev)
+        self.Wp, self.Gp = [], []
+        gsize = sum(w.shape[0] * _ld(w.shape[1]) for w in w0)
+        self.gflat = torch.zeros(gsize, dtype=f32, device=dev)
         off = 0
-        self.G = []
-        for w in self.W:
-            self.G.append(self.gflat[off:off + w.numel()].view_as(w))
-            off += w.numel()
+        for w in w0:
+            r, c = w.shape
+            wp = torch.zeros((r, _ld(c)), dtype=f32, device=dev)
+            wp[:, :c] = torch.from_numpy(w.astype(np.float32)).to(dev)
+            self.Wp.append(wp)
+            self.Gp.append(self.gflat[off:off + wp.numel()].view_as(wp))
+            off += wp.numel()
+        self.W = [wp[:, :w.shape[1]] for wp, w in zip(self.Wp, w0)]
+        self.G = [gp[:, :w.shape[1]] for gp, w in zip(self.Gp, w0)]
         # split-K workspace for the weight-gradient GEMM (G = P^T m, K = rows)
-        gmax = max(w.numel() for w in self.W)
+        gmax = max(w.numel() for w in self.Wp)
         self.gemm_ws = torch.empty(64 * gmax, dtype=f32, device=dev)
-        self.adam_m = [torch.zeros_like(w) for w in self.W]
-        self.adam_v = [torch.zeros_like(w) for w in self.W]
+        self.adam_m = [torch.zeros_like(w) for w in self.Wp]
+        self.adam_v = [torch.zeros_like(w) for w in self.Wp]
         self.adam_t = 0
         # exchange buffers
         par = 2 if mode.variant == "async" else 1
@@ -536,7 +547,7 @@ class DeviceRank:
             dist.all_reduce(self.gflat, group=self.group)
             dist.all_reduce(self.loss_dev, group=self.group)
         self.adam_t += 1
-        for w, g, m, v in zip(self.W, self.G, self.adam_m, self.adam_v):
+        for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
             ops.adam_step(w, g, m, v, self.lr, self.adam_t)
             self.launches += 1
 
@@ -596,7 +607,7 @@ AGG_ORDERS = ("pre", "post", "auto")
 # the B200 (bench r1): the SpMM moves ~17 TB/s of gathered X rows out of L2;
 # the GEMM rate depends on the implementation.
 SPMM_GATHER_BPS = 17e12
-GEMM_FLOPS = {"cublas": 40e12, "tcgen05": 250e12}
+GEMM_FLOPS = {"cublas": 40e12, "tcgen05": 150e12}
 
 
 def choose_agg_order(layer: int, d_in: int, d_out: int, nnz: int, nl: int, nrows: int, model: str,

@@ -108,19 +108,26 @@ def gemm(args):
              ("G=P^T m (l3 half)", 256, 41, NL, "tn"), ("T=m W^T (l2)", NL, 256, 256, "nt"),
              ("T=m W^T (l3)", NL, 256, 41, "nt")]
     ws = torch.empty(64 * 602 * 256, device="cuda")
+    def mat(r, c):   # row-major with a 16-byte row stride, like the trainer's buffers
+        return torch.randn(r, (c + 3) // 4 * 4, device="cuda", generator=g)[:, :c]
     for name, M, N, K, kind in cases:
         if kind == "nn":
-            A = torch.randn(M, K, device="cuda", generator=g); B = torch.randn(K, N, device="cuda", generator=g)
+            A, B = mat(M, K), mat(K, N)
         elif kind == "tn":
-            A = torch.randn(K, M, device="cuda", generator=g).t(); B = torch.randn(K, N, device="cuda", generator=g)
+            A, B = mat(K, M).t(), mat(K, N)
         else:
-            A = torch.randn(M, K, device="cuda", generator=g); B = torch.randn(N, K, device="cuda", generator=g).t()
+            A, B = mat(M, K), mat(N, K).t()
         C = torch.empty(M, N, device="cuda")
         ms = _time(lambda: ops.gemm(A, B, C, ws=ws), reps=5)
+        ops.gemm_set_path(1)
+        ms_v1 = _time(lambda: ops.gemm(A, B, C, ws=ws), reps=5)
+        ops.gemm_set_path(0)
         ms_cb = _time(lambda: torch.mm(A, B, out=C), reps=5)
         fl = 2.0 * M * N * K
-        print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_ms": ms, "cublas_fp32_ms": ms_cb,
-                          "tcgen05_tflops": fl / ms / 1e9, "cublas_tflops": fl / ms_cb / 1e9}), flush=True)
+        print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_tma_ms": round(ms, 4),
+                          "tcgen05_simt_staged_ms": round(ms_v1, 4), "cublas_fp32_ms": round(ms_cb, 4),
+                          "tcgen05_tflops": round(fl / ms / 1e9, 1), "cublas_tflops": round(fl / ms_cb / 1e9, 1)}),
+              flush=True)
 
 
 if __name__ == "__main__":
