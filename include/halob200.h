@@ -95,6 +95,32 @@ int hb_dequant_gather(const hb_segment_t* segs, int32_t nseg, int32_t num_dst,
 int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream);
 
+/* K3/K4 with the algorithm exposed: algo 0 = auto (column sweep when the rows
+ * average >= 32 nonzeros, i.e. nnz >= 32 * nrows, and d > 64), 1 = row
+ * gather (one warp, or a sub-warp group for d <= 64, per row), 2 = column
+ * sweep (CTA-wide lockstep column windows so X rows are reused from L1 across
+ * the block's rows; d > 64).  window = X rows per sweep window (0 = auto,
+ * ~64 KB).  Same result contract as hb_spmm_csr. */
+int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+                   const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
+                   int32_t window, void* stream);
+
+/* K3/K4 tiled path (same result contract as hb_spmm_csr, fp32 accumulation
+ * in tile-then-residual order).  The matrix is pre-split (ops.TiledCsr, built
+ * on the device from the CSR) into dense tiles of 64 rows x 64 columns —
+ * tile_ptr[b]..tile_ptr[b+1] are the tiles of row block b (nblocks =
+ * ceil(nrows / 64)), tile_win[t] the tile's column window (columns
+ * 64*win .. +63), tile_nz[tile_off[t] .. tile_off[t+1]) its row-sorted
+ * records {int32 col - 64*win, float val} (offsets even: 16-byte aligned),
+ * tile_rowoff[t*72 .. +65) the records' row offsets — and a residual CSR
+ * (res_ptr / res_col / res_val over all nrows) for every other nonzero.
+ * X windows (64 rows x 128/256-column panels) are staged in shared memory by
+ * TMA; xrows = rows of X.  X and Y rows must be 16-byte aligned. */
+int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
+                  const int64_t* tile_off, const uint16_t* tile_rowoff, const void* tile_nz, const int64_t* res_ptr,
+                  const int32_t* res_col, const float* res_val, const float* X, int64_t ldx, int32_t d, float* Y,
+                  int64_t ldy, void* stream);
+
 /* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
  * tensor cores with the 3xTF32 split (fp32 accuracy):
  *   C[m, n] = sum_k A(m, k) B(k, n) (+ beta * C[m, n])

@@ -12,7 +12,7 @@ cudaError_t launch_dequant_gather(const hb_segment_t*, int, int, const int32_t*,
                                   const int32_t*, int, int, float*, int64_t, int, cudaStream_t);
 cudaError_t launch_philox_uniforms(uint64_t, uint64_t, uint64_t, int64_t, double*, cudaStream_t);
 cudaError_t launch_spmm(int, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
-                        float*, int64_t, cudaStream_t);
+                        float*, int64_t, int64_t, int, int, cudaStream_t);
 cudaError_t launch_xent(const float*, int64_t, int, int, const int32_t*, const uint8_t*, double, float*,
                         int64_t, double*, double*, cudaStream_t);
 cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaStream_t);
@@ -28,6 +28,9 @@ cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, u
 cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
                                float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_path;
+cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
+                              const int2*, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
+                              float*, int64_t, cudaStream_t);
 
 int num_sms() {
   static int cached = 0;
@@ -94,7 +97,32 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)))
     return fail(HB_EINVAL, "hb_spmm_csr: bad arguments");
-  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, S(stream)), "hb_spmm_csr");
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, -1, 1, 0, S(stream)),
+               "hb_spmm_csr");
+}
+
+int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+                   const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
+                   int32_t window, void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)) || algo < 0 || algo > 2)
+    return fail(HB_EINVAL, "hb_spmm_csr_ex: bad arguments");
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, nnz, algo, window, S(stream)),
+               "hb_spmm_csr_ex");
+}
+
+int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
+                  const int64_t* tile_off, const uint16_t* tile_rowoff, const void* tile_nz, const int64_t* res_ptr,
+                  const int32_t* res_col, const float* res_val, const float* X, int64_t ldx, int32_t d, float* Y,
+                  int64_t ldy, void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || nblocks != (nrows + 63) / 64 ||
+      (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y)))
+    return fail(HB_EINVAL, "hb_spmm_tiled: bad arguments");
+  const cudaError_t e = hb::launch_spmm_tiled(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_rowoff,
+                                              reinterpret_cast<const int2*>(tile_nz), res_ptr, res_col, res_val, X,
+                                              ldx, d, Y, ldy, S(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(HB_EINVAL, "hb_spmm_tiled: X/Y need 16-byte aligned rows (ld % 4 == 0)");
+  return check(e, "hb_spmm_tiled");
 }
 
 int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,

@@ -27,11 +27,93 @@ class DeviceCsr:
         return cls(m.rows, m.cols, m.row_ptr, m.col_idx, m.values, device)
 
 
-def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None):
+class TiledCsr:
+    """The K3/K4 tiled layout of a ``DeviceCsr`` (built on the device, once per
+    matrix): dense (64-row block x 64-column window) tiles holding at least
+    ``threshold`` nonzeros — their X windows are staged in shared memory by TMA
+    and reused across the block's rows — and a residual CSR for the rest.
+    Tile records keep the CSR's (row, column) order, so each row still sums its
+    tile contributions in ascending column order, then its residual ones."""
+
+    RB = 64
+    W = 64
+    ROWOFF = 72
+
+    def __init__(self, a: DeviceCsr, threshold: int = 64):
+        import torch
+        dev = a.row_ptr.device
+        self.rows, self.cols, self.nnz = a.rows, a.cols, a.nnz
+        self.nblocks = (a.rows + self.RB - 1) // self.RB
+        nwin = (a.cols + self.W - 1) // self.W
+        counts_row = a.row_ptr[1:] - a.row_ptr[:-1]
+        rows = torch.repeat_interleave(torch.arange(a.rows, device=dev, dtype=torch.int64), counts_row)
+        col = a.col_idx.long()
+        key = (rows // self.RB) * nwin + col // self.W
+        order = torch.sort(key, stable=True).indices          # (block, window) groups, CSR order inside
+        skey = key[order]
+        del key
+        uniq, cnt = torch.unique_consecutive(skey, return_counts=True)
+        dense_g = cnt >= threshold
+        gid = torch.repeat_interleave(torch.arange(len(uniq), device=dev), cnt)
+        dense_nz = dense_g[gid]
+        tile_key, tile_cnt = uniq[dense_g], cnt[dense_g]
+        self.ntiles = int(tile_key.numel())
+        tile_blk = tile_key // nwin
+        self.tile_win = (tile_key % nwin).to(torch.int32).contiguous()
+        tp = torch.zeros(self.nblocks + 1, dtype=torch.int64, device=dev)
+        tp[1:] = torch.cumsum(torch.bincount(tile_blk, minlength=self.nblocks), 0)
+        self.tile_ptr = tp.to(torch.int32)
+        padded = (tile_cnt + 1) // 2 * 2                      # 16-byte aligned record runs
+        off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
+        off[1:] = torch.cumsum(padded, 0)
+        self.tile_off = off
+        didx = order[dense_nz]                                # original nonzero ids, tile order
+        tile_of = (torch.cumsum(dense_g.long(), 0) - 1)[gid[dense_nz]]
+        start = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
+        start[1:] = torch.cumsum(tile_cnt, 0)
+        rank = torch.arange(didx.numel(), device=dev) - start[tile_of]
+        pos = off[tile_of] + rank
+        nz = torch.zeros((int(off[-1].item()), 2), dtype=torch.int32, device=dev)
+        nz[pos, 0] = (col[didx] - self.tile_win.long()[tile_of] * self.W).to(torch.int32)
+        nz[pos, 1] = a.values[didx].view(torch.int32)
+        self.tile_nz = nz
+        lr = rows[didx] % self.RB
+        per = torch.bincount(tile_of * self.RB + lr, minlength=self.ntiles * self.RB).view(self.ntiles, self.RB)
+        ro = torch.zeros((self.ntiles, self.ROWOFF), dtype=torch.int32, device=dev)
+        ro[:, 1:self.RB + 1] = torch.cumsum(per, 1)
+        self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= 4096, read as uint16
+        keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
+        keep[didx] = False
+        rp = torch.zeros(a.rows + 1, dtype=torch.int64, device=dev)
+        rp[1:] = torch.cumsum(torch.bincount(rows[keep], minlength=a.rows), 0)
+        self.res_ptr = rp
+        self.res_col = a.col_idx[keep].contiguous()
+        self.res_val = a.values[keep].contiguous()
+        self.tiled_nnz = int(didx.numel())
+
+    @property
+    def tiled_fraction(self) -> float:
+        return self.tiled_nnz / max(1, self.nnz)
+
+
+def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
+    """``linalg.spmm`` (linalg.py:71-75) through the TMA-staged tiled kernel."""
+    d = x.shape[1] if d is None else d
+    _lib.call("hb_spmm_tiled", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win), ptr(t.tile_off),
+              ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col), ptr(t.res_val), ptr(x),
+              x.stride(0), d, ptr(out), out.stride(0), stream_handle(stream))
+    return out
+
+
+SPMM_ALGOS = {"auto": 0, "rows": 1, "sweep": 2}
+
+
+def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "auto", window: int = 0):
     """``linalg.spmm`` (linalg.py:71-75): out[:rows, :d] = A @ x[:, :d]."""
     d = x.shape[1] if d is None else d
-    _lib.call("hb_spmm_csr", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
-              x.stride(0), d, ptr(out), out.stride(0), stream_handle(stream))
+    _lib.call("hb_spmm_csr_ex", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
+              x.stride(0), d, ptr(out), out.stride(0), a.nnz, SPMM_ALGOS[algo], int(window),
+              stream_handle(stream))
     return out
 
 

@@ -203,6 +203,10 @@ class DeviceRank:
         self.Ht[1][:NL, :W[0]] = torch.from_numpy(np.ascontiguousarray(feats, dtype=np.float32)).to(dev)
         self.drop = cfg.dropout > 0.0
         self.Hd = {l: torch.zeros_like(self.Ht[l]) for l in range(1, L + 1)} if self.drop else self.Ht
+        self.spmm_impl = os.environ.get("HB_SPMM", "auto")
+        if self.spmm_impl not in ("auto", "rows", "tiled"):
+            raise TrainingError(f"unknown SpMM implementation {self.spmm_impl!r}")
+        self._tiles = {}
         self.gemm_impl = os.environ.get("HB_GEMM", "tcgen05")
         if self.gemm_impl not in GEMM_FLOPS:
             raise TrainingError(f"unknown GEMM implementation {self.gemm_impl!r}")
@@ -418,9 +422,24 @@ class DeviceRank:
                 ops.gemm(a, b, out, beta=1.0 if accumulate else 0.0, relu_out=relu_out, ws=self.gemm_ws)
                 self.launches += 1
 
+    def _tiled(self, a):
+        """Tiled (TMA-staged) layout of `a`, built on first use; None when too
+        little of the matrix falls into dense tiles to pay off."""
+        key = id(a)
+        if key not in self._tiles:
+            t = ops.TiledCsr(a)
+            self._tiles[key] = t if t.tiled_fraction >= 0.5 else None
+        return self._tiles[key]
+
     def _spmm(self, a, x, y, d: int):
+        """K3/K4: the TMA-staged tiled kernel for wide rows of community-
+        structured blocks, the row-gather kernel otherwise."""
+        t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and d > 128)) else None
         with self.timer("spmm", *_spmm_cost(a, d)):
-            ops.spmm(a, x, y, d)
+            if t is not None:
+                ops.spmm_tiled(t, x, y, d)
+            else:
+                ops.spmm(a, x, y, d)
         self.launches += 1
 
     def _layer_forward(self, l: int, Hd):

@@ -30,6 +30,7 @@ from halobit.datasets import SbmSpec, generate_sbm  # noqa: E402
 from halobit.graph import (build_partition, mean_adjacency,  # noqa: E402
                            normalize_adjacency, partition_nodes)
 from halobit.rngstream import RngStream, _derive_key  # noqa: E402
+from halobit.linalg import CsrMatrix, spmm  # noqa: E402
 from halobit.trainer import ModelConfig, TrainMode, train  # noqa: E402
 
 KEY_TUPLES = [
@@ -174,6 +175,46 @@ def graph_cases():
     (OUT / "graph_hashes.json").write_text(json.dumps(info, indent=1))
 
 
+def spmm_cases():
+    """``linalg.spmm`` (linalg.py:71-75) and ``CsrMatrix.transpose`` (:62-63)
+    on the small graph's blocks and on ragged random CSR (empty rows, rows
+    longer than a warp's 32-entry chunk, a dense row), fp32-representable
+    inputs, f64 outputs."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(2303)
+    out, meta = {}, []
+    gs = generate_sbm(SbmSpec(nodes_per_community=30, communities=3, seed=6))
+    a = normalize_adjacency(gs)
+    plan = partition_nodes(gs, 3, "contiguous", 5)
+    p = build_partition(gs, a, plan, 1, mean_adjacency(gs))
+    mats = {"ahat_block": p.adj_block, "mean_block": p.mean_block, "ahat_block_T": p.adj_block.transpose()}
+    dens = np.zeros((200, 300))
+    lens = rng.integers(0, 60, size=200)
+    lens[:7] = 0                      # empty rows
+    lens[10] = 300                    # one dense row
+    lens[11:14] = [31, 32, 33]        # chunk boundaries
+    for r, ln in enumerate(lens):
+        cols = rng.choice(300, size=ln, replace=False)
+        dens[r, cols] = rng.standard_normal(ln).astype(np.float32)
+    mats["ragged"] = CsrMatrix.from_scipy(sp.csr_matrix(dens))
+    mats["ragged_T"] = mats["ragged"].transpose()
+    for name, m in mats.items():
+        vals = np.asarray(m.values, dtype=np.float32)
+        out[name + "_rp"], out[name + "_ci"], out[name + "_v"] = m.row_ptr, m.col_idx, vals
+        mm = CsrMatrix(m.rows, m.cols, m.row_ptr, m.col_idx, vals.astype(np.float64))
+        widths = {"ahat_block": (1, 5, 32, 41, 64, 100, 132), "mean_block": (5, 41, 128),
+                  "ahat_block_T": (5, 41, 100)}.get(name, (1, 41, 64, 256))
+        for d in widths:
+            x = rng.standard_normal((m.cols, d)).astype(np.float32)
+            key = f"{name}_d{d}"
+            out[key + "_x"] = x
+            out[key + "_y"] = spmm(mm, x.astype(np.float64))   # reference output on the fp32 inputs
+            meta.append(dict(key=key, mat=name, rows=int(m.rows), cols=int(m.cols), d=d,
+                             nnz=int(len(m.col_idx))))
+    np.savez_compressed(OUT / "spmm_cases.npz", **out)
+    (OUT / "spmm_cases.json").write_text(json.dumps(meta, indent=1))
+
+
 def _run(g, n, widths, model, mode, bits, epochs, seed, dropout=0.0):
     a = normalize_adjacency(g)
     mh = mean_adjacency(g) if model == "sage" else None
@@ -207,6 +248,10 @@ def train_traces():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["spmm"]:
+        spmm_cases()
+        sys.exit(0)
+    spmm_cases()
     stream_cases()
     codec_cases()
     multi_peer_case()

@@ -1,0 +1,154 @@
+"""K3/K4 CSR SpMM vs the reference's ``linalg.spmm`` (linalg.py:71-75).
+
+Golden outputs come from the reference itself (tests/golden/make_golden.py,
+``spmm_cases``) on fp32-representable inputs; the device accumulates in fp32,
+so the tolerance is |y - y_ref| <= 1e-5 * (|A| @ |X|) elementwise + 1e-30."""
+
+import numpy as np
+import pytest
+
+from conftest import load_json, load_npz
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+def _bound(rp, ci, v, x):
+    import scipy.sparse as sp
+    a = sp.csr_matrix((np.abs(v.astype(np.float64)), ci, rp), shape=(len(rp) - 1, x.shape[0]))
+    return a @ np.abs(x.astype(np.float64))
+
+
+def _run(rp, ci, v, x, ncols, ld_pad=0, ld_out_pad=0, algo="auto", window=0):
+    from paper_2303_01277_b200 import ops
+    rows, d = len(rp) - 1, x.shape[1]
+    A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
+    ldx = d + ld_pad
+    X = torch.zeros(ncols, ldx, device="cuda")
+    X[:, :d] = torch.from_numpy(x)
+    Y = torch.full((rows, d + ld_out_pad), 7.0, device="cuda")
+    ops.spmm(A, X, Y, d, algo=algo, window=window)
+    torch.cuda.synchronize()
+    out = Y.cpu().numpy()
+    if ld_out_pad:
+        assert np.all(out[:, d:] == 7.0)          # padding columns untouched
+    return out[:, :d].astype(np.float64)
+
+
+@pytest.mark.parametrize("algo,window", [("rows", 0), ("sweep", 0), ("sweep", 16)])
+def test_spmm_matches_reference_golden(algo, window):
+    meta, z = load_json("spmm_cases.json"), load_npz("spmm_cases.npz")
+    for m in meta:
+        k, name = m["key"], m["mat"]
+        rp, ci, v = z[name + "_rp"], z[name + "_ci"], z[name + "_v"]
+        x, y = z[k + "_x"], z[k + "_y"]
+        # 16-byte aligned rows (vector path) and unaligned rows (scalar path)
+        for pad in ((-x.shape[1]) % 4, (-x.shape[1]) % 4 + 1):
+            got = _run(rp, ci, v, x, m["cols"], ld_pad=pad, ld_out_pad=pad, algo=algo, window=window)
+            tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+            assert np.all(np.abs(got - y) <= tol), (k, pad, np.abs(got - y).max())
+
+
+@pytest.mark.parametrize("algo", ["rows", "sweep"])
+@pytest.mark.parametrize("d", [3, 8, 20, 44, 96, 128, 200, 300, 512, 1024, 1100])
+def test_spmm_random_power_law_rows(d, algo):
+    """Skewed row lengths (0 .. 2000 nonzeros) at every width class."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(d)
+    rows, cols = 700, 5000
+    lens = np.minimum((rng.pareto(1.2, rows) * 8).astype(int), 2000)
+    lens[::97] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(cols, n, replace=False)) for n in lens]).astype(np.int64)
+    v = rng.standard_normal(len(ci)).astype(np.float32)
+    x = rng.standard_normal((cols, d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci, rp), shape=(rows, cols)) @ x.astype(np.float64)
+    got = _run(rp, ci, v, x, cols, ld_pad=(-d) % 4, algo=algo, window=64)
+    tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+    assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("d", [100, 256, 602])
+def test_spmm_sweep_community_block(d):
+    """Dense community blocks + scattered halo columns (the Reddit shape in
+    miniature): the sweep equals the row gather to fp32 tolerance."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(7 + d)
+    rows, comm = 1500, 500
+    cols = rows + 3000
+    ci, rp = [], [0]
+    for r in range(rows):
+        c0 = (r // comm) * comm
+        intra = rng.choice(comm, size=rng.integers(20, 90), replace=False) + c0
+        halo = rows + rng.choice(3000, size=rng.integers(0, 4), replace=False)
+        c = np.sort(np.concatenate([intra, halo]))
+        ci.append(c)
+        rp.append(rp[-1] + len(c))
+    ci = np.concatenate(ci).astype(np.int64)
+    rp = np.asarray(rp, dtype=np.int64)
+    v = rng.standard_normal(len(ci)).astype(np.float32)
+    x = rng.standard_normal((cols, d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci, rp), shape=(rows, cols)) @ x.astype(np.float64)
+    tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+    for window in (0, 16, 100):
+        got = _run(rp, ci, v, x, cols, ld_pad=(-d) % 4, algo="sweep", window=window)
+        assert np.all(np.abs(got - ref) <= tol), (window, np.abs(got - ref).max())
+
+
+def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0):
+    from paper_2303_01277_b200 import ops
+    rows, d = len(rp) - 1, x.shape[1]
+    A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
+    T = ops.TiledCsr(A, threshold=threshold)
+    X = torch.zeros(ncols, d + ld_pad, device="cuda")
+    X[:, :d] = torch.from_numpy(x)
+    Y = torch.full((rows, d + ld_pad), 7.0, device="cuda")
+    ops.spmm_tiled(T, X, Y, d)
+    torch.cuda.synchronize()
+    out = Y.cpu().numpy()
+    assert np.all(out[:, d:] == 7.0)
+    return out[:, :d].astype(np.float64), T
+
+
+@pytest.mark.parametrize("threshold", [1, 64, 10**9])
+def test_spmm_tiled_matches_reference_golden(threshold):
+    """All-tiles / mixed / all-residual splits against the reference's spmm."""
+    meta, z = load_json("spmm_cases.json"), load_npz("spmm_cases.npz")
+    for m in meta:
+        k, name = m["key"], m["mat"]
+        rp, ci, v = z[name + "_rp"], z[name + "_ci"], z[name + "_v"]
+        x, y = z[k + "_x"], z[k + "_y"]
+        got, _ = _tiled_run(rp, ci, v, x, m["cols"], threshold, ld_pad=(-x.shape[1]) % 4)
+        tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+        assert np.all(np.abs(got - y) <= tol), (k, threshold, np.abs(got - y).max())
+
+
+@pytest.mark.parametrize("d", [41, 100, 128, 256, 602])
+def test_spmm_tiled_community_blocks(d):
+    import scipy.sparse as sp
+    rng = np.random.default_rng(11 + d)
+    rows, comm = 1500, 300
+    cols = rows + 2000
+    ci, rp = [], [0]
+    for r in range(rows):
+        c0 = (r // comm) * comm
+        intra = rng.choice(comm, size=rng.integers(20, 120), replace=False) + c0
+        halo = rows + rng.choice(2000, size=rng.integers(0, 4), replace=False)
+        c = np.sort(np.concatenate([intra, halo]))
+        ci.append(c)
+        rp.append(rp[-1] + len(c))
+    ci = np.concatenate(ci).astype(np.int64)
+    rp = np.asarray(rp, dtype=np.int64)
+    v = rng.standard_normal(len(ci)).astype(np.float32)
+    x = rng.standard_normal((cols, d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci, rp), shape=(rows, cols)) @ x.astype(np.float64)
+    got, T = _tiled_run(rp, ci, v, x, cols, 64, ld_pad=(-d) % 4)
+    assert 0.5 < T.tiled_fraction < 1.0          # both paths exercised
+    tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+    assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()

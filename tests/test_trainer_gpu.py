@@ -213,3 +213,14 @@ def test_zero_epochs_and_empty_mask():
     res = train(g, parts, ModelConfig((32, 8, 2)), TrainMode(), QuantConfig(1), 0, 1)
     assert res.metrics == []
     assert _wdiff(res.final_weights, init_weights(ModelConfig((32, 8, 2)), 1)) == 0.0
+
+
+@pytest.mark.parametrize("impl", ["rows", "tiled"])
+def test_spmm_impls_track_oracle(impl, monkeypatch):
+    """The row-gather and the TMA-tiled SpMM both reproduce the oracle trajectory."""
+    monkeypatch.setenv("HB_SPMM", impl)
+    g = _graph(seed=21, npc=120, comms=3)
+    res, o, losses, _ = _run_both(g, 2, (32, 16, 4), "sage", "sync", 0, 32, 5, 4)
+    for m, lo in zip(res.metrics, losses):
+        assert m.train_loss == pytest.approx(lo, rel=5e-5)
+    assert _wdiff(res.final_weights, o.weights) < 1e-4

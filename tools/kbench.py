@@ -86,16 +86,34 @@ def spmm(args):
     A = ops.DeviceCsr(lay.NL, lay.NL + lay.NH, rp, ci, v, "cuda")
     At = _transpose_device(A)
     print(json.dumps({"setup_s": time.time() - t0, "NL": lay.NL, "NH": lay.NH, "nnz": A.nnz}), flush=True)
-    for name, M, d in (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("A", A, 64)):
+    tiled = {}
+    cases = (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("A", A, 64), ("A", A, 41),
+             ("At", At, 41))
+    if args.d_list:
+        cases = tuple(c for c in cases if c[2] in args.d_list)
+    for name, M, d in cases:
         ld = (d + 3) // 4 * 4
         X = torch.randn(M.cols, ld, device="cuda")
         Y = torch.zeros(M.rows, ld, device="cuda")
-        ms = _time(lambda: ops.spmm(M, X, Y, d), reps=5)
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
-        print(json.dumps({"kernel": "spmm", "mat": name, "d": d, "ms": ms,
-                          "compulsory_gbps": comp / ms / 1e6,
-                          "gather_gbps": (8 * M.nnz + 4 * M.nnz * d) / ms / 1e6,
-                          "tflops": 2 * M.nnz * d / ms / 1e9}), flush=True)
+        variants = [("rows", 0), ("tiled", 0)]
+        for algo, win in variants:
+            if algo == "tiled":
+                if name not in tiled:
+                    t0 = time.time()
+                    tiled[name] = ops.TiledCsr(M)
+                    torch.cuda.synchronize()
+                    print(json.dumps({"tiled": name, "build_s": round(time.time() - t0, 2),
+                                      "tiles": tiled[name].ntiles,
+                                      "tiled_fraction": round(tiled[name].tiled_fraction, 4)}), flush=True)
+                T = tiled[name]
+                ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
+            else:
+                ms = _time(lambda: ops.spmm(M, X, Y, d, algo=algo, window=win), reps=5)
+            print(json.dumps({"kernel": "spmm", "mat": name, "d": d, "algo": algo, "window": win,
+                              "ms": round(ms, 3), "compulsory_gbps": round(comp / ms / 1e6, 1),
+                              "gather_gbps": round((8 * M.nnz + 4 * M.nnz * d) / ms / 1e6, 1),
+                              "tflops": round(2 * M.nnz * d / ms / 1e9, 2)}), flush=True)
 
 
 def gemm(args):
@@ -138,5 +156,6 @@ if __name__ == "__main__":
     ap.add_argument("--bits", type=int, default=1)
     ap.add_argument("--segs", type=int, default=56)
     ap.add_argument("--config", default="reddit")
+    ap.add_argument("--d-list", type=int, nargs="*", default=None)
     a = ap.parse_args()
     {"codec": codec, "spmm": spmm, "gemm": gemm}[a.what](a)
