@@ -295,13 +295,16 @@ class DeviceRank:
             s.header_bytes_sent += hd
             s.messages_sent += ms
 
-    def _send(self, bufs: ExchangeBuffers, src, epoch: int, layer: int, parity: int, count=True):
-        """K1 for every hosted sender (+ NCCL for remote peers)."""
+    def _send(self, bufs: ExchangeBuffers, src, epoch: int, layer: int, parity: int, count=True,
+              defer: bool = False):
+        """K1 for every hosted sender (+ NCCL for remote peers on the comm stream)."""
         torch = self.torch
+        # K1 below overwrites the send buffer: an exchange still in flight on
+        # the comm stream (Sylvie-A, or a drained slot at an adaptor-sync
+        # epoch) must have left it first
+        self._wait_comm(bufs)
         if bufs.n_send:
-            tab = bufs.send_table(self.seed, epoch, layer, parity)
-            segs = torch.from_numpy(tab.view(np.uint8).copy()).to(self.dev, non_blocking=False)
-            bufs._segs_keepalive = segs
+            segs = bufs.upload_send_table(self.seed, epoch, layer, parity)
             R = int(bufs.plan.send_rows.size)
             nbytes = R * bufs.d * 4 + R * 4 + bufs.wire_bytes_total()
             with self.timer("quantize_gather", nbytes):
@@ -315,14 +318,28 @@ class DeviceRank:
             with torch.cuda.stream(self.comm_stream):
                 self.comm_stream.wait_event(ev)
                 nccl_exchange(bufs, parity, self.group)
-            torch.cuda.current_stream().wait_stream(self.comm_stream)
+                done = self.comm_stream.record_event()
+            if defer:
+                # Sylvie-A: the exchange overlaps the rest of this epoch and the
+                # next one up to the consuming K2 (_recv waits on `done`)
+                bufs.comm_done[parity] = done
+            else:
+                torch.cuda.current_stream().wait_event(done)
         if count:
             self._count(bufs)
+
+    def _wait_comm(self, bufs: ExchangeBuffers, parity=None):
+        for p in range(len(bufs.comm_done)) if parity is None else (parity,):
+            ev = bufs.comm_done[p]
+            if ev is not None:
+                self.torch.cuda.current_stream().wait_event(ev)
+                bufs.comm_done[p] = None
 
     def _recv(self, bufs: ExchangeBuffers, parity: int, dst, accumulate: bool):
         """K2: forward scatter into halo rows / backward ascending-peer integration."""
         if bufs.n_recv == 0:
             return
+        self._wait_comm(bufs, parity)
         pd = bufs.plan.dev
         nd, ns = int(bufs.plan.dst_rows.size), int(bufs.plan.src_rows.size)
         nbytes = bufs.wire_bytes_total() + nd * bufs.d * 4 * (2 if accumulate else 1) + 4 * (2 * nd + ns)
@@ -396,7 +413,7 @@ class DeviceRank:
                     self._recv(bufs, (epoch - 1) % 2, H, False)
                 if self.probe:
                     self._probe_halo(epoch, l, tag, H, d)
-                self._send(bufs, H, epoch, l, epoch % 2)
+                self._send(bufs, H, epoch, l, epoch % 2, defer=True)
                 self.slots[(l, FORWARD)] = epoch
             Hd = H
             if training and self.drop:
@@ -554,7 +571,7 @@ class DeviceRank:
                 if epoch > 1:
                     self._consume(epoch, l, BACKWARD)
                     self._recv(bufs, (epoch - 1) % 2, JF, True)
-                self._send(bufs, JF, epoch, l, epoch % 2)
+                self._send(bufs, JF, epoch, l, epoch % 2, defer=True)
                 self.slots[(l, BACKWARD)] = epoch
             J = JF[:NL]
         return self.loss_dev
@@ -562,9 +579,16 @@ class DeviceRank:
     def step(self, epoch: int):
         """All-reduce, Adam (trainer.py:358-366); returns nothing, loss stays on device."""
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.gflat, group=self.group)
-            dist.all_reduce(self.loss_dev, group=self.group)
+            # every NCCL call of the rank is issued from the comm stream, so the
+            # all-reduce queues behind any deferred (Sylvie-A) halo exchange in
+            # host issue order — identical on all ranks — and never runs
+            # concurrently with it on another stream
+            torch = self.torch
+            cur = torch.cuda.current_stream()
+            with torch.cuda.stream(self.comm_stream):
+                self.comm_stream.wait_stream(cur)
+                reduce_gradients(self.gflat, self.loss_dev, self.group)
+            cur.wait_stream(self.comm_stream)
         self.adam_t += 1
         for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
             ops.adam_step(w, g, m, v, self.lr, self.adam_t)
@@ -619,6 +643,15 @@ class DeviceRank:
             t.messages_sent += s.messages_sent
             t.allreduce_bytes += s.allreduce_bytes
         return t.snapshot()
+
+
+def reduce_gradients(gflat, loss, group=None):
+    """``Fabric.all_reduce_sum`` of the weight gradients and the loss
+    (transport.py:126-148, trainer.py:358-360): one flat all-reduce each, so
+    every replica applies bit-identical updates."""
+    import torch.distributed as dist
+    dist.all_reduce(gflat, group=group)
+    dist.all_reduce(loss, group=group)
 
 
 AGG_ORDERS = ("pre", "post", "auto")

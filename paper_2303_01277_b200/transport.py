@@ -80,6 +80,9 @@ class PoisonableBarrier:
         self._barrier.abort()
 
 
+SEG_BYTES = 40          # sizeof(hb_segment_t)
+
+
 def _align16(n: int) -> int:
     return (n + 15) & ~15
 
@@ -256,6 +259,14 @@ class ExchangeBuffers:
             self.recv_segs.append(torch.from_numpy(seg.view(np.uint8).copy()).to(device))
         self.n_send = len(plan.send_msgs)
         self.n_recv = len(plan.recv_msgs)
+        self.comm_done = [None] * parities     # CUDA events of in-flight remote exchanges
+        # K1 descriptor tables change every epoch (keys): staged through two
+        # pinned host slots so the upload is asynchronous (no stream sync)
+        self._dev = torch.device(device)
+        self._seg_dev = torch.zeros(max(1, self.n_send) * SEG_BYTES, dtype=torch.uint8, device=device)
+        self._seg_host = None
+        self._seg_ev = [None, None]
+        self._seg_slot = 0
 
     def send_table(self, seed: int, epoch: int, layer: int, parity: int) -> np.ndarray:
         """hb_segment_t rows for this exchange (keys depend on the epoch)."""
@@ -273,6 +284,23 @@ class ExchangeBuffers:
             k = keys[m.src]
             seg[i] = (k[0], k[1], self.elem_off[(m.src, m.dst)], out, m.row_begin, m.rows)
         return seg
+
+    def upload_send_table(self, seed: int, epoch: int, layer: int, parity: int):
+        """Device copy of ``send_table(...)`` (stream-ordered, host does not block)."""
+        import torch
+        tab = self.send_table(seed, epoch, layer, parity).view(np.uint8)
+        if self._dev.type != "cuda":
+            self._seg_dev.copy_(torch.from_numpy(tab.copy()))
+            return self._seg_dev
+        if self._seg_host is None:
+            self._seg_host = [torch.empty(tab.size, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        k = self._seg_slot = self._seg_slot ^ 1
+        if self._seg_ev[k] is not None:
+            self._seg_ev[k].synchronize()          # the copy from this slot two uploads ago
+        self._seg_host[k].numpy()[:] = tab
+        self._seg_dev.copy_(self._seg_host[k], non_blocking=True)
+        self._seg_ev[k] = torch.cuda.current_stream(self._dev).record_event()
+        return self._seg_dev
 
     def stats_delta(self) -> dict:
         """Per sending partition byte meters of one exchange (transport.py:105-114)."""
