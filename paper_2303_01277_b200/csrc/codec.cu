@@ -665,6 +665,138 @@ dequant_gather_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
   }
 }
 
+// K2, restructured for latency: the received row's metadata is read once per
+// (destination, source) and the lane walks all of its 128-column chunks;
+// the segment of a received row is found from a per-warp cached segment
+// (received rows are visited in ascending order) before falling back to the
+// binary search.  Forward 1-bit rows take an fp32 path that is bit-identical
+// to the f64 formula (f32(f64(sc)*c + f64(mn)) == __fadd_rn(sc, mn) for c = 1:
+// two fp32 operands, so the f64 sum is exact or rounds far below an fp32
+// half-ulp); everything else accumulates in f64 exactly as before.
+template <int NCH, bool FAST1>
+__global__ void __launch_bounds__(kQWarps * 32)
+dequant_rows_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_dst,
+                    const int32_t* __restrict__ dst_rows, const int32_t* __restrict__ src_ptr,
+                    const int32_t* __restrict__ src_rows, int d, int bits, float* __restrict__ dst,
+                    int64_t ld, int accumulate) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  const int rb = bits == 32 ? 4 * d : (d * bits + 7) >> 3;
+  const bool vec = ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
+  constexpr bool fast1 = FAST1;     // caller guarantees !accumulate && bits == 1
+  constexpr int NA = FAST1 ? 1 : NCH;
+  int cs = 0;
+  for (int i = blockIdx.x * kQWarps + warp; i < num_dst; i += gridDim.x * kQWarps) {
+    float* out = dst + (int64_t)dst_rows[i] * ld;
+    const int k0 = src_ptr[i], k1 = src_ptr[i + 1];
+    if (FAST1 && k1 - k0 != 1) {
+      // several (or no) received rows for one destination: chunk-wise f64 sum
+      for (int c0 = 4 * lane; c0 < d; c0 += 128) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = k0; k < k1; ++k) {
+          const int q = src_rows[k];
+          const hb_segment_t& sg = segs_s[find_segment_smem(seg_begin, nseg, q)];
+          const int r = q - sg.row_begin;
+          const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+          const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);  // 4-byte aligned
+          const float2 meta = make_float2(mp[0], mp[1]);
+          const uint8_t* pay = blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+          int code[4];
+          codes4(pay, rb, c0, 1, d, code);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            a4[e] = __dadd_rn(a4[e], __dadd_rn(__dmul_rn((double)meta.y, (double)code[e]), (double)meta.x));
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c0 + e < d) out[c0 + e] = __double2float_rn(a4[e]);
+      }
+      continue;
+    }
+    double acc[NA][4];
+#pragma unroll
+    for (int ch = 0; ch < NA; ++ch)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = ch * 128 + 4 * lane + e;
+        acc[ch][e] = (!FAST1 && accumulate && c < d) ? (double)out[c] : 0.0;
+      }
+    for (int k = k0; k < k1; ++k) {
+      const int q = src_rows[k];
+      if (!(q >= seg_begin[cs] && q < seg_begin[cs + 1])) cs = find_segment_smem(seg_begin, nseg, q);
+      const hb_segment_t& sg = segs_s[cs];
+      const int r = q - sg.row_begin;
+      const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+      if (!FAST1 && bits == 32) {
+        const float* prow = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES) + (int64_t)r * d;
+#pragma unroll
+        for (int ch = 0; ch < NA; ++ch)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = ch * 128 + 4 * lane + e;
+            if (c < d) acc[ch][e] = __dadd_rn(acc[ch][e], (double)prow[c]);
+          }
+        continue;
+      }
+      const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);  // 4-byte aligned
+          const float2 meta = make_float2(mp[0], mp[1]);
+      const uint8_t* pay = blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+      if (fast1) {
+        const float one = __fadd_rn(meta.y, meta.x);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c0 = ch * 128 + 4 * lane;
+          if (c0 >= d) continue;
+          const uint32_t nib = (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+          const float4 v = make_float4((nib & 1u) ? one : meta.x, (nib & 2u) ? one : meta.x,
+                                       (nib & 4u) ? one : meta.x, (nib & 8u) ? one : meta.x);
+          if (vec && c0 + 3 < d) {
+            *reinterpret_cast<float4*>(out + c0) = v;
+          } else {
+            out[c0] = v.x;
+            if (c0 + 1 < d) out[c0 + 1] = v.y;
+            if (c0 + 2 < d) out[c0 + 2] = v.z;
+            if (c0 + 3 < d) out[c0 + 3] = v.w;
+          }
+        }
+        continue;
+      }
+#pragma unroll
+      for (int ch = 0; ch < NA; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        if (c0 >= d) continue;
+        int code[4];
+        codes4(pay, rb, c0, bits, d, code);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc[ch][e] = __dadd_rn(acc[ch][e], __dadd_rn(__dmul_rn((double)meta.y, (double)code[e]), (double)meta.x));
+      }
+    }
+    if (FAST1) continue;     // stored directly
+#pragma unroll
+    for (int ch = 0; ch < NA; ++ch) {
+      const int c0 = ch * 128 + 4 * lane;
+      if (c0 >= d) continue;
+      if (vec && c0 + 3 < d) {
+        *reinterpret_cast<float4*>(out + c0) =
+            make_float4(__double2float_rn(acc[ch][0]), __double2float_rn(acc[ch][1]),
+                        __double2float_rn(acc[ch][2]), __double2float_rn(acc[ch][3]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c0 + e < d) out[c0 + e] = __double2float_rn(acc[ch][e]);
+      }
+    }
+  }
+}
+
 __global__ void philox_uniforms_kernel(uint64_t k0, uint64_t k1, uint64_t start, int64_t n,
                                        double* __restrict__ out) {
   const uint64_t first_blk = start >> 2;
@@ -729,6 +861,25 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
   if (num_dst <= 0) return cudaSuccess;
   const int want = (num_dst + kQWarps - 1) / kQWarps;
   const int grid = want < num_sms() * 8 ? want : num_sms() * 8;
+  const int nch = (d + 127) / 128;
+  static const bool legacy = getenv("HB_K2_LEGACY") != nullptr;
+  if (!legacy && nseg <= kMaxSmemSegs && nch <= 8) {
+#define HB_K2(N, F) dequant_rows_kernel<N, F><<<grid, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, \
+                                                                       src_ptr, src_rows, d, bits, dst, ld, accumulate)
+    // one received row per destination, 1 bit, overwrite: the fp32 fast path
+    if (!accumulate && bits == 1) {
+      if (nch <= 2) HB_K2(2, true);
+      else if (nch <= 4) HB_K2(4, true);
+      else HB_K2(8, true);
+    } else if (nch == 1) HB_K2(1, false);
+    else if (nch == 2) HB_K2(2, false);
+    else if (nch == 3) HB_K2(3, false);
+    else if (nch == 4) HB_K2(4, false);
+    else if (nch == 5) HB_K2(5, false);
+    else HB_K2(8, false);
+#undef HB_K2
+    return cudaGetLastError();
+  }
   dequant_gather_kernel<<<grid, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr,
                                                        src_rows, d, bits, dst, ld, accumulate);
   return cudaGetLastError();

@@ -56,25 +56,64 @@ __global__ void __launch_bounds__(1024) sum_f64_kernel(const double* __restrict_
 }
 
 // ---- ReLU and relu' product ----------------------------------------------------
-__global__ void relu_kernel(const float* __restrict__ z, int64_t ldz, int n, int d,
-                            float* __restrict__ y, int64_t ldy) {
-  const int64_t total = (int64_t)n * d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / d, c = i - r * d;
-    const float v = z[r * ldz + c];
-    y[r * ldy + c] = (v > 0.f || v != v) ? v : 0.f;  // np.maximum propagates NaN
+// Row-tiled elementwise kernels: one warp walks a row with float4 accesses
+// when the rows are 16-byte aligned (the trainer's buffers are), scalar
+// otherwise; no per-element 64-bit division.
+template <typename F>
+__device__ __forceinline__ void rows_apply(int n, int d, bool vec, F f) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    if (vec) {
+      const int d4 = d >> 2;
+      for (int c4 = lane; c4 < d4; c4 += 32) f.vec4(r, 4 * c4);
+      for (int c = 4 * d4 + lane; c < d; c += 32) f.one(r, c);
+    } else {
+      for (int c = lane; c < d; c += 32) f.one(r, c);
+    }
   }
 }
 
-__global__ void relu_grad_mul_kernel(const float* __restrict__ j, int64_t ldj, const float* __restrict__ h,
-                                     int64_t ldh, int n, int d, float* __restrict__ m, int64_t ldm) {
-  const int64_t total = (int64_t)n * d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / d, c = i - r * d;
-    m[r * ldm + c] = h[r * ldh + c] > 0.f ? j[r * ldj + c] : 0.f;
+__device__ __forceinline__ float relu1(float v) { return (v > 0.f || v != v) ? v : 0.f; }  // np.maximum keeps NaN
+
+struct ReluOp {
+  const float* z; int64_t ldz; float* y; int64_t ldy;
+  __device__ void one(int r, int c) const { y[(int64_t)r * ldy + c] = relu1(z[(int64_t)r * ldz + c]); }
+  __device__ void vec4(int r, int c) const {
+    const float4 v = *reinterpret_cast<const float4*>(z + (int64_t)r * ldz + c);
+    *reinterpret_cast<float4*>(y + (int64_t)r * ldy + c) = make_float4(relu1(v.x), relu1(v.y), relu1(v.z), relu1(v.w));
   }
+};
+
+struct ReluGradOp {
+  const float* j; int64_t ldj; const float* h; int64_t ldh; float* m; int64_t ldm;
+  __device__ void one(int r, int c) const {
+    m[(int64_t)r * ldm + c] = h[(int64_t)r * ldh + c] > 0.f ? j[(int64_t)r * ldj + c] : 0.f;
+  }
+  __device__ void vec4(int r, int c) const {
+    const float4 a = *reinterpret_cast<const float4*>(j + (int64_t)r * ldj + c);
+    const float4 b = *reinterpret_cast<const float4*>(h + (int64_t)r * ldh + c);
+    *reinterpret_cast<float4*>(m + (int64_t)r * ldm + c) =
+        make_float4(b.x > 0.f ? a.x : 0.f, b.y > 0.f ? a.y : 0.f, b.z > 0.f ? a.z : 0.f, b.w > 0.f ? a.w : 0.f);
+  }
+};
+
+__global__ void relu_kernel(const float* __restrict__ z, int64_t ldz, int n, int d, float* __restrict__ y,
+                            int64_t ldy, bool vec) {
+  rows_apply(n, d, vec, ReluOp{z, ldz, y, ldy});
+}
+
+__global__ void relu_grad_mul_kernel(const float* __restrict__ j, int64_t ldj, const float* __restrict__ h,
+                                     int64_t ldh, int n, int d, float* __restrict__ m, int64_t ldm, bool vec) {
+  rows_apply(n, d, vec, ReluGradOp{j, ldj, h, ldh, m, ldm});
+}
+
+static bool al16(const void* p, int64_t ld) { return ((((uintptr_t)p) & 15) == 0) && (ld % 4 == 0); }
+
+static int rows_grid(int n) {
+  const int want = (n + 7) / 8;
+  const int cap = num_sms() * 16;
+  return want < cap ? (want > 0 ? want : 1) : cap;
 }
 
 // ---- Adam ------------------------------------------------------------------------
@@ -163,14 +202,15 @@ cudaError_t launch_xent(const float* logits, int64_t ld, int n, int C, const int
 
 cudaError_t launch_relu(const float* z, int64_t ldz, int n, int d, float* y, int64_t ldy, cudaStream_t st) {
   if ((int64_t)n * d <= 0) return cudaSuccess;
-  relu_kernel<<<grid_for((int64_t)n * d, 256), 256, 0, st>>>(z, ldz, n, d, y, ldy);
+  relu_kernel<<<rows_grid(n), 256, 0, st>>>(z, ldz, n, d, y, ldy, al16(z, ldz) && al16(y, ldy));
   return cudaGetLastError();
 }
 
 cudaError_t launch_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, int n, int d,
                                  float* m, int64_t ldm, cudaStream_t st) {
   if ((int64_t)n * d <= 0) return cudaSuccess;
-  relu_grad_mul_kernel<<<grid_for((int64_t)n * d, 256), 256, 0, st>>>(j, ldj, h, ldh, n, d, m, ldm);
+  relu_grad_mul_kernel<<<rows_grid(n), 256, 0, st>>>(j, ldj, h, ldh, n, d, m, ldm,
+                                                     al16(j, ldj) && al16(h, ldh) && al16(m, ldm));
   return cudaGetLastError();
 }
 

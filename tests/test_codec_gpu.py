@@ -103,3 +103,50 @@ def test_non_finite_rejected():
                       RngStream(1, 0, 1, 1, "forward"))
     with pytest.raises(CodecError):
         quantize_rows(np.ones((1, 2)), QuantConfig(1), None)
+
+
+@pytest.mark.parametrize("d", [41, 256, 602])
+@pytest.mark.parametrize("bits", [1, 2, 8, 16, 32])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_dequant_gather_multi_source_exact(d, bits, accumulate):
+    """K2 over several wire blocks: destination t gets
+    f32(f64(t if accumulate) + sum_k f64 dequant(src_k)) with sources summed in
+    the listed (ascending-peer) order (trainer.py:208-216, codec.py:199-207)."""
+    from oracle import codec as oc
+    from paper_2303_01277_b200.codec import dequant_gather, segments_tensor
+    rng = np.random.default_rng(d * 7 + bits)
+    blocks, rows_per = [], [37, 0, 64, 5]
+    for r in rows_per:
+        x = (rng.standard_normal((r, d)) * rng.uniform(0.1, 4.0, (r, 1))).astype(np.float64)
+        u = rng.random(r * d) if bits != 32 else None
+        rmin, rscale, codes = oc.quantize(x.astype(np.float32).astype(np.float64), bits, u)
+        blocks.append((oc.wire_block(rmin, rscale, codes, bits, r, d), oc.dequantize(rmin, rscale, codes, bits)))
+    sizes = [(len(b) + 15) // 16 * 16 for b, _ in blocks]
+    buf = np.zeros(sum(sizes), dtype=np.uint8)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(int)
+    for (b, _), o in zip(blocks, offs):
+        buf[o:o + len(b)] = np.frombuffer(b, dtype=np.uint8)
+    dbuf = torch.from_numpy(buf).cuda()
+    segs = segments_tensor(rows_per, [(0, 0)] * 4, [0] * 4, [dbuf.data_ptr() + int(o) for o in offs], "cuda")
+    recv = np.concatenate([v for _, v in blocks])            # flattened received rows (f64)
+    R = recv.shape[0]
+    ndst = 60
+    # destinations: some get 0, 1 or several sources (ascending flat order)
+    owner = rng.integers(0, ndst, R)
+    order = np.lexsort((np.arange(R), owner))
+    dst_rows, starts = np.unique(owner[order], return_index=True)
+    src_ptr = np.append(starts, R).astype(np.int32)
+    src_rows = order.astype(np.int32)
+    ld = (d + 3) // 4 * 4
+    init = rng.standard_normal((ndst + 3, ld)).astype(np.float32)
+    dst = torch.from_numpy(init.copy()).cuda()
+    dequant_gather(segs, 4, torch.from_numpy(dst_rows.astype(np.int32)).cuda(),
+                   torch.from_numpy(src_ptr).cuda(), torch.from_numpy(src_rows).cuda(), d, bits, dst, accumulate)
+    got = dst.cpu().numpy()
+    want = init.copy()
+    for i, t in enumerate(dst_rows):
+        acc = init[t, :d].astype(np.float64) if accumulate else np.zeros(d)
+        for k in range(src_ptr[i], src_ptr[i + 1]):
+            acc = acc + recv[src_rows[k]]
+        want[t, :d] = acc.astype(np.float32)
+    np.testing.assert_array_equal(got, want)

@@ -1,0 +1,73 @@
+"""K8 elementwise ops vs the oracle (linalg.py:78-140 restated in oracle/epoch.py).
+
+Tolerances: ReLU / relu' masks exact; softmax-CE loss rel 1e-6 (f64 loss
+accumulation on device, fp32 logits) and gradient abs 1e-7; Adam one step
+rel 1e-6 + abs 1e-6 (f64 update math, fp32 storage of w, m, v)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+
+
+@pytest.mark.parametrize("n,d,ld", [(1000, 256, 256), (777, 41, 44), (50, 41, 41), (3, 5, 7)])
+def test_relu_and_relu_grad_mul(n, d, ld):
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    z = torch.randn(n, ld, device="cuda", generator=g)
+    z[0, 0] = float("nan")
+    y = torch.full((n, ld), 9.0, device="cuda")
+    ops.relu(z, y, n, d)
+    zz = z[:, :d].cpu().numpy()
+    np.testing.assert_array_equal(y[:, :d].cpu().numpy(), np.maximum(zz, 0.0))   # NaN propagates like numpy
+    assert torch.all(y[:, d:] == 9.0)
+    j = torch.randn(n, ld, device="cuda", generator=g)
+    m = torch.full((n, ld), 9.0, device="cuda")
+    ops.relu_grad_mul(j, y, m, n, d)
+    want = np.where(y[:, :d].cpu().numpy() > 0, j[:, :d].cpu().numpy(), 0.0)
+    np.testing.assert_array_equal(m[:, :d].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n,C", [(5000, 41), (300, 4), (64, 100)])
+def test_softmax_xent_matches_oracle(n, C):
+    from oracle.epoch import xent
+    from paper_2303_01277_b200 import ops
+    rng = np.random.default_rng(C)
+    logits = (rng.standard_normal((n, C)) * 3).astype(np.float32)
+    labels = rng.integers(0, C, n)
+    mask = rng.random(n) < 0.6
+    norm = float(mask.sum() + 17)              # global normaliser (trainer.py:397)
+    loss_ref, grad_ref = xent(logits.astype(np.float64), labels, mask, norm)
+    ld = (C + 3) // 4 * 4
+    L = torch.zeros(n, ld, device="cuda")
+    L[:, :C] = torch.from_numpy(logits).cuda()
+    grad = torch.zeros(n, ld, device="cuda")
+    row_loss = torch.zeros(n, dtype=torch.float64, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.softmax_xent(L, C, torch.from_numpy(labels.astype(np.int32)).cuda(),
+                     torch.from_numpy(mask.astype(np.uint8)).cuda(), norm, grad, row_loss, loss)
+    assert float(loss) == pytest.approx(loss_ref, rel=1e-6)
+    np.testing.assert_allclose(grad[:, :C].cpu().numpy(), grad_ref, atol=1e-7)
+
+
+def test_adam_matches_oracle():
+    from oracle.epoch import Adam
+    from paper_2303_01277_b200 import ops
+    rng = np.random.default_rng(3)
+    w0 = rng.standard_normal(5000).astype(np.float32)
+    opt = Adam(0.01)
+    w_ref = w0.astype(np.float64)
+    w = torch.from_numpy(w0.copy()).cuda()
+    m, v = torch.zeros_like(w), torch.zeros_like(w)
+    for t in range(1, 4):
+        gr = rng.standard_normal(5000).astype(np.float32)
+        w_ref = opt.step(w_ref, gr.astype(np.float64))
+        ops.adam_step(w, torch.from_numpy(gr).cuda(), m, v, 0.01, t)
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-6, atol=1e-6)   # fp32 storage of w, m, v
