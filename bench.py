@@ -38,6 +38,9 @@ WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (3
 MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn"}
 PARTITIONS = 8
 CPU_SAMPLE_SCALE = 0.125       # the CPU oracle runs the same shape at 1/8 of the nodes/edges
+# Bit-exact Philox4x64-10 throughput of the B200 at full occupancy (uniforms/s,
+# tools/probes/philox_probe.cu measured on the GPU box; profiles/ has the run)
+PHILOX_CEILING_GELEM_S = 414.0
 
 
 def _spec(name: str, scale: float = 1.0):
@@ -251,16 +254,50 @@ def run_b200(args):
     if rank == 0:
         peaks = load_peaks()
         dom = max(ksum, key=lambda k: ksum[k]["ms"]) if ksum else None
+        clocks_mhz = clocks.get("sm_mhz") or 1965
         roof = None
         if "spmm" in ksum:
             s = ksum["spmm"]
-            traffic = _ncu_traffic("spmm")
-            roof = {"kernel": "hb_spmm_csr (K3/K4)", "bound": "hbm",
+            sec = s["ms"] / 1e3
+            # L1TEX/SMEM datapath: 128 B/clk/SM is what a SIMT SpMM can pull into
+            # registers, whether X rows come from L2 (row kernel) or from TMA-
+            # staged smem tiles (tiled kernel); gathered bytes = 4 * nnz * d
+            dp_peak = 148 * 128 * clocks_mhz * 1e6 / 1e9
+            gather_gbps = 2.0 * s["flops"] / sec / 1e9 if sec > 0 else 0.0
+            roof = {"kernel": "hb_spmm_tiled / hb_spmm_csr_ex (K3/K4)", "bound": "hbm",
                     "achieved": s["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": traffic,
+                    "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": _ncu_traffic("spmm"),
                     "algorithmic_bytes_per_launch": s["bytes"] / s["launches"],
+                    "algorithmic_bytes_model": "compulsory: CSR + each X row once + Y once (SURVEY 8d)",
                     "avg_launch_ms": s["ms"] / s["launches"], "peak_source": peaks["source"],
-                    "fp32_simt_tflops": s["tflops"]}
+                    "fp32_simt_tflops": s["tflops"],
+                    "l1_datapath": {"gathered_gbps": gather_gbps, "peak_gbps": dp_peak,
+                                    "frac": gather_gbps / dp_peak,
+                                    "note": "gather model 4*nnz*d bytes per launch vs 148 SM x 128 B/clk"}}
+        kroof = {}
+        if "quantize_gather" in ksum:
+            q = ksum["quantize_gather"]
+            elems = sum(int(b.plan.send_rows.size) * b.d for b in list(eng.xf.values()) + list(eng.xb.values()))
+            rate = elems * args.steps / (q["ms"] / 1e3) / 1e9
+            kroof["quantize_gather"] = {
+                "bound": "hbm", "achieved": q["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": q["gbps"] / peaks["hbm_gbs"],
+                "philox_gelem_s": rate, "philox_ceiling_gelem_s": PHILOX_CEILING_GELEM_S,
+                "philox_frac": rate / PHILOX_CEILING_GELEM_S,
+                "note": "bit-exact Philox4x64-10 (one uniform per element) caps K1 below HBM speed"}
+        for k in ("dequant_gather", "elementwise"):
+            if k in ksum:
+                v = ksum[k]
+                kroof[k] = {"bound": "hbm", "achieved": v["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": v["gbps"] / peaks["hbm_gbs"]}
+        if "gemm" in ksum:
+            g = ksum["gemm"]
+            tf32_peak = peaks["bf16_tflops"] / 2.0
+            kroof["gemm"] = {"bound": "tensor", "achieved": g["tflops"], "unit": "TFLOP/s",
+                             "tf32_mma_tflops": 3.0 * g["tflops"], "peak": tf32_peak,
+                             "frac": 3.0 * g["tflops"] / tf32_peak,
+                             "note": "3xTF32 (hi*hi + hi*lo + lo*hi per fp32 product); peak = dense TF32 = "
+                                     "measured bf16 / 2"}
         wire = sum(b.wire_bytes_total() for b in list(eng.xf.values()) + list(eng.xb.values()))
         halo_ms = sum(ksum.get(k, {}).get("ms", 0.0) for k in ("quantize_gather", "dequant_gather"))
         line = {
@@ -270,6 +307,7 @@ def run_b200(args):
             "data": "synthetic (planted-partition reddit-shaped graph, random-init Glorot weights)",
             "config": workload_config(args),
             "roofline": roof,
+            "kernel_rooflines": kroof,
             "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                         for k, v in ksum.items()},
             "dominant_kernel": dom,

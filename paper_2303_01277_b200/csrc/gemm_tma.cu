@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdint>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace hb {
@@ -534,9 +535,10 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
                             int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
                             int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
   if (!gt::tma_ok(A, lda_m, lda_k) || !gt::tma_ok(B, ldb_n, ldb_k)) return cudaErrorNotSupported;
-  if (N <= 64)
+  static const int max_bn = getenv("HB_GEMM_BN") ? atoi(getenv("HB_GEMM_BN")) : 256;
+  if (N <= 64 || max_bn == 64)
     return gt::launch_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
-  if (N <= 128)
+  if (N <= 128 || max_bn == 128)
     return gt::launch_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   return gt::launch_bn<256>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
 }
