@@ -266,12 +266,14 @@ quantize_gather_kernel(const float* __restrict__ src, int64_t ld, const int32_t*
       }
       if (pow2) {
         // chunk image word k = OR of fields of lanes [k*L, (k+1)*L), L = 8/bits
-        const int L = 8 / bits;
+        // L = 8 / bits lanes share a word: shifts, not a runtime division
+        const int lgL = B1 ? 3 : 3 - (__ffs(bits) - 1);
+        const int L = 1 << lgL;
         uint32_t w = field << ((4 * bits) * (lane & (L - 1)));
         if (L >= 2) w |= __shfl_xor_sync(0xffffffffu, w, 1);
         if (L >= 4) w |= __shfl_xor_sync(0xffffffffu, w, 2);
         if (L >= 8) w |= __shfl_xor_sync(0xffffffffu, w, 4);
-        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + lane / L] = w;
+        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + (lane >> lgL)] = w;
       } else if (field | field_hi) {
         const int c0 = 128 * t + 4 * lane - delta;
         const int pos = 64 + bits * c0;                     // >= 16 for bits <= 16
@@ -350,7 +352,8 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
   const bool pow2 = bits <= 8 && (bits & (bits - 1)) == 0;
   const uint32_t bytes = (uint32_t)(((d + 3) & ~3) * 4);
   const int stride = gridDim.x * kQWarps;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase_bits = 0u;          // bit s = parity of barrier s (a register, not local memory)
+  int cseg = 0;
 
   int row = blockIdx.x * kQWarps + warp;
   if (row < total_rows && lane == 0) {
@@ -366,7 +369,14 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
       tma_load_1d(rows_s + (cur ^ 1) * ldr, src + (int64_t)__ldg(row_idx + nxt) * ld, bytes,
                   &bars[warp][cur ^ 1]);
     }
-    const int si = smem_segs ? find_segment_smem(seg_begin, nseg, row) : find_segment(segs_g, nseg, row);
+    // rows are visited in ascending order: try the previous segment first
+    if (smem_segs) {
+      if (!(row >= seg_begin[cseg] && (cseg + 1 >= nseg || row < seg_begin[cseg + 1])))
+        cseg = find_segment_smem(seg_begin, nseg, row);
+    } else {
+      cseg = find_segment(segs_g, nseg, row);
+    }
+    const int si = cseg;
     const hb_segment_t sg = smem_segs ? segs_s[si] : segs_g[si];
     const int r = row - sg.row_begin;
     const uint64_t e_row = sg.elem_offset + (uint64_t)r * (uint64_t)d;
@@ -375,8 +385,8 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
     const int nchunks = (d + delta + 127) >> 7;
     uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
     const float* xs = rows_s + cur * ldr;
-    mbar_wait(&bars[warp][cur], phase[cur]);
-    phase[cur] ^= 1u;
+    mbar_wait(&bars[warp][cur], (phase_bits >> cur) & 1u);
+    phase_bits ^= 1u << cur;
 
     // ---- pass 1 (smem): min / max / finiteness ----------------------------------
     float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
@@ -465,12 +475,14 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
         }
       }
       if (pow2) {
-        const int L = 8 / bits;
+        // L = 8 / bits lanes share a word: shifts, not a runtime division
+        const int lgL = B1 ? 3 : 3 - (__ffs(bits) - 1);
+        const int L = 1 << lgL;
         uint32_t w = field << ((4 * bits) * (lane & (L - 1)));
         if (L >= 2) w |= __shfl_xor_sync(0xffffffffu, w, 1);
         if (L >= 4) w |= __shfl_xor_sync(0xffffffffu, w, 2);
         if (L >= 8) w |= __shfl_xor_sync(0xffffffffu, w, 4);
-        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + lane / L] = w;
+        if ((lane & (L - 1)) == 0) buf[nw_chunk * t + (lane >> lgL)] = w;
       } else if (field | field_hi) {
         const int c0 = 128 * t + 4 * lane - delta;
         const int pos = 64 + bits * c0;
@@ -832,8 +844,10 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
     const size_t dyn = (size_t)kQWarps * (2 * ldr * 4 + imgw * 4);
     if (dyn <= 200 * 1024) {
       static const int minb = getenv("HB_K1_MINB") ? atoi(getenv("HB_K1_MINB")) : 3;
-      auto kern = bits == 1 ? (minb == 4 ? quantize_gather_tma_kernel<true, 4> : quantize_gather_tma_kernel<true, 3>)
-                            : (minb == 4 ? quantize_gather_tma_kernel<false, 4> : quantize_gather_tma_kernel<false, 3>);
+      auto kern = bits == 1 ? (minb == 4 ? quantize_gather_tma_kernel<true, 4>
+                               : minb == 2 ? quantize_gather_tma_kernel<true, 2> : quantize_gather_tma_kernel<true, 3>)
+                            : (minb == 4 ? quantize_gather_tma_kernel<false, 4>
+                               : minb == 2 ? quantize_gather_tma_kernel<false, 2> : quantize_gather_tma_kernel<false, 3>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
       kern<<<grid, blk, dyn, st>>>(ARGS, ldr, imgw);
 #undef ARGS
