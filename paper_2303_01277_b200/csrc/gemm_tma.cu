@@ -52,6 +52,7 @@ struct Cfg {
 struct Params {
   int M, N, K;
   int a_mn, b_mn;          // 1 = MN-major operand
+  int bsplit;              // 1: B arrives pre-split (hi / lo, K-major) via tmB / tmBl
   int mt, nt, splits, kb_per_split, nkb;
   float* C;
   int64_t ldc;
@@ -111,7 +112,8 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mi, int
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmBl, Params p) {
   using C_ = Cfg<BN>;
   constexpr int S = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -158,7 +160,7 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           uint8_t* st = smem + s * C_::STAGE;
           uint8_t* a_hi = st;
           uint8_t* b_hi = st + 2 * C_::A_BYTES;
-          mbar_expect_tx(&full[s], C_::A_BYTES + C_::B_BYTES);
+          mbar_expect_tx(&full[s], C_::A_BYTES + (p.bsplit ? 2 : 1) * C_::B_BYTES);
           const int k0 = kb * BK;
           if (p.a_mn) {
 #pragma unroll
@@ -166,7 +168,10 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           } else {
             tma_2d(a_hi, &tmA, k0, mi * BM, &full[s]);
           }
-          if (p.b_mn) {
+          if (p.bsplit) {
+            tma_2d(b_hi, &tmB, k0, ni * BN, &full[s]);
+            tma_2d(b_hi + C_::B_BYTES, &tmBl, k0, ni * BN, &full[s]);
+          } else if (p.b_mn) {
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j) tma_2d(b_hi + j * 4096, &tmB, ni * BN + 32 * j, k0, &full[s]);
           } else {
@@ -282,7 +287,7 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           a_lo[i] = l;
         }
 #pragma unroll 4
-        for (int i = ct; i < C_::B_BYTES / 16; i += 128) {
+        for (int i = ct; i < (p.bsplit ? 0 : C_::B_BYTES / 16); i += 128) {
           const uint4 v = b_hi[i];
           uint4 h, l;
           h.x = rna_tf32(__uint_as_float(v.x)); l.x = rna_tf32(__uint_as_float(v.x) - __uint_as_float(h.x));
@@ -421,6 +426,21 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   }
 }
 
+// B pre-split for the GEMMs whose B is a weight (Z = P W, T = m W^T): B is
+// small and shared by every tile, so it is split once into K-major hi / lo
+// arrays ([N][Kp], zero-padded) instead of in every CTA's converter warps.
+__global__ void bsplit_kernel(const float* __restrict__ B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp,
+                              float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = (int64_t)N * Kp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / Kp), k = (int)(i - (int64_t)n * Kp);
+    const float x = k < K ? B[(int64_t)k * ldb_k + (int64_t)n * ldb_n] : 0.f;
+    const uint32_t h = rna_tf32(x);
+    hi[i] = __uint_as_float(h);
+    lo[i] = __uint_as_float(rna_tf32(x - __uint_as_float(h)));
+  }
+}
+
 // Deterministic split-K reduction (fixed order) + beta + optional ReLU copy.
 __global__ void splitk_reduce2_kernel(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C,
                                       int64_t ldc, float beta, float* __restrict__ relu_out, int64_t ldr) {
@@ -503,6 +523,25 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
   }
   p.kb_per_split = (p.nkb + splits - 1) / splits;
   p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
+  // weight-sized B with many tiles: split it once into the workspace
+  CUtensorMap tbl = tb;
+  const int Kp = (K + 3) & ~3;
+  static const bool no_bsplit = getenv("HB_GEMM_NO_BSPLIT") != nullptr;
+  if (!no_bsplit && p.splits == 1 && ws != nullptr && tiles >= 2 * sms && p.nkb >= 4 && (int64_t)N * K <= (1 << 20) &&
+      2 * (int64_t)N * Kp <= ws_floats) {
+    float* hi = ws;
+    float* lo = ws + (int64_t)N * Kp;
+    int g = (int)(((int64_t)N * Kp + 255) / 256);
+    if (g > sms * 4) g = sms * 4;
+    bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, Kp, hi, lo);
+    if (make_map(&tb, hi, K, N, Kp, BN, false) && make_map(&tbl, lo, K, N, Kp, BN, false)) {
+      p.bsplit = 1;
+      p.b_mn = 0;
+    } else {
+      ok = make_map(&tb, B, p.b_mn ? N : K, p.b_mn ? K : N, p.b_mn ? ldb_k : ldb_n, p.b_mn ? 32 : BN, p.b_mn);
+      if (!ok) return cudaErrorNotSupported;
+    }
+  }
   p.C = C; p.ldc = ldc; p.beta = beta; p.relu_out = p.splits > 1 ? nullptr : relu_out; p.ldr = ldr;
   p.ws = p.splits > 1 ? ws : nullptr;
   p.dbg = g_gemm_dbg;
@@ -515,7 +554,7 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  gemm_tma_kernel<BN><<<grid, kThreads, C_::SMEM, st>>>(ta, tb, p);
+  gemm_tma_kernel<BN><<<grid, kThreads, C_::SMEM, st>>>(ta, tb, tbl, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.splits > 1) {

@@ -131,3 +131,21 @@ def test_gemm_accumulate_relu_and_split_relu(gemm_path):
     ops.gemm(P.t(), m, G, ws=ws, relu_out=R)
     _check(P.t(), m, G)
     assert torch.equal(R, torch.clamp(G, min=0))
+
+
+@pytest.mark.parametrize("N,K,kind", [(256, 602, "nn"), (41, 256, "nn"), (256, 256, "nt"), (602, 41, "nt")])
+def test_gemm_presplit_weight_operand(N, K, kind):
+    """Tall GEMMs (>= 2 tiles per SM) with a weight-sized B take the path that
+    splits B into tf32 hi / lo once (workspace) instead of per CTA."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    M = 40_000
+    A = _pad(M, K, g)
+    B = _pad(K, N, g) if kind == "nn" else _pad(N, K, g).t()
+    C0 = torch.randn(M, N, device="cuda", generator=g)
+    C = C0.clone()
+    H = torch.zeros(M, (N + 3) // 4 * 4, device="cuda")
+    ws = torch.empty(64 * 602 * 256, device="cuda")
+    ops.gemm(A, B, C, beta=1.0, relu_out=H[:, :N], ws=ws)
+    _check(A, B, C, beta=1.0, C0=C0)
+    assert torch.equal(H[:, :N], torch.clamp(C, min=0))
