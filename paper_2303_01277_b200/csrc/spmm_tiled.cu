@@ -29,6 +29,7 @@ constexpr int kTRB = 64;         // rows per block (16 consumer warps x 4 rows)
 constexpr int kTW = 64;          // columns per window
 constexpr int kRowOff = 72;      // row offsets per tile (65 used, padded to 144 bytes)
 constexpr int kRPW = 4;          // rows per consumer warp
+constexpr int kMaxRec = 1024;    // records per tile (ops.TiledCsr splits denser tiles)
 constexpr int kConsumers = kTRB / kRPW;
 constexpr int kThreads = 32 * (kConsumers + 1);
 
@@ -49,14 +50,16 @@ struct Args {
   int64_t ldy;
 };
 
-template <int NV>
+// NV float4 per lane, G lanes per record group (32, or 16 for d <= 64 so two
+// records go through one warp instruction), S pipeline stages.
+template <int NV, int G, int S>
 struct Smem {
-  static constexpr int P = 128 * NV;                     // panel width (floats)
+  static constexpr int P = 4 * G * NV;                   // panel width (floats)
   static constexpr int X_BYTES = kTW * P * 4;
-  static constexpr int NZ_BYTES = kTRB * kTW * 8;        // worst case: dense tile
+  static constexpr int NZ_BYTES = kMaxRec * 8;
   static constexpr int RO_BYTES = kRowOff * 2;
   static constexpr int STAGE = X_BYTES + NZ_BYTES + 256;
-  static constexpr int TOTAL = 2 * STAGE + 128;
+  static constexpr int TOTAL = S * STAGE + 128;
 };
 
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
@@ -70,27 +73,29 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
-template <int NV>
+template <int NV, int G>
 __device__ __forceinline__ void fma_row(float4 (&acc)[NV], float v, const float4* __restrict__ x) {
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    const float4 t = x[q * 32];
+    const float4 t = x[q * G];
     acc[q].x = fmaf(v, t.x, acc[q].x); acc[q].y = fmaf(v, t.y, acc[q].y);
     acc[q].z = fmaf(v, t.z, acc[q].z); acc[q].w = fmaf(v, t.w, acc[q].w);
   }
 }
 
-template <int NV>
+template <int NV, int G, int S>
 __global__ void __launch_bounds__(kThreads, 1)
 spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
-  using S_ = Smem<NV>;
+  using S_ = Smem<NV, G, S>;
   constexpr int P = S_::P;
+  constexpr int NG = 32 / G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ __align__(8) uint64_t full[S], empty[S];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hg = lane / G, gl = lane % G;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
     }
@@ -106,8 +111,8 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int b = item / a.npanels, pn = item % a.npanels;
         for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
-          const int s = it & 1;
-          mbar_wait(&empty[s], ((it >> 1) & 1) ^ 1);
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           uint8_t* st = smem + s * S_::STAGE;
           const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
           const uint32_t nzb = (uint32_t)((o1 - o0) * 8);
@@ -125,6 +130,7 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
 
   // ---------------- consumers ----------------
   int it = 0;
+  const int pw4 = a.pw / 4;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / a.npanels, pn = item % a.npanels;
     const int r0 = b * kTRB + warp * kRPW;
@@ -136,34 +142,33 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       for (int q = 0; q < NV; ++q) acc[i][q] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
-      const int s = it & 1;
-      mbar_wait(&full[s], (it >> 1) & 1);
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
       const uint8_t* st = smem + s * S_::STAGE;
-      const float4* xs = reinterpret_cast<const float4*>(st) + lane;
-      const int pw4 = a.pw / 4;
+      const float4* xs = reinterpret_cast<const float4*>(st) + gl;
       const int2* nz = reinterpret_cast<const int2*>(st + S_::X_BYTES);
       const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + S_::NZ_BYTES) + warp * kRPW;
 #pragma unroll
       for (int i = 0; i < kRPW; ++i) {
         const int k1 = ro[i + 1];
-        int k = ro[i];
-        for (; k + 4 <= k1; k += 4) {
-          const int2 e0 = nz[k], e1 = nz[k + 1], e2 = nz[k + 2], e3 = nz[k + 3];
-          fma_row<NV>(acc[i], __int_as_float(e0.y), xs + e0.x * pw4);
-          fma_row<NV>(acc[i], __int_as_float(e1.y), xs + e1.x * pw4);
-          fma_row<NV>(acc[i], __int_as_float(e2.y), xs + e2.x * pw4);
-          fma_row<NV>(acc[i], __int_as_float(e3.y), xs + e3.x * pw4);
+        int k = ro[i] + hg;                    // group hg takes records hg, hg + NG, ...
+        for (; k + 3 * NG < k1; k += 4 * NG) {
+          const int2 e0 = nz[k], e1 = nz[k + NG], e2 = nz[k + 2 * NG], e3 = nz[k + 3 * NG];
+          fma_row<NV, G>(acc[i], __int_as_float(e0.y), xs + e0.x * pw4);
+          fma_row<NV, G>(acc[i], __int_as_float(e1.y), xs + e1.x * pw4);
+          fma_row<NV, G>(acc[i], __int_as_float(e2.y), xs + e2.x * pw4);
+          fma_row<NV, G>(acc[i], __int_as_float(e3.y), xs + e3.x * pw4);
         }
-        for (; k < k1; ++k) {
+        for (; k < k1; k += NG) {
           const int2 e = nz[k];
-          fma_row<NV>(acc[i], __int_as_float(e.y), xs + e.x * pw4);
+          fma_row<NV, G>(acc[i], __int_as_float(e.y), xs + e.x * pw4);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[s]);
     }
 
-    // residual nonzeros: gathered from global X
+    // residual nonzeros: gathered from global X (group hg takes every NG-th)
     const float* Xp = a.X + col0;
 #pragma unroll
     for (int i = 0; i < kRPW; ++i) {
@@ -175,14 +180,16 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         const int my_c = k < e1 ? __ldg(a.res_col + k) : 0;
         const float my_v = k < e1 ? __ldg(a.res_val + k) : 0.f;
         const int n = (int)min((int64_t)32, e1 - base);
-        for (int j = 0; j < n; ++j) {
-          const int c = __shfl_sync(0xffffffffu, my_c, j);
-          const float v = __shfl_sync(0xffffffffu, my_v, j);
-          const float4* xr = reinterpret_cast<const float4*>(Xp + (int64_t)c * a.ldx) + lane;
+        for (int j0 = 0; j0 < n; j0 += NG) {
+          const int j = j0 + hg;
+          const int c = __shfl_sync(0xffffffffu, my_c, j & 31);
+          const float vj = __shfl_sync(0xffffffffu, my_v, j & 31);   // every lane shuffles
+          const float v = j < n ? vj : 0.f;
+          const float4* xr = reinterpret_cast<const float4*>(Xp + (int64_t)c * a.ldx) + gl;
 #pragma unroll
           for (int q = 0; q < NV; ++q) {
-            if (col0 + (q * 32 + lane) * 4 < a.d) {
-              const float4 t4 = __ldg(xr + q * 32);
+            if (col0 + (q * G + gl) * 4 < a.d) {
+              const float4 t4 = __ldg(xr + q * G);
               acc[i][q].x = fmaf(v, t4.x, acc[i][q].x); acc[i][q].y = fmaf(v, t4.y, acc[i][q].y);
               acc[i][q].z = fmaf(v, t4.z, acc[i][q].z); acc[i][q].w = fmaf(v, t4.w, acc[i][q].w);
             }
@@ -190,7 +197,19 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         }
       }
     }
-    // store the panel
+    // combine the record groups, store the panel
+#pragma unroll
+    for (int i = 0; i < kRPW; ++i)
+#pragma unroll
+      for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          acc[i][q].x += __shfl_xor_sync(0xffffffffu, acc[i][q].x, off);
+          acc[i][q].y += __shfl_xor_sync(0xffffffffu, acc[i][q].y, off);
+          acc[i][q].z += __shfl_xor_sync(0xffffffffu, acc[i][q].z, off);
+          acc[i][q].w += __shfl_xor_sync(0xffffffffu, acc[i][q].w, off);
+        }
+    if (hg != 0) continue;
 #pragma unroll
     for (int i = 0; i < kRPW; ++i) {
       const int r = r0 + i;
@@ -198,7 +217,7 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       float* y = a.Y + (int64_t)r * a.ldy + col0;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        const int col = (q * 32 + lane) * 4;
+        const int col = (q * G + gl) * 4;
         const int rem = a.d - col0 - col;
         if (rem >= 4) {
           *reinterpret_cast<float4*>(y + col) = acc[i][q];
@@ -224,9 +243,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int NV>
+template <int NV, int G, int S>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
-  using S_ = Smem<NV>;
+  using S_ = Smem<NV, G, S>;
+  static_assert(S_::TOTAL <= 227 * 1024, "smem");
   Args a = a0;
   a.npanels = (a.d + S_::P - 1) / S_::P;
   a.pw = a.npanels > 1 ? S_::P : (a.d + 3) / 4 * 4;
@@ -243,14 +263,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_tiled_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(spmm_tiled_kernel<NV, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < num_sms() ? items : num_sms();
-  if (grid > 0) spmm_tiled_kernel<NV><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_tiled_kernel<NV, G, S><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -267,8 +287,9 @@ cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* 
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_nz = tile_nz; a.res_ptr = res_ptr; a.res_col = res_col; a.res_val = res_val;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-  if (d <= 128) return st::launch_nv<1>(a, xrows, stream);
-  return st::launch_nv<2>(a, xrows, stream);
+  if (d <= 64) return st::launch_nv<1, 16, 8>(a, xrows, stream);     // 24 KB stages
+  if (d <= 128) return st::launch_nv<1, 32, 5>(a, xrows, stream);    // 40 KB stages
+  return st::launch_nv<2, 32, 3>(a, xrows, stream);                  // 72 KB stages, 256-column panels
 }
 
 }  // namespace hb

@@ -38,6 +38,7 @@ class TiledCsr:
     RB = 64
     W = 64
     ROWOFF = 72
+    MAXREC = 1024
 
     def __init__(self, a: DeviceCsr, threshold: int = 64):
         import torch
@@ -56,7 +57,16 @@ class TiledCsr:
         dense_g = cnt >= threshold
         gid = torch.repeat_interleave(torch.arange(len(uniq), device=dev), cnt)
         dense_nz = dense_g[gid]
-        tile_key, tile_cnt = uniq[dense_g], cnt[dense_g]
+        grp_key, grp_cnt = uniq[dense_g], cnt[dense_g]
+        # a tile holds at most MAXREC records (the kernel's smem record slot);
+        # denser (block, window) groups become several tiles of the same window
+        nsplit = (grp_cnt + self.MAXREC - 1) // self.MAXREC
+        sub_of_grp = torch.repeat_interleave(torch.arange(grp_key.numel(), device=dev), nsplit)
+        first_sub = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
+        first_sub[1:] = torch.cumsum(nsplit, 0)
+        j = torch.arange(sub_of_grp.numel(), device=dev) - first_sub[sub_of_grp]
+        tile_key = grp_key[sub_of_grp]
+        tile_cnt = torch.clamp(grp_cnt[sub_of_grp] - j * self.MAXREC, max=self.MAXREC)
         self.ntiles = int(tile_key.numel())
         tile_blk = tile_key // nwin
         self.tile_win = (tile_key % nwin).to(torch.int32).contiguous()
@@ -68,10 +78,12 @@ class TiledCsr:
         off[1:] = torch.cumsum(padded, 0)
         self.tile_off = off
         didx = order[dense_nz]                                # original nonzero ids, tile order
-        tile_of = (torch.cumsum(dense_g.long(), 0) - 1)[gid[dense_nz]]
-        start = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
-        start[1:] = torch.cumsum(tile_cnt, 0)
-        rank = torch.arange(didx.numel(), device=dev) - start[tile_of]
+        grp_of = (torch.cumsum(dense_g.long(), 0) - 1)[gid[dense_nz]]
+        gstart = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
+        gstart[1:] = torch.cumsum(grp_cnt, 0)
+        grank = torch.arange(didx.numel(), device=dev) - gstart[grp_of]
+        tile_of = first_sub[grp_of] + grank // self.MAXREC
+        rank = grank % self.MAXREC
         pos = off[tile_of] + rank
         nz = torch.zeros((int(off[-1].item()), 2), dtype=torch.int32, device=dev)
         nz[pos, 0] = (col[didx] - self.tile_win.long()[tile_of] * self.W).to(torch.int32)

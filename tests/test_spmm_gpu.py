@@ -152,3 +152,24 @@ def test_spmm_tiled_community_blocks(d):
     assert 0.5 < T.tiled_fraction < 1.0          # both paths exercised
     tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("d", [41, 128, 256])
+def test_spmm_tiled_splits_dense_tiles(d):
+    """A fully dense 64x64 block (4096 records) exceeds a tile's record slot
+    and is split into several tiles of the same window."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(d)
+    rows, cols = 200, 400
+    dense = np.zeros((rows, cols), dtype=np.float32)
+    dense[64:128, 128:192] = rng.standard_normal((64, 64))
+    mask = rng.random((rows, cols)) < 0.05
+    dense[mask] = rng.standard_normal(mask.sum())
+    a = sp.csr_matrix(dense)
+    rp, ci, v = a.indptr.astype(np.int64), a.indices.astype(np.int64), a.data.astype(np.float32)
+    x = rng.standard_normal((cols, d)).astype(np.float32)
+    ref = a.astype(np.float64) @ x.astype(np.float64)
+    got, T = _tiled_run(rp, ci, v, x, cols, 64, ld_pad=(-d) % 4)
+    assert T.ntiles > int((T.tile_ptr[1:] - T.tile_ptr[:-1]).gt(0).sum())   # some window has >1 tile
+    tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+    assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
