@@ -452,7 +452,7 @@ class DeviceRank:
         """K3/K4: the TMA-staged tiled kernel for wide rows of community-
         structured blocks, the row-gather kernel otherwise."""
         t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and d > 128)) else None
-        with self.timer("spmm", *_spmm_cost(a, d)):
+        with self.timer("spmm_tiled" if t is not None else "spmm_rows", *_spmm_cost(a, d)):
             if t is not None:
                 ops.spmm_tiled(t, x, y, d)
             else:
