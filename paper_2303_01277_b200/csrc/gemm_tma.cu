@@ -376,37 +376,51 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int e = 0; e < 32; ++e)
               if (e < nv) crow[nb + e] = __uint_as_float(r[e]);
           } else {
-            const bool vec = nv == 32 && ((p.ldc & 3) == 0) && ((((uintptr_t)(crow + nb)) & 15) == 0) &&
-                             (!p.relu_out || (((p.ldr & 3) == 0) &&
-                                              ((((uintptr_t)(p.relu_out + (int64_t)row * p.ldr + nb)) & 15) == 0)));
-            if (vec) {
+            // all loads of the old C values first (no store can alias them in
+            // between), then the stores; float4 wherever the row allows it
+            float* rrow = p.relu_out ? p.relu_out + (int64_t)row * p.ldr + nb : nullptr;
+            const bool cvec = ((p.ldc & 3) == 0) && ((((uintptr_t)(crow + nb)) & 15) == 0);
+            const bool rvec = rrow && ((p.ldr & 3) == 0) && ((((uintptr_t)rrow) & 15) == 0);
+            float v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+            if (p.beta != 0.f) {
+              float o[32];
 #pragma unroll
               for (int e = 0; e < 32; e += 4) {
-                float4 v = make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), __uint_as_float(r[e + 2]),
-                                       __uint_as_float(r[e + 3]));
-                float4* dst = reinterpret_cast<float4*>(crow + nb + e);
-                if (p.beta != 0.f) {
-                  const float4 o = *dst;
-                  v.x += p.beta * o.x; v.y += p.beta * o.y; v.z += p.beta * o.z; v.w += p.beta * o.w;
-                }
-                *dst = v;
-                if (p.relu_out) {
-                  float4 q;
-                  q.x = (v.x > 0.f || v.x != v.x) ? v.x : 0.f;
-                  q.y = (v.y > 0.f || v.y != v.y) ? v.y : 0.f;
-                  q.z = (v.z > 0.f || v.z != v.z) ? v.z : 0.f;
-                  q.w = (v.w > 0.f || v.w != v.w) ? v.w : 0.f;
-                  *reinterpret_cast<float4*>(p.relu_out + (int64_t)row * p.ldr + nb + e) = q;
+                if (cvec && e + 3 < nv) {
+                  const float4 t = *reinterpret_cast<const float4*>(crow + nb + e);
+                  o[e] = t.x; o[e + 1] = t.y; o[e + 2] = t.z; o[e + 3] = t.w;
+                } else {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) o[e + u] = e + u < nv ? crow[nb + e + u] : 0.f;
                 }
               }
-            } else {
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                if (e >= nv) break;
-                float v = __uint_as_float(r[e]);
-                if (p.beta != 0.f) v += p.beta * crow[nb + e];
-                crow[nb + e] = v;
-                if (p.relu_out) p.relu_out[(int64_t)row * p.ldr + nb + e] = (v > 0.f || v != v) ? v : 0.f;
+              for (int e = 0; e < 32; ++e) v[e] += p.beta * o[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              if (cvec && e + 3 < nv) {
+                *reinterpret_cast<float4*>(crow + nb + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+              } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (e + u < nv) crow[nb + e + u] = v[e + u];
+              }
+            }
+            if (rrow) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = (v[e] > 0.f || v[e] != v[e]) ? v[e] : 0.f;
+#pragma unroll
+              for (int e = 0; e < 32; e += 4) {
+                if (rvec && e + 3 < nv) {
+                  *reinterpret_cast<float4*>(rrow + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                } else {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    if (e + u < nv) rrow[e + u] = v[e + u];
+                }
               }
             }
           }

@@ -226,7 +226,7 @@ class DeviceRank:
                   for l in range(1, L + 1) if self.post[l]}
         self.S = {l: torch.zeros((NL + NH, _ld(W[l])), dtype=f32, device=dev)
                   for l in range(1, L + 1) if self.post[l]}
-        self.Z = {l: torch.zeros((NL, W[l]), dtype=f32, device=dev) for l in range(1, L + 1)}
+        self.Z = {l: torch.zeros((NL, _ld(W[l])), dtype=f32, device=dev)[:, :W[l]] for l in range(1, L + 1)}
         self.JF = {l: torch.zeros((NL + NH, _ld(W[l - 1])), dtype=f32, device=dev) for l in range(2, L + 1)}
         self.T = {l: torch.zeros((NL, _ld(W[l - 1])), dtype=f32, device=dev)
                   for l in range(2, L + 1) if not self.post[l]}
