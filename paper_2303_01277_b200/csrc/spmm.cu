@@ -319,7 +319,11 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
     const int d4 = (d + 3) / 4;
 #define HB_S(NV, G, U) spmm_rows_vec_kernel<NV, G, U><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy)
     if (d4 <= 8) HB_S(1, 8, 8);
-    else if (d4 <= 16) HB_S(1, 16, 8);
+    else if (d4 <= 16) {   // `window` doubles as an unroll override (tuning only)
+      if (window == 4) HB_S(1, 16, 4);
+      else if (window == 8) HB_S(1, 16, 8);
+      else HB_S(1, 16, 16);
+    }
     else switch ((d4 + 31) / 32) {
       case 1: HB_S(1, 32, 8); break;
       case 2:   // `window` doubles as an unroll override for the row kernel (tuning only)

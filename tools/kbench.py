@@ -96,7 +96,7 @@ def spmm(args):
         X = torch.randn(M.cols, ld, device="cuda")
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
-        variants = [("rows", 0), ("tiled", 0)]
+        variants = [("rows", 0), ("tiled", 0)] + ([("rows", 4), ("rows", 16)] if d <= 64 else [])
         for algo, win in variants:
             if algo == "tiled":
                 if name not in tiled:
