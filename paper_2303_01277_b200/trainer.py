@@ -578,6 +578,11 @@ class DeviceRank:
 
     def step(self, epoch: int):
         """All-reduce, Adam (trainer.py:358-366); returns nothing, loss stays on device."""
+        self.reduce(epoch)
+        self.adam()
+
+    def reduce(self, epoch: int):
+        """Gradient + loss all-reduce (trainer.py:358-360)."""
         if self.world > 1:
             # every NCCL call of the rank is issued from the comm stream, so the
             # all-reduce queues behind any deferred (Sylvie-A) halo exchange in
@@ -589,6 +594,9 @@ class DeviceRank:
                 self.comm_stream.wait_stream(cur)
                 reduce_gradients(self.gflat, self.loss_dev, self.group)
             cur.wait_stream(self.comm_stream)
+
+    def adam(self):
+        """adam_step per layer (trainer.py:365-366)."""
         self.adam_t += 1
         for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
             ops.adam_step(w, g, m, v, self.lr, self.adam_t)
@@ -598,9 +606,10 @@ class DeviceRank:
         epoch_mode = staleness_adaptor(epoch, self.mode)
         logits = self.forward(epoch, epoch_mode)
         self.backward(epoch, epoch_mode, logits)
-        if check:
+        self.reduce(epoch)
+        if check:                 # on the all-reduced loss, before Adam (trainer.py:358-366)
             self.check_epoch(epoch)
-        self.step(epoch)
+        self.adam()
         return epoch_mode
 
     def check_epoch(self, epoch: int):
@@ -625,7 +634,13 @@ class DeviceRank:
         ops.argmax_accuracy(logits, self.cfg.widths[-1], self.labels, self.eval_mask, self.counts)
         if self.world > 1:
             import torch.distributed as dist
-            dist.all_reduce(self.counts, group=self.group)
+            from .transport import host_staged
+            if host_staged(self.group):
+                c = self.counts.cpu()
+                dist.all_reduce(c, group=self.group)
+                self.counts.copy_(c)
+            else:
+                dist.all_reduce(self.counts, group=self.group)
         c = self.counts.cpu().numpy()
         names = ("train_acc", "val_acc", "test_acc")
         return {n: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0)
@@ -650,6 +665,14 @@ def reduce_gradients(gflat, loss, group=None):
     (transport.py:126-148, trainer.py:358-360): one flat all-reduce each, so
     every replica applies bit-identical updates."""
     import torch.distributed as dist
+    from .transport import host_staged
+    if gflat.is_cuda and host_staged(group):        # gloo test runs: stage through host memory
+        g, l_ = gflat.cpu(), loss.cpu()
+        dist.all_reduce(g, group=group)
+        dist.all_reduce(l_, group=group)
+        gflat.copy_(g)
+        loss.copy_(l_)
+        return
     dist.all_reduce(gflat, group=group)
     dist.all_reduce(loss, group=group)
 

@@ -317,17 +317,34 @@ class ExchangeBuffers:
         return sum(wire_bytes(m.rows, self.d, self.bits) for m in self.plan.send_msgs)
 
 
+def host_staged(group=None) -> bool:
+    """True when the process group cannot move device buffers itself (gloo:
+    used by the multi-process tests that share one GPU); the wire blocks are
+    then staged through host memory.  Production runs NCCL (device to device
+    over NVLink)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) != "nccl"
+
+
 def nccl_exchange(bufs: ExchangeBuffers, parity: int, group=None):
     """Move the remote groups with NCCL send/recv (one pair per peer rank).
     Called on the comm stream; a no-op on a single rank."""
     import torch.distributed as dist
-    ops = []
+    stage = bufs.send.is_cuda and host_staged(group)
+    ops, landing = [], []
     for r, (o, n) in bufs.send_group.items():
-        ops.append(dist.P2POp(dist.isend, bufs.send[o:o + n], r, group=group))
+        t = bufs.send[o:o + n]
+        ops.append(dist.P2POp(dist.isend, t.cpu() if stage else t, r, group=group))
     for r, (o, n) in bufs.recv_group.items():
         if r == bufs.layout.rank:
             continue
-        ops.append(dist.P2POp(dist.irecv, bufs.recv[parity][o:o + n], r, group=group))
+        t = bufs.recv[parity][o:o + n]
+        h = t.cpu() if stage else t
+        if stage:
+            landing.append((t, h))
+        ops.append(dist.P2POp(dist.irecv, h, r, group=group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+    for t, h in landing:
+        t.copy_(h, non_blocking=False)

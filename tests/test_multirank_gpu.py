@@ -1,0 +1,113 @@
+"""The multi-rank device path (DeviceRank with world size 2) on one B200.
+
+Two processes share cuda:0 and talk over gloo (NCCL refuses two ranks on one
+device), so the wire blocks are staged through host memory
+(`transport.host_staged`); everything else — the per-rank layouts, K1 writing
+remote messages into the send buffer and local ones straight into the
+receiver's slot, the per-peer-rank send/recv groups, comm-stream ordering and
+Sylvie-A deferral, the gradient/loss all-reduce — is the production N>1 code.
+
+Checks against the single-process run of the same 4 partitions:
+* passthrough (bits 32): global losses every epoch rel 1e-5 and final weights
+  max-abs/max 1e-5 (fp32 summation order of the all-reduce differs), sync and
+  Sylvie-A;
+* 1-bit: byte meters summed over ranks equal the single-rank meters every
+  epoch, and the epoch-1 loss matches (identical inputs to the first
+  exchange).
+"""
+
+import os
+import socket
+import traceback
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+EPOCHS = 4
+CASES = [("sync", 0, 32), ("async", 0, 32), ("async", 2, 32), ("sync", 0, 1)]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _setup():
+    from paper_2303_01277_b200.datasets import SbmSpec, generate_sbm
+    from paper_2303_01277_b200.graph import build_partitions
+    g = generate_sbm(SbmSpec(nodes_per_community=60, communities=4, feature_dim=32, seed=8))
+    return g, build_partitions(g, 4, "hash", 0, "sage")[2]
+
+
+def _run(rank, world, owner, variant, st, bits):
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
+    from paper_2303_01277_b200.transport import RankLayout
+    g, parts = _setup()
+    lay = RankLayout({p.id: p for p in parts if owner[p.id] == rank}, owner, rank)
+    eng = DeviceRank(lay, ModelConfig((32, 16, 8), "sage"), TrainMode(variant, st), QuantConfig(bits), 3, 0.01,
+                     int(g.train_mask.sum()), device="cuda:0")
+    losses, meters = [], []
+    prev = eng.total_stats()
+    for e in range(1, EPOCHS + 1):
+        eng.run_epoch(e)
+        losses.append(eng.epoch_loss)
+        t = eng.total_stats()
+        meters.append(tuple(t[k] - prev[k] for k in ("main_bytes_sent", "metadata_bytes_sent",
+                                                   "header_bytes_sent", "messages_sent")))
+        prev = t
+    torch.cuda.synchronize()
+    return losses, meters, [w.double().cpu().numpy() for w in eng.W]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        out = {c: _run(rank, world, [0, 1, 1, 0], *c) for c in CASES}
+        q.put((rank, "ok", out))
+    except Exception:
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_two_ranks_on_one_gpu_match_single_rank():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, status, info = q.get(timeout=600)
+        assert status == "ok", f"rank {rank}:\n{info}"
+        res[rank] = info
+    for p in procs:
+        p.join(timeout=60)
+    for case in CASES:
+        single = _run(0, 1, [0, 0, 0, 0], *case)
+        l0, m0, w0 = res[0][case]
+        l1, m1, w1 = res[1][case]
+        assert l0 == l1                                            # both ranks see the all-reduced loss
+        np.testing.assert_allclose(w0[0], w1[0], rtol=0, atol=0)   # replicas bit-identical
+        summed = [tuple(a + b for a, b in zip(x, y)) for x, y in zip(m0, m1)]
+        assert summed == single[1], case
+        if case[2] == 32:
+            np.testing.assert_allclose(l0, single[0], rtol=1e-5)
+            scale = max(np.abs(w).max() for w in single[2])
+            assert max(np.abs(a - b).max() for a, b in zip(w0, single[2])) / scale < 1e-5, case
+        else:
+            assert l0[0] == pytest.approx(single[0][0], rel=1e-6)
