@@ -182,9 +182,16 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.share_gpu:
+        # test mode: every rank on cuda:0, gloo transport (wire blocks staged
+        # through host memory) — exercises the N>1 host logic on one GPU
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     owner = [p * world // PARTITIONS for p in range(PARTITIONS)]
     mine = [p for p in range(PARTITIONS) if owner[p] == rank]
     t0 = time.perf_counter()
@@ -228,10 +235,7 @@ def run_b200(args):
     eng.timer.enabled = False
     eng.check_epoch(epoch)
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = _max_over_ranks(ms, world)
     ksum = timer.summary()
     clocks = clk.result()
 
@@ -247,9 +251,7 @@ def run_b200(args):
         eng.run_epoch(epoch, check=True)            # reads loss + codec flag back (D2H)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
-    e2e = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e = _max_over_ranks(statistics.mean(e2e_times), world)
 
     if rank == 0:
         peaks = load_peaks()
@@ -321,7 +323,7 @@ def run_b200(args):
                              "K1 writes each wire block straight into its receiver's buffer"},
             "gpu_launches": launches,
             "clocks": clocks,
-            "e2e": {"value": float(e2e.item()), "unit": "s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 12},
             "setup_s": round(setup_s, 1),
             "final_loss": eng.epoch_loss,
@@ -335,6 +337,18 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    """Max of a per-rank timing over all ranks (device clocks, CPU tensor for gloo)."""
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    dev = "cpu" if dist.get_backend() != "nccl" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def _fp32_equiv(eng) -> int:
@@ -366,6 +380,8 @@ def main():
     ap.add_argument("--staleness", type=int, default=0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: all ranks on cuda:0 over gloo (the N>1 path on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
