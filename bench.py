@@ -158,7 +158,7 @@ def run_reference(args):
 
 
 def workload_config(args) -> dict:
-    spec = _spec(args.config)
+    spec = _spec(args.config, getattr(args, "scale", 1.0))
     return {"workload": f"{args.config}-shaped {len(WIDTHS[args.config]) - 1}-layer "
                         f"{MODEL[args.config].upper()} {'-'.join(map(str, WIDTHS[args.config]))}, "
                         f"{PARTITIONS} partitions over {args.gpus} GPU(s), {args.bits}-bit halos, "
@@ -166,7 +166,9 @@ def workload_config(args) -> dict:
             "nodes": spec.num_nodes, "edges": spec.num_edges, "partitions": PARTITIONS,
             "bits": args.bits, "mode": args.mode, "staleness": args.staleness,
             "model": MODEL[args.config], "widths": list(WIDTHS[args.config]),
-            "l2": "inputs larger than L2 (features 561 MB, aggregation CSR 0.9 GB)"}
+            "scale": getattr(args, "scale", 1.0),
+            "l2": "inputs larger than L2 (features 561 MB, aggregation CSR 0.9 GB)" if getattr(args, "scale", 1.0) == 1.0
+                  else "reduced-scale diagnostic run"}
 
 
 def run_b200(args):
@@ -195,7 +197,7 @@ def run_b200(args):
     owner = [p * world // PARTITIONS for p in range(PARTITIONS)]
     mine = [p for p in range(PARTITIONS) if owner[p] == rank]
     t0 = time.perf_counter()
-    g, parts = build_graph(args.config, 1.0, mine)
+    g, parts = build_graph(args.config, args.scale, mine)
     gnorm = int(g.train_mask.sum())
     layout = RankLayout(parts, owner, rank)
     eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config]),
@@ -224,9 +226,11 @@ def run_b200(args):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             epoch += 1
             eng.run_epoch(epoch, check=False)
+        host_issue_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         ev1.record()
         torch.cuda.synchronize()
         barrier()
@@ -322,6 +326,7 @@ def run_b200(args):
                      "note": "N=1: the 8 partitions share one GPU, so halo messages move HBM->HBM; "
                              "K1 writes each wire block straight into its receiver's buffer"},
             "gpu_launches": launches,
+            "host_issue_ms_per_step": round(host_issue_ms, 3),
             "clocks": clocks,
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 12},
@@ -380,6 +385,8 @@ def main():
     ap.add_argument("--staleness", type=int, default=0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="graph size factor (1.0 = the BASELINE shape; smaller only for diagnostics)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="test mode: all ranks on cuda:0 over gloo (the N>1 path on one GPU)")
     args = ap.parse_args()
