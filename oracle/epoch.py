@@ -315,6 +315,7 @@ class OracleTrainer:
         if not np.isfinite(tl):
             raise OracleProtocolError(f"NaN/inf loss at epoch {epoch}")
         self.loss = float(tl)
+        self.last_grads = total          # (test hook) the all-reduced gradients this epoch
         self.weights = [a.step(w, g) for w, g, a in zip(self.weights, total, self.adam)]
         return mode
 

@@ -224,3 +224,31 @@ def test_spmm_impls_track_oracle(impl, monkeypatch):
     for m, lo in zip(res.metrics, losses):
         assert m.train_loss == pytest.approx(lo, rel=5e-5)
     assert _wdiff(res.final_weights, o.weights) < 1e-4
+
+
+@pytest.mark.parametrize("model", ["gcn", "sage"])
+@pytest.mark.parametrize("order", ["pre", "post"])
+def test_gradients_match_oracle(model, order):
+    """Epoch-1 all-reduced weight gradients (trainer.py:313, 358) vs the
+    oracle's f64 gradients, passthrough halos: max|G - G_ref| <= 1e-5 max|G_ref|
+    per layer."""
+    from oracle.epoch import OracleTrainer
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
+    from paper_2303_01277_b200.transport import RankLayout
+    g = _graph(seed=17, npc=40)
+    parts = _parts(g, 3, model)
+    widths = (32, 24, 8, 4)
+    lay = RankLayout({p.id: p for p in parts}, [0] * 3, 0)
+    eng = DeviceRank(lay, ModelConfig(widths, model), TrainMode(), QuantConfig(32), 5, 0.01,
+                     int(g.train_mask.sum()), agg_order=order)
+    logits = eng.forward(1, "sync")
+    eng.backward(1, "sync", logits)
+    eng.reduce(1)
+    torch.cuda.synchronize()
+    o = OracleTrainer(parts, widths, model, "sync", 0, 32, 5, features=_f32(parts))
+    o.run_epoch(1)
+    for l, (gd, gr) in enumerate(zip(eng.G, o.last_grads)):
+        got = gd.double().cpu().numpy()
+        assert np.abs(got - gr).max() <= 1e-5 * np.abs(gr).max(), (l, np.abs(got - gr).max(), np.abs(gr).max())
+    assert float(eng.loss_dev) == pytest.approx(o.loss, rel=1e-6)
