@@ -252,3 +252,36 @@ def test_gradients_match_oracle(model, order):
         got = gd.double().cpu().numpy()
         assert np.abs(got - gr).max() <= 1e-5 * np.abs(gr).max(), (l, np.abs(got - gr).max(), np.abs(gr).max())
     assert float(eng.loss_dev) == pytest.approx(o.loss, rel=1e-6)
+
+
+def test_reddit_shaped_small_accuracy_vs_oracle():
+    """Reduced-scale Reddit-shaped graph (4,100 nodes, 246k edges, 602-d,
+    41 communities, noisy features so test accuracy is ~0.84, not saturated),
+    3-layer SAGE 602-64-41, 4 partitions, 1-bit halos, 15 epochs: mean final
+    test accuracy over seeds 1-3 within 0.5 points of the oracle's (the
+    north-star accuracy bar; the reference's own acceptance test allows 2
+    points between b=1 and b=32)."""
+    from dataclasses import replace
+
+    from oracle.epoch import OracleTrainer, accuracies, full_forward
+    from paper_2303_01277_b200 import datasets as ds
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.graph import build_partitions, mean_adjacency, normalize_adjacency
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, train
+    spec = replace(ds.REDDIT, num_nodes=4100, num_edges=246_000, communities=41, feature_noise=8.0, cut=0.05)
+    g = ds.generate_planted(spec)
+    _, _, parts = build_partitions(g, 4, "contiguous", 0, "sage")
+    a, m = normalize_adjacency(g).to_scipy(), mean_adjacency(g).to_scipy()
+    widths = (602, 64, 41)
+    dev, ref = [], []
+    for seed in (1, 2, 3):
+        res = train(g, parts, ModelConfig(widths, "sage"), TrainMode("sync", 0), QuantConfig(1), 15, seed,
+                    evaluate_each_epoch=False)
+        logits = full_forward(np.asarray(g.features, np.float64), a, res.final_weights, "sage", m)
+        dev.append(accuracies(logits, g.labels, (g.train_mask, g.val_mask, g.test_mask))["test_acc"])
+        o = OracleTrainer(parts, widths, "sage", "sync", 0, 1, seed, threads=4)
+        for e in range(1, 16):
+            o.run_epoch(e)
+        logits = full_forward(np.asarray(g.features, np.float64), a, o.weights, "sage", m)
+        ref.append(accuracies(logits, g.labels, (g.train_mask, g.val_mask, g.test_mask))["test_acc"])
+    assert abs(np.mean(dev) - np.mean(ref)) <= 0.005, (dev, ref)
