@@ -95,12 +95,11 @@ int hb_dequant_gather(const hb_segment_t* segs, int32_t nseg, int32_t num_dst,
 int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream);
 
-/* K3/K4 with the algorithm exposed: algo 0 = auto (column sweep when the rows
- * average >= 32 nonzeros, i.e. nnz >= 32 * nrows, and d > 64), 1 = row
- * gather (one warp, or a sub-warp group for d <= 64, per row), 2 = column
- * sweep (CTA-wide lockstep column windows so X rows are reused from L1 across
- * the block's rows; d > 64).  window = X rows per sweep window (0 = auto,
- * ~64 KB).  Same result contract as hb_spmm_csr. */
+/* K3/K4 row-gather kernel with its knobs exposed: algo 0 = auto, 1 = row
+ * gather (one warp, or an 8/16-lane group for d <= 64, per row, several
+ * nonzeros in flight); window > 0 = nonzeros kept in flight per lane group
+ * (tuning; 0 = default); nnz = stored entries (informational).  Same result
+ * contract as hb_spmm_csr. */
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
                    int32_t window, void* stream);

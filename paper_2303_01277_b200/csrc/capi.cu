@@ -104,7 +104,7 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
                    int32_t window, void* stream) {
-  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)) || algo < 0 || algo > 2)
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)) || algo < 0 || algo > 1)
     return fail(HB_EINVAL, "hb_spmm_csr_ex: bad arguments");
   return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, nnz, algo, window, S(stream)),
                "hb_spmm_csr_ex");

@@ -32,8 +32,6 @@
 namespace hb {
 namespace gt {
 
-uint32_t* g_gemm_dbg = nullptr;
-int g_gemm_dbg_mode = 0;
 constexpr int BM = 128;
 constexpr int BK = 32;                    // fp32 per 128-byte swizzle row
 constexpr int kThreads = 320;
@@ -60,8 +58,6 @@ struct Params {
   float* relu_out;
   int64_t ldr;
   float* ws;               // split-K partials [splits][M][N]
-  uint32_t* dbg;           // debug: stage-0 smem after the split + marker words
-  int dbg_mode;            // debug: 2 = K-major operands re-laid out without swizzle
 };
 
 __device__ __forceinline__ uint32_t rna_tf32(float x) {
@@ -208,47 +204,15 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const int s = it % S;
           mbar_wait(&conv[s], (it / S) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          if (p.dbg && it == 0 && blockIdx.x == 0) {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(smem);
-            for (int i = 0; i < C_::STAGE / 4; ++i) p.dbg[i] = w[i];
-            p.dbg[C_::STAGE / 4] = 0xC0FFEEu;
-            p.dbg[C_::STAGE / 4 + 1] = tmem;
-            p.dbg[C_::STAGE / 4 + 2] = idesc;
-          }
           const uint32_t st = smem_u32(smem + s * C_::STAGE);
           const uint32_t a_hi = st, a_lo = st + C_::A_BYTES;
           const uint32_t b_hi = st + 2 * C_::A_BYTES, b_lo = b_hi + C_::B_BYTES;
-          if (p.dbg_mode == 2) {
-            // interleaved no-swizzle K-major: byte(r,k) = (k/4)*(R*16) + (r/8)*128 + (r%8)*16 + (k%4)*4
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              auto nd = [](uint32_t a, uint32_t lbo) {
-                return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-                       ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
-              };
-              const uint32_t la = BM * 16, lb = BN * 16;
-              const uint64_t dah = nd(a_hi + 2 * kk * la, la), dal = nd(a_lo + 2 * kk * la, la);
-              const uint64_t dbh = nd(b_hi + 2 * kk * lb, lb), dbl = nd(b_lo + 2 * kk * lb, lb);
-              if (p.dbg && it == 0 && blockIdx.x == 0 && kk == 0) {
-                p.dbg[C_::STAGE / 4 + 4] = (uint32_t)dah; p.dbg[C_::STAGE / 4 + 5] = (uint32_t)(dah >> 32);
-              }
-              umma_tf32(d_tmem, dal, dbh, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-              umma_tf32(d_tmem, dah, dbl, idesc, 1u);
-              umma_tf32(d_tmem, dah, dbh, idesc, 1u);
-            }
-            umma_commit(&empty[s]);
-            continue;
-          }
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t dah = sw_desc(a_hi + kk * a_step, a_lbo, a_sbo, a_lay);
             const uint64_t dal = sw_desc(a_lo + kk * a_step, a_lbo, a_sbo, a_lay);
             const uint64_t dbh = sw_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
             const uint64_t dbl = sw_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
-            if (p.dbg && it == 0 && blockIdx.x == 0 && kk == 0) {
-              p.dbg[C_::STAGE / 4 + 4] = (uint32_t)dah; p.dbg[C_::STAGE / 4 + 5] = (uint32_t)(dah >> 32);
-              p.dbg[C_::STAGE / 4 + 6] = (uint32_t)dbh; p.dbg[C_::STAGE / 4 + 7] = (uint32_t)(dbh >> 32);
-              p.dbg[C_::STAGE / 4 + 8] = st;
-            }
             umma_tf32(d_tmem, dal, dbh, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
             umma_tf32(d_tmem, dah, dbl, idesc, 1u);
             umma_tf32(d_tmem, dah, dbh, idesc, 1u);
@@ -296,43 +260,6 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           h.w = rna_tf32(__uint_as_float(v.w)); l.w = rna_tf32(__uint_as_float(v.w) - __uint_as_float(h.w));
           b_hi[i] = h;
           b_lo[i] = l;
-        }
-        if (p.dbg_mode == 2 && !p.a_mn && !p.b_mn && BN == 64) {
-          // re-lay the (already split) K-major tiles out as interleaved no-swizzle
-          float va[32], vb[16], la_[32], lb_[16];
-          const float* fa = reinterpret_cast<const float*>(a_hi);
-          const float* fal = reinterpret_cast<const float*>(a_lo);
-          const float* fb = reinterpret_cast<const float*>(b_hi);
-          const float* fbl = reinterpret_cast<const float*>(b_lo);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int e = ct + 128 * j, r = e >> 5, k = e & 31;
-            const int src = r * 32 + ((((k >> 2) ^ (r & 7))) << 2) + (k & 3);
-            va[j] = fa[src]; la_[j] = fal[src];
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int e = ct + 128 * j, r = e >> 5, k = e & 31;
-            const int src = r * 32 + ((((k >> 2) ^ (r & 7))) << 2) + (k & 3);
-            vb[j] = fb[src]; lb_[j] = fbl[src];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          float* ga = reinterpret_cast<float*>(a_hi);
-          float* gal = reinterpret_cast<float*>(a_lo);
-          float* gb = reinterpret_cast<float*>(b_hi);
-          float* gbl = reinterpret_cast<float*>(b_lo);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int e = ct + 128 * j, r = e >> 5, k = e & 31;
-            const int dst = (k >> 2) * (BM * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
-            ga[dst] = va[j]; gal[dst] = la_[j];
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int e = ct + 128 * j, r = e >> 5, k = e & 31;
-            const int dst = (k >> 2) * (BN * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
-            gb[dst] = vb[j]; gbl[dst] = lb_[j];
-          }
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -558,8 +485,6 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
   }
   p.C = C; p.ldc = ldc; p.beta = beta; p.relu_out = p.splits > 1 ? nullptr : relu_out; p.ldr = ldr;
   p.ws = p.splits > 1 ? ws : nullptr;
-  p.dbg = g_gemm_dbg;
-  p.dbg_mode = g_gemm_dbg_mode;
   const int total = tiles * p.splits;
   const int grid = total < sms ? total : sms;
   static bool attr_set = false;
@@ -597,9 +522,3 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
 }
 
 }  // namespace hb
-
-extern "C" int hb_gemm_debug_buffer(uint32_t* p, int mode) {   // test-only hook (not in the public header)
-  hb::gt::g_gemm_dbg = p;
-  hb::gt::g_gemm_dbg_mode = mode;
-  return 0;
-}

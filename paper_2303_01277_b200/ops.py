@@ -117,7 +117,7 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
     return out
 
 
-SPMM_ALGOS = {"auto": 0, "rows": 1, "sweep": 2}
+SPMM_ALGOS = {"auto": 0, "rows": 1}
 
 
 def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "auto", window: int = 0):
