@@ -525,6 +525,192 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
   }
 }
 
+// K1, 1-bit: two rows per warp, one per 16-lane half.  The per-row work that
+// does not scale with d (segment lookup, TMA issue, min/max reductions, the
+// f64 scale, metadata) is shared by the two rows of a warp instruction, and
+// each lane runs two interleaved Philox4x64-10 blocks (64-column chunks in
+// pairs) for twice the multiply-chain ILP.  Each half streams its rows through
+// two TMA-filled smem row buffers, one row ahead, like the 32-lane kernel.
+template <int MINB>
+__global__ void __launch_bounds__(kQWarps * 32, MINB)
+quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
+                      int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
+                      uint32_t* __restrict__ flags, int ldr, int imgw) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  __shared__ __align__(8) uint64_t bars[kQWarps][2][2];   // [warp][half][buffer]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = lane >> 4, hl = lane & 15;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  const size_t per_half = (size_t)2 * ldr * 4 + (size_t)imgw * 4;
+  float* rows_s = reinterpret_cast<float*>(dsm + (size_t)(2 * warp + hw) * per_half);
+  uint32_t* buf = reinterpret_cast<uint32_t*>(rows_s + 2 * ldr);
+  if (hl == 0) {
+    mbar_init(&bars[warp][hw][0], 1);
+    mbar_init(&bars[warp][hw][1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const unsigned hmask = 0xffffu << (16 * hw);
+  const int rb = (d + 7) >> 3;
+  const uint32_t bytes = (uint32_t)(((d + 3) & ~3) * 4);
+  const int stride = gridDim.x * kQWarps * 2;
+  uint32_t phase_bits = 0u;
+  int cseg = 0;
+  int row = (blockIdx.x * kQWarps + warp) * 2 + hw;
+  if (row < total_rows && hl == 0) {
+    mbar_expect_tx(&bars[warp][hw][0], bytes);
+    tma_load_1d(rows_s, src + (int64_t)__ldg(row_idx + row) * ld, bytes, &bars[warp][hw][0]);
+  }
+  for (int k = 0;; row += stride, ++k) {
+    const bool active = row < total_rows;
+    if (!__any_sync(0xffffffffu, active)) break;
+    const int cur = k & 1;
+    const int nxt = row + stride;
+    if (nxt < total_rows && hl == 0) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bars[warp][hw][cur ^ 1], bytes);
+      tma_load_1d(rows_s + (cur ^ 1) * ldr, src + (int64_t)__ldg(row_idx + nxt) * ld, bytes,
+                  &bars[warp][hw][cur ^ 1]);
+    }
+    if (active && !(row >= seg_begin[cseg] && row < seg_begin[cseg + 1]))
+      cseg = find_segment_smem(seg_begin, nseg, row);
+    const hb_segment_t& sg = segs_s[cseg];
+    const int r = row - sg.row_begin;
+    const uint64_t e_row = sg.elem_offset + (uint64_t)r * (uint64_t)d;
+    const int delta = (int)(e_row & 3ull);
+    const uint64_t blk0 = e_row >> 2;
+    const int nch = (d + delta + 63) >> 6;                        // 64-column chunks of this half
+    const int nch2 = max(nch, __shfl_xor_sync(0xffffffffu, nch, 16));
+    uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
+    const float* xs = rows_s + cur * ldr;
+    if (active) {
+      mbar_wait(&bars[warp][hw][cur], (phase_bits >> cur) & 1u);
+      phase_bits ^= 1u << cur;
+    }
+    __syncwarp();
+
+    // ---- pass 1 (smem): min / max / finiteness, reduced within the half --------
+    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+    bool bad = false;
+    if (active) {
+      const int d4 = d >> 2;
+      for (int c4 = hl; c4 < d4; c4 += 16) {
+        const float4 a = reinterpret_cast<const float4*>(xs)[c4];
+        mn = fminf(fminf(mn, a.x), fminf(a.y, fminf(a.z, a.w)));
+        mx = fmaxf(fmaxf(mx, a.x), fmaxf(a.y, fmaxf(a.z, a.w)));
+        bad |= !(isfinite(a.x) & isfinite(a.y) & isfinite(a.z) & isfinite(a.w));
+      }
+      for (int c = 4 * d4 + hl; c < d; c += 16) {
+        const float a = xs[c];
+        mn = fminf(mn, a);
+        mx = fmaxf(mx, a);
+        bad |= !isfinite(a);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const bool badh = (__ballot_sync(0xffffffffu, bad) & hmask) != 0u;
+    if (badh && active && hl == 0) atomicOr(flags, HB_FLAG_NONFINITE);
+    const bool live_row = active && !badh;
+    if (live_row && r == 0 && hl == 0) write_header(out, 1, sg.num_rows, d);
+    QuantRowCtx q;
+    q.bits = 1;
+    q.B = 1;
+    q.mn = mn;
+    q.s = live_row ? __double2float_rn(__dsub_rn((double)mx, (double)mn)) : 0.f;
+    q.live = q.s > 0.0f;
+    q.inv_s = q.live ? __frcp_rn(q.s) : 0.f;
+    q.fast = q.live && q.s >= 7.888609052210118e-31f && fabsf(mn) <= 1.2676506002282294e30f &&
+             fabsf(mx) <= 1.2676506002282294e30f;
+    q.E = 3.0f * 2.384185791015625e-07f;                          // (B+2) * 2^-22
+    q.Eu = q.E + 2.384185791015625e-07f;
+    if (live_row && hl == 0) {
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r) = q.mn;
+      *reinterpret_cast<float*>(out + HB_HEADER_BYTES + 8 * (int64_t)r + 4) = q.s;
+    }
+
+    // ---- pass 2: chunk pairs, two interleaved Philox blocks per lane ------------
+    for (int t = 0; t < nch2; t += 2) {
+      uint32_t f2[2] = {0u, 0u};
+      if (q.live) {
+        U64x4 ua, ub;
+        philox4x64_10_x2(blk0 + (uint64_t)(16 * t + hl) + 1ull, blk0 + (uint64_t)(16 * (t + 1) + hl) + 1ull,
+                         sg.key0, sg.key1, ua, ub);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const U64x4& u = j ? ub : ua;
+          const uint64_t ws[4] = {u.w0, u.w1, u.w2, u.w3};
+          const int tt = t + j;
+          const int c0 = 64 * tt + 4 * hl - delta;
+          const bool full = q.fast && (64 * tt - delta >= 0) && (64 * tt - delta + 64 <= d);
+          uint32_t code[4];
+          bool amb[4];
+          if (full) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) code[i] = quant_fast_b1(xs[c0 + i], q, ws[i], amb[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int c = c0 + i;
+              amb[i] = false;
+              code[i] = 0;
+              if (c >= 0 && c < d) {
+                if (q.fast) code[i] = quant_fast_b1(xs[c], q, ws[i], amb[i]);
+                else amb[i] = true;
+              }
+            }
+          }
+          if (amb[0] | amb[1] | amb[2] | amb[3]) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (amb[i]) code[i] = (uint32_t)quant_exact(xs[c0 + i], q.mn, q.s, 1, ws[i]);
+          }
+          f2[j] = code[0] | (code[1] << 1) | (code[2] << 2) | (code[3] << 3);
+        }
+      }
+      // 64-bit chunk image = 16 lanes x 4 bits: word (hl >> 3) from lanes 8w .. 8w+7
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t w = f2[j] << (4 * (hl & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((hl & 7) == 0 && t + j < nch) buf[2 * (t + j) + (hl >> 3)] = w;
+      }
+    }
+    __syncwarp();
+    // ---- emit the row image (the Philox frame starts delta columns early) --------
+    if (live_row) {
+      uint8_t* pay = out + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+      const int nrw = (rb + 3) >> 2;
+      const int total_w = 2 * nch;
+      const bool wordstore = ((((uintptr_t)pay) & 3) == 0) && ((rb & 3) == 0);
+      for (int m = hl; m < nrw; m += 16) {
+        const uint32_t lo = buf[m];
+        const uint32_t hi = (m + 1 < total_w) ? buf[m + 1] : 0u;
+        const uint32_t rw = delta ? ((lo >> delta) | (hi << (32 - delta))) : lo;
+        if (wordstore) {
+          reinterpret_cast<uint32_t*>(pay)[m] = rw;
+        } else {
+#pragma unroll
+          for (int b4 = 0; b4 < 4; ++b4)
+            if (4 * m + b4 < rb) pay[4 * m + b4] = (uint8_t)(rw >> (8 * b4));
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Generic per-element path (rows wider than the smem row image).
 __global__ void __launch_bounds__(kQWarps * 32)
 quantize_gather_wide_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
@@ -837,7 +1023,24 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
   const dim3 blk(kQWarps * 32);
 #define ARGS src, ld, row_idx, total_rows, segs, nseg, d, bits, flags
   static const bool no_tma = getenv("HB_K1_NO_TMA") != nullptr;
+  static const bool no_hw = getenv("HB_K1_NO_HW") != nullptr;
   const bool aligned = (ld % 4 == 0) && ((((uintptr_t)src) & 15) == 0);
+  if (!no_tma && !no_hw && aligned && bits == 1 && d <= 4096 && nseg <= kMaxSmemSegs) {
+    const int ldr = (d + 3) & ~3;
+    const int nch64 = (d + 3 + 63) >> 6;
+    const int imgw = (2 * nch64 + 2 + 3) & ~3;
+    const size_t dyn = (size_t)kQWarps * 2 * (2 * ldr * 4 + imgw * 4);
+    if (dyn <= 200 * 1024) {
+      static const int minb = getenv("HB_K1_MINB") ? atoi(getenv("HB_K1_MINB")) : 3;
+      auto kern = minb == 2 ? quantize_b1_hw_kernel<2> : (minb == 4 ? quantize_b1_hw_kernel<4>
+                                                                     : quantize_b1_hw_kernel<3>);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      const int want2 = (total_rows + 2 * kQWarps - 1) / (2 * kQWarps);
+      const int grid2 = want2 < num_sms() * 16 ? want2 : num_sms() * 16;
+      kern<<<grid2, kQWarps * 32, dyn, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags, ldr, imgw);
+      return cudaGetLastError();
+    }
+  }
   if (!no_tma && aligned && bits != 32 && d <= 4096) {
     const int ldr = (d + 3) & ~3;
     const int imgw = ((pow2 ? 4 * bits * nch + 2 : ((64 + bits * nch * 128) >> 5) + 4) + 3) & ~3;  // 16B multiple
