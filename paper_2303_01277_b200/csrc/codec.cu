@@ -559,10 +559,11 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
   const unsigned hmask = 0xffffu << (16 * hw);
   const int rb = (d + 7) >> 3;
   const uint32_t bytes = (uint32_t)(((d + 3) & ~3) * 4);
-  const int stride = gridDim.x * kQWarps * 2;
+  const int nwarps = blockDim.x >> 5;                           // <= kQWarps
+  const int stride = gridDim.x * nwarps * 2;
   uint32_t phase_bits = 0u;
   int cseg = 0;
-  int row = (blockIdx.x * kQWarps + warp) * 2 + hw;
+  int row = (blockIdx.x * nwarps + warp) * 2 + hw;
   if (row < total_rows && hl == 0) {
     mbar_expect_tx(&bars[warp][hw][0], bytes);
     tma_load_1d(rows_s, src + (int64_t)__ldg(row_idx + row) * ld, bytes, &bars[warp][hw][0]);
@@ -1029,15 +1030,19 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
     const int ldr = (d + 3) & ~3;
     const int nch64 = (d + 3 + 63) >> 6;
     const int imgw = (2 * nch64 + 2 + 3) & ~3;
-    const size_t dyn = (size_t)kQWarps * 2 * (2 * ldr * 4 + imgw * 4);
+    // wide rows: smaller CTAs so the per-warp row buffers do not cap the warps per SM
+    const size_t per_warp = (size_t)2 * (2 * ldr * 4 + imgw * 4);
+    const int wpc = per_warp > 6 * 1024 ? 4 : kQWarps;
+    const size_t dyn = (size_t)wpc * per_warp;
     if (dyn <= 200 * 1024) {
       static const int minb = getenv("HB_K1_MINB") ? atoi(getenv("HB_K1_MINB")) : 3;
       auto kern = minb == 2 ? quantize_b1_hw_kernel<2> : (minb == 4 ? quantize_b1_hw_kernel<4>
                                                                      : quantize_b1_hw_kernel<3>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      const int want2 = (total_rows + 2 * kQWarps - 1) / (2 * kQWarps);
-      const int grid2 = want2 < num_sms() * 16 ? want2 : num_sms() * 16;
-      kern<<<grid2, kQWarps * 32, dyn, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags, ldr, imgw);
+      const int want2 = (total_rows + 2 * wpc - 1) / (2 * wpc);
+      const int cap = num_sms() * 16 * (kQWarps / wpc);
+      const int grid2 = want2 < cap ? want2 : cap;
+      kern<<<grid2, wpc * 32, dyn, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags, ldr, imgw);
       return cudaGetLastError();
     }
   }
