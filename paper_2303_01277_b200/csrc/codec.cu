@@ -996,6 +996,102 @@ dequant_rows_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_d
   }
 }
 
+// K2 forward, 1 bit, batched: a warp takes 32 consecutive destinations at a
+// time, lane l resolves destination l (indices, segment, metadata, payload
+// pointer) with independent loads, and the rows are then written one after
+// another from register broadcasts — the dependent index/metadata chain is
+// paid once per 32 rows instead of once per row.  Values are bit-identical to
+// dequant_rows_kernel's fp32 fast path.
+template <int NCH>
+__global__ void __launch_bounds__(kQWarps * 32)
+dequant_b1_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_dst,
+                          const int32_t* __restrict__ dst_rows, const int32_t* __restrict__ src_ptr,
+                          const int32_t* __restrict__ src_rows, int d, float* __restrict__ dst, int64_t ld) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  const int rb = (d + 7) >> 3;
+  const bool vec = ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
+  int cs = 0;
+  for (int i0 = (blockIdx.x * kQWarps + warp) * 32; i0 < num_dst; i0 += gridDim.x * kQWarps * 32) {
+    const int i = i0 + lane;
+    const bool valid = i < num_dst;
+    const int my_t = valid ? dst_rows[i] : 0;
+    const int my_k0 = valid ? src_ptr[i] : 0;
+    const int my_k1 = valid ? src_ptr[i + 1] : 0;
+    const bool my_single = valid && my_k1 - my_k0 == 1;
+    const int my_q = my_single ? src_rows[my_k0] : 0;
+    if (my_single && !(my_q >= seg_begin[cs] && my_q < seg_begin[cs + 1]))
+      cs = find_segment_smem(seg_begin, nseg, my_q);
+    float my_mn = 0.f, my_one = 0.f;
+    uint64_t my_pay = 0;
+    if (my_single) {
+      const hb_segment_t& sg = segs_s[cs];
+      const int r = my_q - sg.row_begin;
+      const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+      const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
+      my_mn = mp[0];
+      my_one = __fadd_rn(mp[1], my_mn);
+      my_pay = reinterpret_cast<uint64_t>(blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb);
+    }
+    const unsigned singles = __ballot_sync(0xffffffffu, my_single);
+    const int n = min(32, num_dst - i0);
+    for (int j = 0; j < n; ++j) {
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      float* out = dst + (int64_t)t * ld;
+      if (!((singles >> j) & 1u)) {
+        // zero or several received rows for this destination: chunk-wise f64 sum
+        const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
+        for (int c0 = 4 * lane; c0 < d; c0 += 128) {
+          double a4[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int k = k0; k < k1; ++k) {
+            const int q = src_rows[k];
+            const hb_segment_t& sg = segs_s[find_segment_smem(seg_begin, nseg, q)];
+            const int r = q - sg.row_begin;
+            const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+            const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
+            const uint8_t* pay = blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+            int code[4];
+            codes4(pay, rb, c0, 1, d, code);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              a4[e] = __dadd_rn(a4[e], __dadd_rn(__dmul_rn((double)mp[1], (double)code[e]), (double)mp[0]));
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (c0 + e < d) out[c0 + e] = __double2float_rn(a4[e]);
+        }
+        continue;
+      }
+      const float mn = __shfl_sync(0xffffffffu, my_mn, j);
+      const float one = __shfl_sync(0xffffffffu, my_one, j);
+      const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, j));
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        if (c0 >= d) continue;
+        const uint32_t nib = (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+        const float4 v = make_float4((nib & 1u) ? one : mn, (nib & 2u) ? one : mn, (nib & 4u) ? one : mn,
+                                     (nib & 8u) ? one : mn);
+        if (vec && c0 + 3 < d) {
+          *reinterpret_cast<float4*>(out + c0) = v;
+        } else {
+          out[c0] = v.x;
+          if (c0 + 1 < d) out[c0 + 1] = v.y;
+          if (c0 + 2 < d) out[c0 + 2] = v.z;
+          if (c0 + 3 < d) out[c0 + 3] = v.w;
+        }
+      }
+    }
+  }
+}
+
 __global__ void philox_uniforms_kernel(uint64_t k0, uint64_t k1, uint64_t start, int64_t n,
                                        double* __restrict__ out) {
   const uint64_t first_blk = start >> 2;
@@ -1090,9 +1186,15 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
                                                                        src_ptr, src_rows, d, bits, dst, ld, accumulate)
     // one received row per destination, 1 bit, overwrite: the fp32 fast path
     if (!accumulate && bits == 1) {
-      if (nch <= 2) HB_K2(2, true);
-      else if (nch <= 4) HB_K2(4, true);
-      else HB_K2(8, true);
+      const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
+      const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
+#define HB_K2B(N) dequant_b1_batched_kernel<N><<<g32, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, \
+                                                                          src_rows, d, dst, ld)
+      if (nch <= 1) HB_K2B(1);
+      else if (nch <= 2) HB_K2B(2);
+      else if (nch <= 4) HB_K2B(4);
+      else HB_K2B(8);
+#undef HB_K2B
     } else if (nch == 1) HB_K2(1, false);
     else if (nch == 2) HB_K2(2, false);
     else if (nch == 3) HB_K2(3, false);
