@@ -1092,6 +1092,111 @@ dequant_b1_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int
   }
 }
 
+// K2 general (any b <= 16, overwrite or ascending-peer accumulate), batched
+// like dequant_b1_batched_kernel: 32 destinations per warp; their received
+// rows are contiguous in src_rows, so a sliding window of 32 sources is
+// resolved lane-parallel (segment, metadata, payload pointer) and broadcast.
+// Per element: f64(sc) * code + f64(mn) (separate mul and add), summed in
+// f64 on top of the current value when accumulating, one fp32 rounding —
+// exactly dequant_rows_kernel's arithmetic.
+template <int NCH>
+__global__ void __launch_bounds__(kQWarps * 32)
+dequant_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_dst,
+                       const int32_t* __restrict__ dst_rows, const int32_t* __restrict__ src_ptr,
+                       const int32_t* __restrict__ src_rows, int d, int bits, float* __restrict__ dst,
+                       int64_t ld, int accumulate) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  const int rb = (d * bits + 7) >> 3;
+  const bool vec = ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
+  int cs = 0;
+  float my_mn = 0.f, my_sc = 0.f;
+  uint64_t my_pay = 0;
+  auto prepare = [&](int w0, int s1) {
+    const int k = w0 + lane;
+    my_mn = 0.f;
+    my_sc = 0.f;
+    my_pay = 0;
+    if (k < s1) {
+      const int q = src_rows[k];
+      if (!(q >= seg_begin[cs] && q < seg_begin[cs + 1])) cs = find_segment_smem(seg_begin, nseg, q);
+      const hb_segment_t& sg = segs_s[cs];
+      const int r = q - sg.row_begin;
+      const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+      const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
+      my_mn = mp[0];
+      my_sc = mp[1];
+      my_pay = reinterpret_cast<uint64_t>(blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb);
+    }
+  };
+  for (int i0 = (blockIdx.x * kQWarps + warp) * 32; i0 < num_dst; i0 += gridDim.x * kQWarps * 32) {
+    const int i = i0 + lane;
+    const bool valid = i < num_dst;
+    const int my_t = valid ? dst_rows[i] : 0;
+    const int my_k0 = valid ? src_ptr[i] : 0;
+    const int my_k1 = valid ? src_ptr[i + 1] : 0;
+    const int n = min(32, num_dst - i0);
+    const int s0 = __shfl_sync(0xffffffffu, my_k0, 0);
+    const int s1 = __shfl_sync(0xffffffffu, my_k1, n - 1);
+    int w0 = s0;
+    prepare(w0, s1);
+    for (int j = 0; j < n; ++j) {
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
+      float* out = dst + (int64_t)t * ld;
+      double acc[NCH][4];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = ch * 128 + 4 * lane + e;
+          acc[ch][e] = (accumulate && c < d) ? (double)out[c] : 0.0;
+        }
+      for (int k = k0; k < k1; ++k) {
+        if (k >= w0 + 32) {           // warp-uniform: slide the source window
+          w0 = k;
+          prepare(w0, s1);
+        }
+        const int sl = k - w0;
+        const double mn = (double)__shfl_sync(0xffffffffu, my_mn, sl);
+        const double sc = (double)__shfl_sync(0xffffffffu, my_sc, sl);
+        const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, sl));
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c0 = ch * 128 + 4 * lane;
+          if (c0 >= d) continue;
+          int code[4];
+          codes4(pay, rb, c0, bits, d, code);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            acc[ch][e] = __dadd_rn(acc[ch][e], __dadd_rn(__dmul_rn(sc, (double)code[e]), mn));
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        if (c0 >= d) continue;
+        if (vec && c0 + 3 < d) {
+          *reinterpret_cast<float4*>(out + c0) =
+              make_float4(__double2float_rn(acc[ch][0]), __double2float_rn(acc[ch][1]),
+                          __double2float_rn(acc[ch][2]), __double2float_rn(acc[ch][3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (c0 + e < d) out[c0 + e] = __double2float_rn(acc[ch][e]);
+        }
+      }
+    }
+  }
+}
+
 __global__ void philox_uniforms_kernel(uint64_t k0, uint64_t k1, uint64_t start, int64_t n,
                                        double* __restrict__ out) {
   const uint64_t first_blk = start >> 2;
@@ -1193,8 +1298,18 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
       if (nch <= 1) HB_K2B(1);
       else if (nch <= 2) HB_K2B(2);
       else if (nch <= 4) HB_K2B(4);
+      else if (nch <= 5) HB_K2B(5);
       else HB_K2B(8);
 #undef HB_K2B
+    } else if (bits != 32 && nch <= 4) {
+      const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
+      const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
+#define HB_K2G(N) dequant_batched_kernel<N><<<g32, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, \
+                                                                       src_rows, d, bits, dst, ld, accumulate)
+      if (nch <= 1) HB_K2G(1);
+      else if (nch <= 2) HB_K2G(2);
+      else HB_K2G(4);
+#undef HB_K2G
     } else if (nch == 1) HB_K2(1, false);
     else if (nch == 2) HB_K2(2, false);
     else if (nch == 3) HB_K2(3, false);
