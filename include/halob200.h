@@ -134,7 +134,8 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
 /* Selects the K5-K7 kernel: 0 = TMA-fed warp-specialised tcgen05 kernel
  * whenever both operands are TMA-describable (16-byte aligned, unit stride on
  * one axis, 16-byte row stride), else the SIMT-staged tcgen05 kernel;
- * 1 = SIMT-staged kernel only (tests compare the two). */
+ * 1 = SIMT-staged kernel only; 2 = as 0 but 128 < N <= 256 runs on CTA
+ * pairs (tcgen05.mma.cta_group::2, 256-row tiles, half of B per SM). */
 int hb_gemm_set_path(int32_t path);
 
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:

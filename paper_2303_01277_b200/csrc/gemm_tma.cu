@@ -507,12 +507,43 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
 
 }  // namespace gt
 
+// host helpers shared with the CTA-pair kernel (gemm_tma2.cu)
+bool gemm_make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld, int box_outer,
+                   bool mn_major) {
+  return gt::make_map(m, base, inner, outer, ld, box_outer, mn_major);
+}
+cudaError_t gemm_bsplit(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp, float* hi, float* lo,
+                        cudaStream_t st) {
+  int g = (int)(((int64_t)N * Kp + 255) / 256);
+  if (g > num_sms() * 4) g = num_sms() * 4;
+  gt::bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, Kp, hi, lo);
+  return cudaGetLastError();
+}
+cudaError_t gemm_splitk_reduce(const float* ws, int splits, int M, int N, float* C, int64_t ldc, float beta,
+                               float* relu_out, int64_t ldr, cudaStream_t st) {
+  int g = (int)(((int64_t)M * N + 255) / 256);
+  if (g > num_sms() * 8) g = num_sms() * 8;
+  gt::splitk_reduce2_kernel<<<g, 256, 0, st>>>(ws, splits, M, N, C, ldc, beta, relu_out, ldr);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemm_tma_pair(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
+                                 float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+extern int g_gemm_pair;
+
 // Returns cudaErrorNotSupported when an operand is not TMA-describable (the
 // caller then uses the SIMT-staged kernel).
 cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
                             int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
                             int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
   if (!gt::tma_ok(A, lda_m, lda_k) || !gt::tma_ok(B, ldb_n, ldb_k)) return cudaErrorNotSupported;
+  // CTA-pair (cta_group::2) variant: opt-in — it halves the B bytes per SM but
+  // measured no faster than the single-CTA kernel on the trainer's shapes
+  static const bool pair = getenv("HB_GEMM_PAIR") != nullptr;
+  if ((pair || g_gemm_pair) && N > 128 && N <= 256) {
+    const cudaError_t e = launch_gemm_tma_pair(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out,
+                                               ldr, ws, ws_floats, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   static const int max_bn = getenv("HB_GEMM_BN") ? atoi(getenv("HB_GEMM_BN")) : 256;
   if (N <= 64 || max_bn == 64)
     return gt::launch_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);

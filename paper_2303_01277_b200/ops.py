@@ -143,7 +143,8 @@ def gemm(A, B, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
 
 
 def gemm_set_path(path: int):
-    """0: TMA warp-specialised tcgen05 kernel where operands allow; 1: SIMT-staged kernel."""
+    """0: TMA warp-specialised tcgen05 kernel where operands allow; 1: SIMT-staged kernel;
+    2: as 0 with CTA pairs (cta_group::2) for 128 < N <= 256."""
     _lib.call("hb_gemm_set_path", int(path))
 
 

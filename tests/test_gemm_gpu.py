@@ -65,7 +65,7 @@ def _pad(rows, cols, g, ld=None):
     return torch.randn(rows, ld, device="cuda", generator=g)[:, :cols]
 
 
-@pytest.fixture(params=[0, 1], ids=["tma", "simt_staged"])
+@pytest.fixture(params=[0, 1, 2], ids=["tma", "simt_staged", "tma_cta_pair"])
 def gemm_path(request):
     from paper_2303_01277_b200 import ops
     ops.gemm_set_path(request.param)
@@ -134,7 +134,7 @@ def test_gemm_accumulate_relu_and_split_relu(gemm_path):
 
 
 @pytest.mark.parametrize("N,K,kind", [(256, 602, "nn"), (41, 256, "nn"), (256, 256, "nt"), (602, 41, "nt")])
-def test_gemm_presplit_weight_operand(N, K, kind):
+def test_gemm_presplit_weight_operand(N, K, kind, gemm_path):
     """Tall GEMMs (>= 2 tiles per SM) with a weight-sized B take the path that
     splits B into tf32 hi / lo once (workspace) instead of per CTA."""
     from paper_2303_01277_b200 import ops
