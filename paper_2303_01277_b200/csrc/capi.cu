@@ -29,6 +29,7 @@ cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, co
                                float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_path;
 extern int g_gemm_pair;
+extern int g_gemm_ts;
 cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                               const int2*, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
                               float*, int64_t, cudaStream_t);
@@ -137,10 +138,11 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
 }
 
 int hb_gemm_set_path(int32_t path) {
-  if (path < 0 || path > 2)
-    return fail(HB_EINVAL, "hb_gemm_set_path: path must be 0 (auto), 1 (SIMT-staged) or 2 (CTA pair)");
+  if (path < 0 || path > 3)
+    return fail(HB_EINVAL, "hb_gemm_set_path: path must be 0 (auto), 1 (SIMT-staged), 2 (CTA pair) or 3 (A in TMEM)");
   hb::g_gemm_path = path == 1 ? 1 : 0;
   hb::g_gemm_pair = path == 2 ? 1 : 0;
+  hb::g_gemm_ts = path == 3 ? 1 : 0;
   return HB_OK;
 }
 

@@ -294,6 +294,7 @@ cudaError_t launch_gemm_tma(int, int, int, const float*, int64_t, int64_t, const
 
 int g_gemm_path = 0;   // 0: TMA warp-specialised kernel when operands allow; 1: SIMT-staged kernel only
 int g_gemm_pair = 0;   // 1: use the CTA-pair (cta_group::2) kernel for 128 < N <= 256
+int g_gemm_ts = 0;     // 1: A split into TMEM (tcgen05.mma A-from-TMEM) kernel
 
 cudaError_t launch_gemm_tf32x3(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
                                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,

@@ -529,6 +529,10 @@ cudaError_t gemm_splitk_reduce(const float* ws, int splits, int M, int N, float*
 cudaError_t launch_gemm_tma_pair(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
                                  float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_pair;
+extern int g_gemm_ts;
+extern int g_gemm_path;
+cudaError_t launch_gemm_ts(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
+                           int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 
 // Returns cudaErrorNotSupported when an operand is not TMA-describable (the
 // caller then uses the SIMT-staged kernel).
@@ -538,6 +542,17 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
   if (!gt::tma_ok(A, lda_m, lda_k) || !gt::tma_ok(B, ldb_n, ldb_k)) return cudaErrorNotSupported;
   // CTA-pair (cta_group::2) variant: opt-in — it halves the B bytes per SM but
   // measured no faster than the single-CTA kernel on the trainer's shapes
+  // A-in-TMEM kernel: default for tall GEMMs (many 128-row tiles, no split-K);
+  // the long-K weight gradients (split-K) stay on the all-smem kernel, which
+  // measured faster there
+  static const int ts_env = getenv("HB_GEMM_TS") ? atoi(getenv("HB_GEMM_TS")) : -1;
+  const bool tall = (int64_t)((M + 127) / 128) * ((N + 127) / 128) >= num_sms();
+  const bool use_ts = ts_env >= 0 ? ts_env == 1 : (g_gemm_ts || (g_gemm_path == 0 && !g_gemm_pair && tall));
+  if (use_ts) {
+    const cudaError_t e = launch_gemm_ts(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
+                                         ws_floats, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   static const bool pair = getenv("HB_GEMM_PAIR") != nullptr;
   if ((pair || g_gemm_pair) && N > 128 && N <= 256) {
     const cudaError_t e = launch_gemm_tma_pair(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out,
