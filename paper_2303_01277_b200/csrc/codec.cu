@@ -560,20 +560,26 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
   const int rb = (d + 7) >> 3;
   const uint32_t bytes = (uint32_t)(((d + 3) & ~3) * 4);
   const int nwarps = blockDim.x >> 5;                           // <= kQWarps
-  const int stride = gridDim.x * nwarps * 2;
+  // blocked rows per half-warp: consecutive rows stay in one message (the
+  // cached segment hits) and their gather indices are neighbours
+  const int nhalves = gridDim.x * nwarps * 2;
+  const int chunk = (total_rows + nhalves - 1) / nhalves;
+  const int hid = (blockIdx.x * nwarps + warp) * 2 + hw;
+  const int row_end = min(total_rows, (hid + 1) * chunk);
+  const int stride = 1;
   uint32_t phase_bits = 0u;
   int cseg = 0;
-  int row = (blockIdx.x * nwarps + warp) * 2 + hw;
-  if (row < total_rows && hl == 0) {
+  int row = hid * chunk;
+  if (row < row_end && hl == 0) {
     mbar_expect_tx(&bars[warp][hw][0], bytes);
     tma_load_1d(rows_s, src + (int64_t)__ldg(row_idx + row) * ld, bytes, &bars[warp][hw][0]);
   }
   for (int k = 0;; row += stride, ++k) {
-    const bool active = row < total_rows;
+    const bool active = row < row_end;
     if (!__any_sync(0xffffffffu, active)) break;
     const int cur = k & 1;
     const int nxt = row + stride;
-    if (nxt < total_rows && hl == 0) {
+    if (nxt < row_end && hl == 0) {
       fence_proxy_async_smem();
       mbar_expect_tx(&bars[warp][hw][cur ^ 1], bytes);
       tma_load_1d(rows_s + (cur ^ 1) * ldr, src + (int64_t)__ldg(row_idx + nxt) * ld, bytes,
