@@ -203,8 +203,13 @@ def run_b200(args):
     eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config]),
                      TrainMode(args.mode, args.staleness), QuantConfig(args.bits), args.seed, 0.01, gnorm,
                      device=torch.device("cuda", local))
-    feats_host = torch.from_numpy(np.concatenate([np.asarray(p.features, dtype=np.float32)
-                                                  for p in layout.parts])).pin_memory()
+    # the step's input features, pinned and laid out like the device buffer
+    # (16-byte padded rows) so each step's upload is one contiguous copy
+    feats = np.concatenate([np.asarray(p.features, dtype=np.float32) for p in layout.parts])
+    ldf = eng.Ht[1].shape[1]
+    feats_host = torch.zeros((feats.shape[0], ldf), dtype=torch.float32).pin_memory()
+    feats_host[:, :feats.shape[1]] = torch.from_numpy(feats)
+    del feats
     del g
     setup_s = time.perf_counter() - t0
     epoch = 0
@@ -251,7 +256,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         epoch += 1
-        eng.Ht[1][:eng.NL, :WIDTHS[args.config][0]].copy_(feats_host, non_blocking=True)
+        eng.Ht[1][:eng.NL].copy_(feats_host, non_blocking=True)
         eng.run_epoch(epoch, check=True)            # reads loss + codec flag back (D2H)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)

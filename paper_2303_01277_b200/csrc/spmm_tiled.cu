@@ -106,11 +106,17 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
 
   if (warp == kConsumers) {
     // ---------------- producer ----------------
-    if (lane == 0) {
+    // one producer lane per ring stage (lane s issues every tile that lands
+    // in stage s, so each barrier is still waited on in phase order by a
+    // single thread): the tiles' metadata loads (tile_off / tile_win,
+    // dependent global reads) are then S deep in flight ahead of the ring
+    if (lane < S) {
       int it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int b = item / a.npanels, pn = item % a.npanels;
-        for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
+        const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
+        for (int t = t0; t < t1; ++t, ++it) {
+          if (it % S != lane) continue;
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           uint8_t* st = smem + s * S_::STAGE;
