@@ -131,6 +131,19 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
                 const float* B, int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta,
                 float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream);
 
+/* Dual dense combine C = A1 B1 + A2 B2 (+ beta C), optional ReLU copy: the
+ * SAGE layer z = [h | A h] [W_top; W_bot] (trainer.py:294) and its input
+ * gradient j = [S | m] [W_bot^T; W_top^T] (trainer.py:318-321) without
+ * materialising the concatenation.  One pass of the A-in-TMEM kernel over
+ * both K ranges (C written once, never read back) when all operands are
+ * TMA-describable with matching major order; otherwise two hb_gemm_f32
+ * passes.  Operand conventions as hb_gemm_f32; K1, K2 > 0. */
+int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1_m, int64_t lda1_k,
+                 const float* B1, int64_t ldb1_k, int64_t ldb1_n, int32_t K2, const float* A2,
+                 int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,
+                 float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr, float* ws,
+                 int64_t ws_floats, void* stream);
+
 /* Selects the K5-K7 kernel: 0 = TMA-fed warp-specialised tcgen05 kernel
  * whenever both operands are TMA-describable (16-byte aligned, unit stride on
  * one axis, 16-byte row stride), else the SIMT-staged tcgen05 kernel;

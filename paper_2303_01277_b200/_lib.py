@@ -26,7 +26,7 @@ assert SEGMENT_DTYPE.itemsize == 40
 
 EXPORTS = (
     "hb_version", "hb_last_error", "hb_philox_uniforms", "hb_quantize_gather",
-    "hb_dequant_gather", "hb_spmm_csr", "hb_spmm_csr_ex", "hb_spmm_tiled", "hb_gemm_f32", "hb_gemm_set_path", "hb_softmax_xent", "hb_relu", "hb_relu_grad_mul",
+    "hb_dequant_gather", "hb_spmm_csr", "hb_spmm_csr_ex", "hb_spmm_tiled", "hb_gemm_f32", "hb_gemm2_f32", "hb_gemm_set_path", "hb_softmax_xent", "hb_relu", "hb_relu_grad_mul",
     "hb_adam_step", "hb_argmax_accuracy", "hb_dropout",
 )
 
@@ -38,6 +38,8 @@ _SIGS = {
     "hb_spmm_csr": [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, P],
     "hb_gemm_f32": [c_int32, c_int32, c_int32, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64,
                     c_float, P, c_int64, P, c_int64, P],
+    "hb_gemm2_f32": [c_int32, c_int32, c_int32, P, c_int64, c_int64, P, c_int64, c_int64, c_int32, P, c_int64,
+                     c_int64, P, c_int64, c_int64, P, c_int64, c_float, P, c_int64, P, c_int64, P],
     "hb_gemm_set_path": [c_int32],
     "hb_spmm_tiled": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64, P],
     "hb_spmm_csr_ex": [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, c_int64, c_int32, c_int32, P],

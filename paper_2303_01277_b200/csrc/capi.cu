@@ -27,6 +27,9 @@ cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, u
 
 cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
                                float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+cudaError_t launch_gemm2_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, int,
+                                const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*, int64_t, float,
+                                float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_path;
 extern int g_gemm_pair;
 extern int g_gemm_ts;
@@ -135,6 +138,18 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
   return check(hb::launch_gemm_tf32x3(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                       ws_floats, S(stream)),
                "hb_gemm_f32");
+}
+
+int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1_m, int64_t lda1_k, const float* B1,
+                 int64_t ldb1_k, int64_t ldb1_n, int32_t K2, const float* A2, int64_t lda2_m, int64_t lda2_k,
+                 const float* B2, int64_t ldb2_k, int64_t ldb2_n, float* C, int64_t ldc, float beta,
+                 float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream) {
+  if (M < 0 || N < 0 || K1 <= 0 || K2 <= 0 || ldc < N ||
+      (M > 0 && N > 0 && (!A1 || !B1 || !A2 || !B2 || !C)))
+    return fail(HB_EINVAL, "hb_gemm2_f32: bad arguments");
+  return check(hb::launch_gemm2_tf32x3(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2,
+                                       ldb2_k, ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, S(stream)),
+               "hb_gemm2_f32");
 }
 
 int hb_gemm_set_path(int32_t path) {

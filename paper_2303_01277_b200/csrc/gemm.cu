@@ -10,6 +10,7 @@
 // an mbarrier per stage; the epilogue reads TMEM with tcgen05.ld.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace hb {
@@ -311,6 +312,34 @@ cudaError_t launch_gemm_tf32x3(int M, int N, int K, const float* A, int64_t lda_
   if (N <= 128) return launch_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   // N > 128: 256-wide tiles over N
   return launch_bn<256>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+}
+
+cudaError_t launch_gemm_ts_dual(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, int,
+                                const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*, int64_t, float,
+                                float*, int64_t, float*, int64_t, cudaStream_t);
+
+// C = A1 B1 + A2 B2 (+ beta C): one pass of the A-in-TMEM kernel over both K
+// ranges when the operands allow (C written once, no read-back), otherwise
+// two accumulating GEMMs.
+cudaError_t launch_gemm2_tf32x3(int M, int N, int K1, const float* A1, int64_t lda1_m, int64_t lda1_k,
+                                const float* B1, int64_t ldb1_k, int64_t ldb1_n, int K2, const float* A2,
+                                int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,
+                                float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr, float* ws,
+                                int64_t ws_floats, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (K1 <= 0 || K2 <= 0) return cudaErrorInvalidValue;
+  static const bool no_dual = getenv("HB_GEMM_NO_DUAL") != nullptr;
+  if (!no_dual && g_gemm_path == 0 && !g_gemm_pair) {
+    const cudaError_t e = launch_gemm_ts_dual(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m,
+                                              lda2_k, B2, ldb2_k, ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats,
+                                              st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  cudaError_t e = launch_gemm_tf32x3(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, C, ldc, beta, nullptr, 0, ws,
+                                     ws_floats, st);
+  if (e != cudaSuccess) return e;
+  return launch_gemm_tf32x3(M, N, K2, A2, lda2_m, lda2_k, B2, ldb2_k, ldb2_n, C, ldc, 1.f, relu_out, ldr, ws,
+                            ws_floats, st);
 }
 
 }  // namespace hb

@@ -370,15 +370,17 @@ gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // B pre-split for the GEMMs whose B is a weight (Z = P W, T = m W^T): B is
 // small and shared by every tile, so it is split once into K-major hi / lo
 // arrays ([N][Kp], zero-padded) instead of in every CTA's converter warps.
-__global__ void bsplit_kernel(const float* __restrict__ B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp,
-                              float* __restrict__ hi, float* __restrict__ lo) {
-  const int64_t total = (int64_t)N * Kp;
+// hi/lo[n * Kp + koff + k] = tf32 split of B[k, n] for k < kcnt (zero for k >= K)
+__global__ void bsplit_kernel(const float* __restrict__ B, int64_t ldb_k, int64_t ldb_n, int K, int N, int kcnt,
+                              int Kp, int koff, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = (int64_t)N * kcnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int n = (int)(i / Kp), k = (int)(i - (int64_t)n * Kp);
+    const int n = (int)(i / kcnt), k = (int)(i - (int64_t)n * kcnt);
     const float x = k < K ? B[(int64_t)k * ldb_k + (int64_t)n * ldb_n] : 0.f;
     const uint32_t h = rna_tf32(x);
-    hi[i] = __uint_as_float(h);
-    lo[i] = __uint_as_float(rna_tf32(x - __uint_as_float(h)));
+    const int64_t o = (int64_t)n * Kp + koff + k;
+    hi[o] = __uint_as_float(h);
+    lo[o] = __uint_as_float(rna_tf32(x - __uint_as_float(h)));
   }
 }
 
@@ -474,7 +476,7 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
     float* lo = ws + (int64_t)N * Kp;
     int g = (int)(((int64_t)N * Kp + 255) / 256);
     if (g > sms * 4) g = sms * 4;
-    bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, Kp, hi, lo);
+    bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, Kp, Kp, 0, hi, lo);
     if (make_map(&tb, hi, K, N, Kp, BN, false) && make_map(&tbl, lo, K, N, Kp, BN, false)) {
       p.bsplit = 1;
       p.b_mn = 0;
@@ -512,13 +514,19 @@ bool gemm_make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t out
                    bool mn_major) {
   return gt::make_map(m, base, inner, outer, ld, box_outer, mn_major);
 }
-cudaError_t gemm_bsplit(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp, float* hi, float* lo,
-                        cudaStream_t st) {
-  int g = (int)(((int64_t)N * Kp + 255) / 256);
+cudaError_t gemm_bsplit_range(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int kcnt, int Kp, int koff,
+                              float* hi, float* lo, cudaStream_t st) {
+  int g = (int)(((int64_t)N * kcnt + 255) / 256);
   if (g > num_sms() * 4) g = num_sms() * 4;
-  gt::bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, Kp, hi, lo);
+  if (g < 1) g = 1;
+  gt::bsplit_kernel<<<g, 256, 0, st>>>(B, ldb_k, ldb_n, K, N, kcnt, Kp, koff, hi, lo);
   return cudaGetLastError();
 }
+cudaError_t gemm_bsplit(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp, float* hi, float* lo,
+                        cudaStream_t st) {
+  return gemm_bsplit_range(B, ldb_k, ldb_n, K, N, Kp, Kp, 0, hi, lo, st);
+}
+bool gemm_tma_ok(const float* base, int64_t s_mn, int64_t s_k) { return gt::tma_ok(base, s_mn, s_k); }
 cudaError_t gemm_splitk_reduce(const float* ws, int splits, int M, int N, float* C, int64_t ldc, float beta,
                                float* relu_out, int64_t ldr, cudaStream_t st) {
   int g = (int)(((int64_t)M * N + 255) / 256);

@@ -36,7 +36,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = A_BYTES + 2 * B_BYTES;     // raw A | B hi | B lo
   static constexpr int STAGES = BN == 128 ? 4 : 6;
-  static constexpr int SMEM = STAGES * STAGE + 1024;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;          // 4 epilogue warps x 2 staging chunks (32 rows x 128 B)
+  static constexpr int SMEM = STAGES * STAGE + EPI_BYTES + 1024;
   static constexpr uint32_t ACC_COLS = 2 * BN;
   static constexpr uint32_t TMEM_COLS = 512;
   static_assert(ACC_COLS + STAGES * 64 <= TMEM_COLS, "TMEM budget");
@@ -47,6 +48,8 @@ struct Params {
   int a_mn, b_mn;
   int bsplit;
   int mt, nt, splits, kb_per_split, nkb;
+  int nkb1;          // K blocks read from A1/B1; blocks nkb1.. come from A2/B2 (dual GEMM)
+  int tma_store;     // epilogue writes C (and the ReLU copy) through TMA bulk stores
   float* C;
   int64_t ldc;
   float beta;
@@ -70,6 +73,31 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// One warp's 32 rows x 32 fp32 chunk -> SW128 staging (row = lane, 16-byte
+// chunk c at c ^ (row & 7): conflict-free) -> TMA bulk store at (col, row0).
+// The staging buffer is reused two stores later, so wait for <= 1 pending read.
+__device__ __forceinline__ void stage_and_store(uint8_t* buf, const float (&v)[32], const CUtensorMap* map, int col,
+                                                int row0, int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+  uint4* row = reinterpret_cast<uint4*>(buf + lane * 128);
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    row[c ^ (lane & 7)] = make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+                                     __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) tma_store_2d(map, buf, col, row0);
 }
 
 __device__ __forceinline__ uint64_t sw_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -114,7 +142,9 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mi, int
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmBl, Params p) {
+               const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmA2,
+               const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+               const __grid_constant__ CUtensorMap tmR, Params p) {
   using C_ = Cfg<BN>;
   constexpr int S = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -162,21 +192,25 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           uint8_t* a_raw = st;
           uint8_t* b_hi = st + C_::A_BYTES;
           mbar_expect_tx(&full[s], C_::A_BYTES + (p.bsplit ? 2 : 1) * C_::B_BYTES);
-          const int k0 = kb * BK;
+          const bool second = kb >= p.nkb1;               // dual GEMM: A2/B2 blocks follow A1/B1
+          const CUtensorMap* ma = second ? &tmA2 : &tmA;
+          const CUtensorMap* mb = second ? &tmB2 : &tmB;
+          const int k0 = (second ? kb - p.nkb1 : kb) * BK;
           if (p.a_mn) {
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) tma_2d(a_raw + j * 4096, &tmA, mi * BM + 32 * j, k0, &full[s]);
+            for (int j = 0; j < BM / 32; ++j) tma_2d(a_raw + j * 4096, ma, mi * BM + 32 * j, k0, &full[s]);
           } else {
-            tma_2d(a_raw, &tmA, k0, mi * BM, &full[s]);
+            tma_2d(a_raw, ma, k0, mi * BM, &full[s]);
           }
           if (p.bsplit) {
-            tma_2d(b_hi, &tmB, k0, ni * BN, &full[s]);
-            tma_2d(b_hi + C_::B_BYTES, &tmBl, k0, ni * BN, &full[s]);
+            // pre-split workspace: A1 blocks at K kb*BK, A2 blocks right after nkb1*BK
+            tma_2d(b_hi, &tmB, kb * BK, ni * BN, &full[s]);
+            tma_2d(b_hi + C_::B_BYTES, &tmBl, kb * BK, ni * BN, &full[s]);
           } else if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) tma_2d(b_hi + j * 4096, &tmB, ni * BN + 32 * j, k0, &full[s]);
+            for (int j = 0; j < BN / 32; ++j) tma_2d(b_hi + j * 4096, mb, ni * BN + 32 * j, k0, &full[s]);
           } else {
-            tma_2d(b_hi, &tmB, k0, ni * BN, &full[s]);
+            tma_2d(b_hi, mb, k0, ni * BN, &full[s]);
           }
         }
       }
@@ -286,8 +320,15 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else {
-    // ---------------- epilogue (as gemm_tma.cu) ----------------
+    // ---------------- epilogue ----------------
+    // TMEM -> registers (tcgen05.ld, 32 columns per step); the accumulator is
+    // released to the MMA warp right after the tile's last load.  With
+    // tma_store the chunk goes through a swizzled smem buffer and a TMA bulk
+    // store (coalesced full-line writes, clipped at M / N by the tensor map);
+    // otherwise (beta != 0, split-K workspace, unaligned C) per-row stores.
     const int lg = warp & 3;
+    uint8_t* stg = smem + S * C_::STAGE + (warp - kEpi0) * (2 * 4096);
+    int sb = 0;
     int tc = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
       int mi, ni, si;
@@ -295,7 +336,8 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int acc = tc & 1;
       mbar_wait(&tfull[acc], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int row = mi * BM + lg * 32 + lane;
+      const int row0 = mi * BM + lg * 32;
+      const int row = row0 + lane;
       const int n0 = ni * BN;
       const int ncols = min(BN, p.N - n0);
       const bool split = p.splits > 1;
@@ -314,20 +356,36 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               "=r"(rr[28]), "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
             : "r"(taddr)
             : "memory");
+        if (c0 + 32 >= ncols) {
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&tempty[acc]);
+        }
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]);
+        if (p.tma_store) {
+          stage_and_store(stg + sb * 4096, v, &tmC, n0 + c0, row0, lane);
+          sb ^= 1;
+          if (p.relu_out) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = (v[e] > 0.f || v[e] != v[e]) ? v[e] : 0.f;
+            stage_and_store(stg + sb * 4096, v, &tmR, n0 + c0, row0, lane);
+            sb ^= 1;
+          }
+          continue;
+        }
         if (row < p.M) {
           const int nb = n0 + c0;
           const int nv = min(32, p.N - nb);
           if (split) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (e < nv) crow[nb + e] = __uint_as_float(rr[e]);
+              if (e < nv) crow[nb + e] = v[e];
           } else {
             float* rrow = p.relu_out ? p.relu_out + (int64_t)row * p.ldr + nb : nullptr;
             const bool cvec = ((p.ldc & 3) == 0) && ((((uintptr_t)(crow + nb)) & 15) == 0);
             const bool rvec = rrow && ((p.ldr & 3) == 0) && ((((uintptr_t)rrow) & 15) == 0);
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]);
             if (p.beta != 0.f) {
               float o[32];
 #pragma unroll
@@ -370,10 +428,9 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_local(&tempty[acc]);
     }
+    if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -388,30 +445,45 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
 bool gemm_make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld, int box_outer,
                    bool mn_major);
-cudaError_t gemm_bsplit(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int Kp, float* hi, float* lo,
-                        cudaStream_t st);
+bool gemm_tma_ok(const float* base, int64_t s_mn, int64_t s_k);
+cudaError_t gemm_bsplit_range(const float* B, int64_t ldb_k, int64_t ldb_n, int K, int N, int kcnt, int Kp, int koff,
+                              float* hi, float* lo, cudaStream_t st);
 cudaError_t gemm_splitk_reduce(const float* ws, int splits, int M, int N, float* C, int64_t ldc, float beta,
                                float* relu_out, int64_t ldr, cudaStream_t st);
 
+// C = A1 B1 (+ A2 B2) (+ beta C), optional ReLU copy.  K2 == 0: single GEMM.
+// A operands are (M x K) with element (m, k) at A + m*lda_m + k*lda_k, B
+// operands (K x N) at B + k*ldb_k + n*ldb_n; the two A (and the two raw B)
+// operands must share their major order.
 template <int BN>
-static cudaError_t launch_ts_bn(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
-                                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
-                                int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
+static cudaError_t launch_ts_bn(int M, int N, int K1, const float* A1, int64_t lda1_m, int64_t lda1_k,
+                                const float* B1, int64_t ldb1_k, int64_t ldb1_n, int K2, const float* A2,
+                                int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,
+                                float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr, float* ws,
+                                int64_t ws_floats, cudaStream_t st) {
   using C_ = gts::Cfg<BN>;
+  const bool dual = K2 > 0;
   gts::Params p{};
-  p.M = M; p.N = N; p.K = K;
-  p.a_mn = lda_k == 1 ? 0 : 1;
-  p.b_mn = ldb_k == 1 ? 0 : 1;
-  CUtensorMap ta, tb, tbl;
-  bool ok = p.a_mn ? gemm_make_map(&ta, A, M, K, lda_k, 32, true) : gemm_make_map(&ta, A, K, M, lda_m, gts::BM, false);
+  p.M = M; p.N = N; p.K = K1 + K2;
+  p.a_mn = lda1_k == 1 ? 0 : 1;
+  p.b_mn = ldb1_k == 1 ? 0 : 1;
+  if (dual && ((lda2_k == 1 ? 0 : 1) != p.a_mn)) return cudaErrorNotSupported;
+  CUtensorMap ta, tb, tbl, ta2, tb2, tc, tr;
+  bool ok = p.a_mn ? gemm_make_map(&ta, A1, M, K1, lda1_k, 32, true) : gemm_make_map(&ta, A1, K1, M, lda1_m, gts::BM, false);
+  if (dual)
+    ok = ok && (p.a_mn ? gemm_make_map(&ta2, A2, M, K2, lda2_k, 32, true)
+                       : gemm_make_map(&ta2, A2, K2, M, lda2_m, gts::BM, false));
+  else
+    ta2 = ta;
   if (!ok) return cudaErrorNotSupported;
   p.mt = (M + gts::BM - 1) / gts::BM;
   p.nt = (N + BN - 1) / BN;
-  p.nkb = (K + gts::BK - 1) / gts::BK;
+  p.nkb1 = (K1 + gts::BK - 1) / gts::BK;
+  p.nkb = p.nkb1 + (K2 + gts::BK - 1) / gts::BK;
   const int sms = num_sms();
   int splits = 1;
   const int tiles = p.mt * p.nt;
-  if (ws != nullptr && tiles < sms && p.nkb >= 8) {
+  if (!dual && ws != nullptr && tiles < sms && p.nkb >= 8) {
     splits = sms / tiles;
     if (splits > p.nkb / 4) splits = p.nkb / 4;
     const int64_t by_ws = ws_floats / ((int64_t)M * N);
@@ -422,23 +494,43 @@ static cudaError_t launch_ts_bn(int M, int N, int K, const float* A, int64_t lda
   p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
   p.C = C; p.ldc = ldc; p.beta = beta; p.relu_out = p.splits > 1 ? nullptr : relu_out; p.ldr = ldr;
   p.ws = p.splits > 1 ? ws : nullptr;
-  const int Kp = (K + 3) & ~3;
+  // B pre-split once into the workspace (hi | lo, K-major, row stride Kp);
+  // a dual GEMM's B2 rows start at K block nkb1
+  const int kb2 = p.nkb1 * gts::BK;
+  const int Kext = dual ? kb2 + K2 : K1;
+  const int Kp = (Kext + 3) & ~3;
   static const bool no_bsplit = getenv("HB_GEMM_NO_BSPLIT") != nullptr;
-  if (!no_bsplit && p.splits == 1 && ws != nullptr && tiles >= 2 * sms && p.nkb >= 4 &&
-      (int64_t)N * K <= (1 << 20) && 2 * (int64_t)N * Kp <= ws_floats) {
+  const bool want_split = !no_bsplit && p.splits == 1 && ws != nullptr && (tiles >= 2 * sms || dual) &&
+                          (p.nkb >= 4 || dual) && (int64_t)N * Kp <= (1 << 20) && 2 * (int64_t)N * Kp <= ws_floats;
+  if (want_split) {
     float* hi = ws;
     float* lo = ws + (int64_t)N * Kp;
-    cudaError_t e = gemm_bsplit(B, ldb_k, ldb_n, K, N, Kp, hi, lo, st);
+    cudaError_t e = gemm_bsplit_range(B1, ldb1_k, ldb1_n, K1, N, dual ? kb2 : Kp, Kp, 0, hi, lo, st);
+    if (e == cudaSuccess && dual) e = gemm_bsplit_range(B2, ldb2_k, ldb2_n, K2, N, Kp - kb2, Kp, kb2, hi, lo, st);
     if (e != cudaSuccess) return e;
-    if (!gemm_make_map(&tb, hi, K, N, Kp, BN, false) || !gemm_make_map(&tbl, lo, K, N, Kp, BN, false))
+    if (!gemm_make_map(&tb, hi, Kext, N, Kp, BN, false) || !gemm_make_map(&tbl, lo, Kext, N, Kp, BN, false))
       return cudaErrorNotSupported;
     p.bsplit = 1;
     p.b_mn = 0;
+    tb2 = tb;
   } else {
-    ok = p.b_mn ? gemm_make_map(&tb, B, N, K, ldb_k, 32, true) : gemm_make_map(&tb, B, K, N, ldb_n, BN, false);
+    if (dual && (ldb2_k == 1 ? 0 : 1) != p.b_mn) return cudaErrorNotSupported;
+    ok = p.b_mn ? gemm_make_map(&tb, B1, N, K1, ldb1_k, 32, true) : gemm_make_map(&tb, B1, K1, N, ldb1_n, BN, false);
+    if (dual)
+      ok = ok && (p.b_mn ? gemm_make_map(&tb2, B2, N, K2, ldb2_k, 32, true)
+                         : gemm_make_map(&tb2, B2, K2, N, ldb2_n, BN, false));
+    else
+      tb2 = tb;
     if (!ok) return cudaErrorNotSupported;
     tbl = tb;
   }
+  // TMA-store epilogue: plain overwrite of a TMA-describable C (and ReLU copy)
+  static const bool no_tma_store = getenv("HB_GEMM_NO_TMA_STORE") != nullptr;
+  p.tma_store = !no_tma_store && beta == 0.f && p.splits == 1 && gemm_tma_ok(C, ldc, 1) &&
+                (!p.relu_out || gemm_tma_ok(p.relu_out, ldr, 1)) && gemm_make_map(&tc, C, N, M, ldc, 32, false) &&
+                (!p.relu_out || gemm_make_map(&tr, p.relu_out, N, M, ldr, 32, false));
+  if (!p.tma_store) tc = tr = ta;
+  else if (!p.relu_out) tr = tc;
   const int total = tiles * p.splits;
   const int grid = total < sms ? total : sms;
   static bool attr_set = false;
@@ -448,7 +540,7 @@ static cudaError_t launch_ts_bn(int M, int N, int K, const float* A, int64_t lda
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  gts::gemm_ts_kernel<BN><<<grid, gts::kThreads, C_::SMEM, st>>>(ta, tb, tbl, p);
+  gts::gemm_ts_kernel<BN><<<grid, gts::kThreads, C_::SMEM, st>>>(ta, tb, tbl, ta2, tb2, tc, tr, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (p.splits > 1) e = gemm_splitk_reduce(ws, p.splits, M, N, C, ldc, beta, relu_out, ldr, st);
@@ -459,8 +551,27 @@ cudaError_t launch_gemm_ts(int M, int N, int K, const float* A, int64_t lda_m, i
                            int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr,
                            float* ws, int64_t ws_floats, cudaStream_t st) {
   if (N <= 64)
-    return launch_ts_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
-  return launch_ts_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+    return launch_ts_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, 0, nullptr, 0, 0, nullptr, 0, 0, C, ldc, beta,
+                            relu_out, ldr, ws, ws_floats, st);
+  return launch_ts_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, 0, nullptr, 0, 0, nullptr, 0, 0, C, ldc, beta,
+                           relu_out, ldr, ws, ws_floats, st);
+}
+
+// Dual GEMM on the A-in-TMEM kernel; cudaErrorNotSupported when an operand is
+// not TMA-describable or the majors differ (the caller then runs two GEMMs).
+cudaError_t launch_gemm_ts_dual(int M, int N, int K1, const float* A1, int64_t lda1_m, int64_t lda1_k,
+                                const float* B1, int64_t ldb1_k, int64_t ldb1_n, int K2, const float* A2,
+                                int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,
+                                float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr, float* ws,
+                                int64_t ws_floats, cudaStream_t st) {
+  if (!gemm_tma_ok(A1, lda1_m, lda1_k) || !gemm_tma_ok(A2, lda2_m, lda2_k) || !gemm_tma_ok(B1, ldb1_n, ldb1_k) ||
+      !gemm_tma_ok(B2, ldb2_n, ldb2_k))
+    return cudaErrorNotSupported;
+  if (N <= 64)
+    return launch_ts_bn<64>(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2, ldb2_k,
+                            ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+  return launch_ts_bn<128>(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2, ldb2_k,
+                           ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
 }
 
 }  // namespace hb

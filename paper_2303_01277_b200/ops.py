@@ -142,6 +142,22 @@ def gemm(A, B, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
     return C
 
 
+def gemm2(A1, B1, A2, B2, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
+    """C = A1 @ B1 + A2 @ B2 (+ beta C) in one tcgen05 pass where the operands
+    allow: the SAGE combine [h | A h] [W_top; W_bot] without the concatenation
+    (trainer.py:294,318-321).  Returns C."""
+    M, K1 = A1.shape
+    M2, K2 = A2.shape
+    assert M == M2 and B1.shape[0] == K1 and B2.shape[0] == K2 and B1.shape[1] == B2.shape[1]
+    N = B1.shape[1]
+    assert C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
+    _lib.call("hb_gemm2_f32", M, N, K1, ptr(A1), A1.stride(0), A1.stride(1), ptr(B1), B1.stride(0), B1.stride(1),
+              K2, ptr(A2), A2.stride(0), A2.stride(1), ptr(B2), B2.stride(0), B2.stride(1), ptr(C), C.stride(0),
+              float(beta), ptr(relu_out), relu_out.stride(0) if relu_out is not None else 0, ptr(ws),
+              ws.numel() if ws is not None else 0, stream_handle(stream))
+    return C
+
+
 def gemm_set_path(path: int):
     """0: TMA warp-specialised tcgen05 kernel where operands allow; 1: SIMT-staged kernel;
     2: as 0 with CTA pairs (cta_group::2) for 128 < N <= 256."""

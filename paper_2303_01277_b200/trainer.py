@@ -439,6 +439,21 @@ class DeviceRank:
                 ops.gemm(a, b, out, beta=1.0 if accumulate else 0.0, relu_out=relu_out, ws=self.gemm_ws)
                 self.launches += 1
 
+    def _mm2(self, a1, b1, a2, b2, out, relu_out=None):
+        """out = a1 @ b1 + a2 @ b2: the SAGE combine over [h | A h] (trainer.py:294,318-321)
+        in one GEMM pass, without materialising the concatenation."""
+        nl, nc = out.shape
+        with self.timer("gemm", 0, 2 * a1.shape[0] * (a1.shape[1] + a2.shape[1]) * b1.shape[1]):
+            if self.gemm_impl == "cublas":
+                self.torch.mm(a1, b1, out=out)
+                out.addmm_(a2, b2)
+                if relu_out is not None:
+                    ops.relu(out, relu_out, nl, nc)
+                    self.launches += 1
+            else:
+                ops.gemm2(a1, b1, a2, b2, out, relu_out=relu_out, ws=self.gemm_ws)
+                self.launches += 1
+
     def _tiled(self, a):
         """Tiled (TMA-staged) layout of `a`, built on first use; None when too
         little of the matrix falls into dense tiles to pay off."""
@@ -476,16 +491,14 @@ class DeviceRank:
         if not self.post[l]:
             self._spmm(self.A, Hd, agg, d)
             if sage:
-                self._mm(Hd[:NL, :d], Wtop, Z)
-                self._mm(agg[:, :d], Wbot, Z, accumulate=True, relu_out=hout)
+                self._mm2(Hd[:NL, :d], Wtop, agg[:, :d], Wbot, Z, relu_out=hout)
             else:
                 self._mm(agg[:, :d], Wbot, Z, relu_out=hout)
             return
         Y = self.Y[l]
         self._mm(Hd[:, :d], Wbot, Y[:, :dout])
         if sage:
-            self._spmm(self.A, Y, agg, dout)
-            Z.copy_(agg[:, :dout])
+            self._spmm(self.A, Y, Z, dout)           # aggregate straight into z, then z += h~ W_top
             self._mm(Hd[:NL, :d], Wtop, Z, accumulate=True, relu_out=hout)
         else:
             self._spmm(self.A, Y, agg, dout)
@@ -521,6 +534,12 @@ class DeviceRank:
             self._spmm(self.At, m, S, dout)
             self._mm(Hd[:, :d].t(), S[:, :dout], Gbot)
             if JF is None:
+                return
+            if sage:
+                # local rows: j = S W_bot^T + m W_top^T in one pass; halo rows: S W_bot^T
+                self._mm2(S[:NL, :dout], Wbot.t(), m, Wtop.t(), JF[:NL, :d])
+                if JF.shape[0] > NL:
+                    self._mm(S[NL:, :dout], Wbot.t(), JF[NL:, :d])
                 return
             self._mm(S[:, :dout], Wbot.t(), JF[:, :d])
         if sage:

@@ -149,3 +149,54 @@ def test_gemm_presplit_weight_operand(N, K, kind, gemm_path):
     ops.gemm(A, B, C, beta=1.0, relu_out=H[:, :N], ws=ws)
     _check(A, B, C, beta=1.0, C0=C0)
     assert torch.equal(H[:, :N], torch.clamp(C, min=0))
+
+
+@pytest.mark.parametrize("M,N,K", [(40000, 128, 100), (40001, 41, 256), (37900, 256, 602), (38000, 94, 128)])
+@pytest.mark.parametrize("ws_on", [True, False])
+def test_tall_gemm_tma_store_epilogue(M, N, K, ws_on):
+    """Tall GEMMs (>= 148 output tiles) run the A-in-TMEM kernel whose epilogue
+    stages through shared memory and TMA bulk-stores C and the ReLU copy."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K + 4, device="cuda", generator=g)[:, :K]
+    B = torch.randn(K, N, device="cuda", generator=g)
+    ldc = (N + 3) // 4 * 4
+    C = torch.full((M, ldc), 7.0, device="cuda")[:, :N]
+    H = torch.full((M, ldc + 4), 7.0, device="cuda")
+    ws = torch.empty(4 << 20, device="cuda") if ws_on else None
+    ops.gemm(A, B, C, relu_out=H[:, :N], ws=ws)
+    _check(A, B, C)
+    assert torch.equal(H[:, :N], torch.clamp(C, min=0))
+    assert bool((H[:, N:] == 7.0).all())                      # nothing written past N
+    if ldc > N:
+        full = C.as_strided((M, ldc), (ldc, 1))
+        assert bool((full[:, N:] == 7.0).all())
+
+
+@pytest.mark.parametrize("M", [40000, 40001, 700])
+@pytest.mark.parametrize("ws_on", [True, False])
+def test_gemm2_dual(M, ws_on):
+    """C = A1 B1 + A2 B2 (the SAGE combine and its input gradient) in one pass,
+    K1 not a multiple of the 32-wide K block, B operands as transposed views."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M)
+    d, dout = 100, 128
+    H = torch.randn(M, 104, device="cuda", generator=g)[:, :d]
+    AGG = torch.randn(M, 104, device="cuda", generator=g)[:, :d]
+    W = torch.randn(2 * d, dout, device="cuda", generator=g)
+    ws = torch.empty(4 << 20, device="cuda") if ws_on else None
+    Z = torch.empty(M, dout, device="cuda")
+    R = torch.empty(M, dout + 4, device="cuda")
+    ops.gemm2(H, W[:d], AGG, W[d:], Z, relu_out=R[:, :dout], ws=ws)
+    _check(torch.cat([H, AGG], 1), W, Z)
+    assert torch.equal(R[:, :dout], torch.clamp(Z, min=0))
+    # input gradient: j = S W_bot^T + m W_top^T
+    S = torch.randn(M, dout, device="cuda", generator=g)
+    m = torch.randn(M, dout, device="cuda", generator=g)
+    J = torch.empty(M, 104, device="cuda")[:, :d]
+    ops.gemm2(S, W[d:].t(), m, W[:d].t(), J, ws=ws)
+    _check(torch.cat([S, m], 1), torch.cat([W[d:].t(), W[:d].t()], 0), J)
+    # beta accumulate
+    J0 = J.clone()
+    ops.gemm2(S, W[d:].t(), m, W[:d].t(), J, beta=1.0, ws=ws)
+    _check(torch.cat([S, m], 1), torch.cat([W[d:].t(), W[:d].t()], 0), J, beta=1.0, C0=J0)

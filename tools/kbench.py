@@ -125,10 +125,27 @@ def gemm(args):
              ("Z=P W   (l3 half)", NL, 41, 256, "nn"), ("G=P^T m (l1 half)", 602, 256, NL, "tn"),
              ("G=P^T m (l3 half)", 256, 41, NL, "tn"), ("T=m W^T (l2)", NL, 256, 256, "nt"),
              ("T=m W^T (l3)", NL, 256, 41, "nt")]
+    if args.config == "ogbn":
+        NL = 2_449_029
+        cases = [("Z=P W   (l1 half)", NL, 128, 100, "nn"), ("Z=P W   (l2 half)", NL, 128, 128, "nn"),
+                 ("Y=H W   (l3 bot)", NL, 47, 128, "nn"), ("G=P^T m (l2 half)", 128, 128, NL, "tn"),
+                 ("T=m W^T (l2)", NL, 128, 128, "nt"), ("dual Z=[H|AH] W (l1)", NL, 128, 100, "dual"),
+                 ("dual Z=[H|AH] W (l2)", NL, 128, 128, "dual"), ("dual j=[S|m] W^T (l3)", NL, 128, 47, "dualt")]
     ws = torch.empty(64 * 602 * 256, device="cuda")
     def mat(r, c):   # row-major with a 16-byte row stride, like the trainer's buffers
         return torch.randn(r, (c + 3) // 4 * 4, device="cuda", generator=g)[:, :c]
     for name, M, N, K, kind in cases:
+        if kind.startswith("dual"):
+            A1, A2 = mat(M, K), mat(M, K)
+            W = mat(2 * K, N) if kind == "dual" else mat(N, 2 * K)
+            B1, B2 = (W[:K], W[K:]) if kind == "dual" else (W[:, :K].t(), W[:, K:].t())
+            C = torch.empty(M, N, device="cuda")
+            ms = _time(lambda: ops.gemm2(A1, B1, A2, B2, C, ws=ws), reps=5)
+            ms2 = _time(lambda: (ops.gemm(A1, B1, C, ws=ws), ops.gemm(A2, B2, C, beta=1.0, ws=ws)), reps=5)
+            print(json.dumps({"gemm": name, "M": M, "N": N, "K": 2 * K, "dual_ms": round(ms, 4),
+                              "two_pass_ms": round(ms2, 4),
+                              "dual_hbm_gbps": round(4 * M * (2 * K + N) / ms / 1e6, 1)}), flush=True)
+            continue
         if kind == "nn":
             A, B = mat(M, K), mat(K, N)
         elif kind == "tn":
@@ -142,6 +159,11 @@ def gemm(args):
         ops.gemm_set_path(0)
         ms_cb = _time(lambda: torch.mm(A, B, out=C), reps=5)
         fl = 2.0 * M * N * K
+        if args.config == "ogbn":
+            print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_ms": round(ms, 4),
+                              "hbm_gbps": round(4 * (M * K + M * N + K * N) / ms / 1e6, 1),
+                              "cublas_fp32_ms": round(ms_cb, 4)}), flush=True)
+            continue
         print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_tma_ms": round(ms, 4),
                           "tcgen05_simt_staged_ms": round(ms_v1, 4), "cublas_fp32_ms": round(ms_cb, 4),
                           "tcgen05_tflops": round(fl / ms / 1e9, 1), "cublas_tflops": round(fl / ms_cb / 1e9, 1)}),
