@@ -500,8 +500,10 @@ static cudaError_t launch_ts_bn(int M, int N, int K1, const float* A1, int64_t l
   const int Kext = dual ? kb2 + K2 : K1;
   const int Kp = (Kext + 3) & ~3;
   static const bool no_bsplit = getenv("HB_GEMM_NO_BSPLIT") != nullptr;
-  const bool want_split = !no_bsplit && p.splits == 1 && ws != nullptr && (tiles >= 2 * sms || dual) &&
-                          (p.nkb >= 4 || dual) && (int64_t)N * Kp <= (1 << 20) && 2 * (int64_t)N * Kp <= ws_floats;
+  const bool b_tma = gemm_tma_ok(B1, ldb1_n, ldb1_k) && (!dual || gemm_tma_ok(B2, ldb2_n, ldb2_k));
+  const bool want_split = p.splits == 1 && ws != nullptr && (int64_t)N * Kp <= (1 << 20) &&
+                          2 * (int64_t)N * Kp <= ws_floats &&
+                          (!b_tma || (!no_bsplit && (tiles >= 2 * sms || dual) && (p.nkb >= 4 || dual)));
   if (want_split) {
     float* hi = ws;
     float* lo = ws + (int64_t)N * Kp;
@@ -564,9 +566,9 @@ cudaError_t launch_gemm_ts_dual(int M, int N, int K1, const float* A1, int64_t l
                                 int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,
                                 float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr, float* ws,
                                 int64_t ws_floats, cudaStream_t st) {
-  if (!gemm_tma_ok(A1, lda1_m, lda1_k) || !gemm_tma_ok(A2, lda2_m, lda2_k) || !gemm_tma_ok(B1, ldb1_n, ldb1_k) ||
-      !gemm_tma_ok(B2, ldb2_n, ldb2_k))
-    return cudaErrorNotSupported;
+  // B operands need not be TMA-describable: the dual path pre-splits them
+  // into the workspace whenever it is large enough
+  if (!gemm_tma_ok(A1, lda1_m, lda1_k) || !gemm_tma_ok(A2, lda2_m, lda2_k)) return cudaErrorNotSupported;
   if (N <= 64)
     return launch_ts_bn<64>(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2, ldb2_k,
                             ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);

@@ -130,16 +130,20 @@ def gemm(args):
         cases = [("Z=P W   (l1 half)", NL, 128, 100, "nn"), ("Z=P W   (l2 half)", NL, 128, 128, "nn"),
                  ("Y=H W   (l3 bot)", NL, 47, 128, "nn"), ("G=P^T m (l2 half)", 128, 128, NL, "tn"),
                  ("T=m W^T (l2)", NL, 128, 128, "nt"), ("dual Z=[H|AH] W (l1)", NL, 128, 100, "dual"),
-                 ("dual Z=[H|AH] W (l2)", NL, 128, 128, "dual"), ("dual j=[S|m] W^T (l3)", NL, 128, 47, "dualt")]
+                 ("dual Z=[H|AH] W (l2)", NL, 128, 128, "dual"), ("dual j=[S|m] W^T (l3)", NL, 128, 47, "dualt"), ("dual j=[S|m] W^T (l2)", NL, 128, 128, "dualt")]
     ws = torch.empty(64 * 602 * 256, device="cuda")
     def mat(r, c):   # row-major with a 16-byte row stride, like the trainer's buffers
         return torch.randn(r, (c + 3) // 4 * 4, device="cuda", generator=g)[:, :c]
     for name, M, N, K, kind in cases:
         if kind.startswith("dual"):
             A1, A2 = mat(M, K), mat(M, K)
-            W = mat(2 * K, N) if kind == "dual" else mat(N, 2 * K)
-            B1, B2 = (W[:K], W[K:]) if kind == "dual" else (W[:, :K].t(), W[:, K:].t())
-            C = torch.empty(M, N, device="cuda")
+            if kind == "dual":
+                W = mat(2 * K, N)
+                B1, B2 = W[:K], W[K:]
+            else:   # the trainer's W_bot^T / W_top^T views of one padded (2K x N) weight
+                W = mat(2 * N, K)
+                B1, B2 = W[N:].t(), W[:N].t()
+            C = mat(M, N)
             ms = _time(lambda: ops.gemm2(A1, B1, A2, B2, C, ws=ws), reps=5)
             ms2 = _time(lambda: (ops.gemm(A1, B1, C, ws=ws), ops.gemm(A2, B2, C, beta=1.0, ws=ws)), reps=5)
             print(json.dumps({"gemm": name, "M": M, "N": N, "K": 2 * K, "dual_ms": round(ms, 4),
@@ -152,7 +156,7 @@ def gemm(args):
             A, B = mat(K, M).t(), mat(K, N)
         else:
             A, B = mat(M, K), mat(N, K).t()
-        C = torch.empty(M, N, device="cuda")
+        C = mat(M, N)
         ms = _time(lambda: ops.gemm(A, B, C, ws=ws), reps=5)
         ops.gemm_set_path(1)
         ms_v1 = _time(lambda: ops.gemm(A, B, C, ws=ws), reps=5)
