@@ -98,11 +98,14 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
 /* K3/K4 row-gather kernel with its knobs exposed: algo 0 = auto, 1 = row
  * gather (one warp, or an 8/16-lane group for d <= 64, per row, several
  * nonzeros in flight); window > 0 = nonzeros kept in flight per lane group
- * (tuning; 0 = default); nnz = stored entries (informational).  Same result
- * contract as hb_spmm_csr. */
+ * (tuning; 0 = default); nnz = stored entries (informational);
+ * stream_col: X rows >= stream_col (the halo copies) are referenced a few
+ * times each and are read L2-evict-first, like the CSR arrays and Y, so the
+ * local rows being aggregated stay L2-resident (INT32_MAX: no hint).  Same
+ * result contract as hb_spmm_csr. */
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
-                   int32_t window, void* stream);
+                   int32_t window, int32_t stream_col, void* stream);
 
 /* K3/K4 tiled path (same result contract as hb_spmm_csr, fp32 accumulation
  * in tile-then-residual order).  The matrix is pre-split (ops.TiledCsr, built

@@ -12,7 +12,7 @@ cudaError_t launch_dequant_gather(const hb_segment_t*, int, int, const int32_t*,
                                   const int32_t*, int, int, float*, int64_t, int, cudaStream_t);
 cudaError_t launch_philox_uniforms(uint64_t, uint64_t, uint64_t, int64_t, double*, cudaStream_t);
 cudaError_t launch_spmm(int, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
-                        float*, int64_t, int64_t, int, int, cudaStream_t);
+                        float*, int64_t, int64_t, int, int, int, cudaStream_t);
 cudaError_t launch_xent(const float*, int64_t, int, int, const int32_t*, const uint8_t*, double, float*,
                         int64_t, double*, double*, cudaStream_t);
 cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaStream_t);
@@ -102,16 +102,17 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)))
     return fail(HB_EINVAL, "hb_spmm_csr: bad arguments");
-  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, -1, 1, 0, S(stream)),
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, -1, 1, 0, INT32_MAX, S(stream)),
                "hb_spmm_csr");
 }
 
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
-                   int32_t window, void* stream) {
+                   int32_t window, int32_t stream_col, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)) || algo < 0 || algo > 1)
     return fail(HB_EINVAL, "hb_spmm_csr_ex: bad arguments");
-  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, nnz, algo, window, S(stream)),
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, nnz, algo, window, stream_col,
+                               S(stream)),
                "hb_spmm_csr_ex");
 }
 

@@ -10,11 +10,43 @@
 // 8(n+1) + 8 nnz + 4 nnz d + 4 n d.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
+#include <mutex>
+#include <vector>
 #include "common.cuh"
 
 namespace hb {
 
 constexpr int kSpWarps = 8;
+
+// L2 residency: the row-gather kernel's hit rate depends on the local X rows
+// of the community being aggregated staying in L2.  Everything read or written
+// once — CSR entries, Y, and the halo rows (columns >= stream_col: copies of
+// remote boundary nodes, each referenced by a handful of cut edges) — is
+// marked evict-first so it does not push those rows out.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_f4_hint(const float4* a, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_i32_hint(const int32_t* a, uint64_t pol) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_f32_hint(const float* a, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(a), "l"(pol));
+  return r;
+}
 
 // NV float4 per lane, G lanes per nonzero group (32/G groups share a warp and
 // walk interleaved nonzeros of the row), U nonzeros per group per step (loads
@@ -25,40 +57,79 @@ template <int NV, int G, int U>
 __global__ void __launch_bounds__(kSpWarps * 32)
 spmm_rows_vec_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                      const float* __restrict__ vals, const float* __restrict__ X, int64_t ldx, int d,
-                     float* __restrict__ Y, int64_t ldy) {
+                     float* __restrict__ Y, int64_t ldy, int stream_col, int hint, int* __restrict__ next_row,
+                     int chunk) {
   constexpr int NG = 32 / G;
+  const uint64_t pf = policy_evict_first();
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, gl = lane % G;
   const int warp_global = blockIdx.x * kSpWarps + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * kSpWarps;
-  for (int row = warp_global; row < nrows; row += nwarps) {
+  // Rows are handed out in ascending chunks from a global counter, so all
+  // warps stay within a narrow band of rows: the X rows of the community being
+  // aggregated stay L2-resident.  (A fixed grid-stride split lets warps drift
+  // apart by several communities over the launch and multiplies HBM reads.)
+  int r0 = 0, r1 = 0, row = warp_global;
+  for (;;) {
+    if (next_row) {
+      if (row >= r1) {
+        int got = 0;
+        if (lane == 0) got = atomicAdd(next_row, chunk);
+        r0 = __shfl_sync(0xffffffffu, got, 0);
+        if (r0 >= nrows) {
+          // the last warp out re-arms the counter for the next launch on this stream
+          if (lane == 0 && atomicAdd(next_row + 1, 1) == nwarps - 1) {
+            atomicExch(next_row, 0);
+            atomicExch(next_row + 1, 0);
+          }
+          break;
+        }
+        r1 = min(nrows, r0 + chunk);
+        row = r0;
+      }
+    } else if (row >= nrows) {
+      break;
+    }
     const int64_t start = row_ptr[row], end = row_ptr[row + 1];
     float4 acc[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t base = start; base < end; base += 32) {
       const int64_t k = base + lane;
-      const int my_c = k < end ? __ldg(col_idx + k) : 0;
-      const float my_v = k < end ? __ldg(vals + k) : 0.f;
+      int my_c = 0;
+      float my_v = 0.f;
+      if (k < end) {
+        if (hint) {
+          my_c = ld_i32_hint(col_idx + k, pf);
+          my_v = ld_f32_hint(vals + k, pf);
+        } else {
+          my_c = __ldg(col_idx + k);
+          my_v = __ldg(vals + k);
+        }
+      }
       const int n = (int)min((int64_t)32, end - base);
       for (int jj = 0; jj < n; jj += NG * U) {
         int c[U];
         float v[U];
+        bool live[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int j = jj + u * NG + grp;          // j < 32 always (jj < n <= 32, steps of NG*U | 32)
           c[u] = __shfl_sync(0xffffffffu, my_c, j & 31);
           v[u] = __shfl_sync(0xffffffffu, my_v, j & 31);
-          if (j >= n) v[u] = 0.f;                   // padding nonzero: row my_c of lane j (valid), weight 0
+          live[u] = j < n;                          // padding slots issue no load
         }
         float4 x[U][NV];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const float4* xr = reinterpret_cast<const float4*>(X + (int64_t)c[u] * ldx);
+          const bool once = hint && c[u] >= stream_col;
 #pragma unroll
           for (int q = 0; q < NV; ++q) {
             const int col = (q * G + gl) * 4;
-            x[u][q] = col < d ? __ldg(xr + q * G + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[u][q] = (col >= d || !live[u]) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                      : once ? ld_f4_hint(xr + q * G + gl, pf)
+                             : __ldg(xr + q * G + gl);
           }
         }
 #pragma unroll
@@ -85,7 +156,10 @@ spmm_rows_vec_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32
       for (int q = 0; q < NV; ++q) {
         const int col = (q * G + gl) * 4;
         if (col + 3 < d) {
-          *reinterpret_cast<float4*>(y + col) = acc[q];
+          if (hint)
+            __stcs(reinterpret_cast<float4*>(y + col), acc[q]);
+          else
+            *reinterpret_cast<float4*>(y + col) = acc[q];
         } else if (col < d) {
           y[col] = acc[q].x;
           if (col + 1 < d) y[col + 1] = acc[q].y;
@@ -93,6 +167,7 @@ spmm_rows_vec_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32
         }
       }
     }
+    row = next_row ? row + 1 : row + nwarps;
   }
 }
 
@@ -129,9 +204,27 @@ spmm_rows_scalar_kernel(int nrows, const int64_t* __restrict__ row_ptr, const in
 // algo: 0 auto, 1 row gather (the same kernel: the TMA-tiled path is a
 // separate entry point, hb_spmm_tiled).  `window` > 0 overrides the number of
 // nonzeros a lane group keeps in flight (tuning only).
+// Per-(device, stream) pair of ints {next row, warps finished}: launches on one
+// stream are ordered, and each launch leaves the pair at zero for the next.
+static int* row_counter(cudaStream_t st) {
+  struct Slot { int dev; cudaStream_t st; int* p; };
+  static std::mutex mu;
+  static std::vector<Slot> slots;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  for (const Slot& s : slots)
+    if (s.dev == dev && s.st == st) return s.p;
+  int* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+  slots.push_back({dev, st, p});
+  return p;
+}
+
 cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                         const float* X, int64_t ldx, int d, float* Y, int64_t ldy, int64_t nnz, int algo,
-                        int window, cudaStream_t st) {
+                        int window, int stream_col, cudaStream_t st) {
   (void)nnz;
   (void)algo;
   if (nrows <= 0 || d <= 0) return cudaSuccess;
@@ -140,13 +233,28 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
   const int grid = want < cap ? want : cap;
   const bool vec = (ldx % 4 == 0) && (ldy % 4 == 0) && ((((uintptr_t)X) & 15) == 0) &&
                    ((((uintptr_t)Y) & 15) == 0);
+  static const int hint = getenv("HB_SPMM_HINT") ? atoi(getenv("HB_SPMM_HINT")) : 0;
+  static const int dyn = getenv("HB_SPMM_DYN") ? atoi(getenv("HB_SPMM_DYN")) : 1;
+  static const int chunk_env = getenv("HB_SPMM_CHUNK") ? atoi(getenv("HB_SPMM_CHUNK")) : 0;
+  int* next_row = nullptr;
+  int chunk = 1;
+  if (dyn) {
+    next_row = row_counter(st);
+    if (!next_row) return cudaErrorMemoryAllocation;
+    // ~256 nonzeros per grab
+    const int64_t avg = nnz > 0 ? (nnz + nrows - 1) / nrows : 32;
+    chunk = chunk_env > 0 ? chunk_env : (int)std::max<int64_t>(1, std::min<int64_t>(32, 256 / std::max<int64_t>(1, avg)));
+  }
   if (vec && d <= 1024) {
     const int d4 = (d + 3) / 4;
-#define HB_S(NV, G, U) spmm_rows_vec_kernel<NV, G, U><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy)
+#define HB_S(NV, G, U) spmm_rows_vec_kernel<NV, G, U><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, stream_col, hint, next_row, chunk)
     if (d4 <= 8) HB_S(1, 8, 8);
     else if (d4 <= 16) {
-      if (window == 4) HB_S(1, 16, 4);
-      else if (window == 8) HB_S(1, 16, 8);
+      // short rows (few nonzeros per row): fewer loads in flight per group,
+      // more resident warps; long rows: 16 per group
+      const int w = window > 0 ? window : (nnz >= 0 && nnz < (int64_t)64 * nrows ? 4 : 16);
+      if (w == 4) HB_S(1, 16, 4);
+      else if (w == 8) HB_S(1, 16, 8);
       else HB_S(1, 16, 16);
     }
     else switch ((d4 + 31) / 32) {

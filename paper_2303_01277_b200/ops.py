@@ -120,11 +120,14 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
 SPMM_ALGOS = {"auto": 0, "rows": 1}
 
 
-def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "auto", window: int = 0):
-    """``linalg.spmm`` (linalg.py:71-75): out[:rows, :d] = A @ x[:, :d]."""
+def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "auto", window: int = 0,
+         stream_col: int | None = None):
+    """``linalg.spmm`` (linalg.py:71-75): out[:rows, :d] = A @ x[:, :d].
+    Columns >= stream_col (halo copies) are read L2-evict-first."""
     d = x.shape[1] if d is None else d
+    sc = 2**31 - 1 if stream_col is None else int(stream_col)
     _lib.call("hb_spmm_csr_ex", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
-              x.stride(0), d, ptr(out), out.stride(0), a.nnz, SPMM_ALGOS[algo], int(window),
+              x.stride(0), d, ptr(out), out.stride(0), a.nnz, SPMM_ALGOS[algo], int(window), sc,
               stream_handle(stream))
     return out
 

@@ -471,7 +471,7 @@ class DeviceRank:
             if t is not None:
                 ops.spmm_tiled(t, x, y, d)
             else:
-                ops.spmm(a, x, y, d)
+                ops.spmm(a, x, y, d, stream_col=self.NL if a is self.A else None)
         self.launches += 1
 
     def _layer_forward(self, l: int, Hd):

@@ -25,7 +25,7 @@ def _bound(rp, ci, v, x):
     return a @ np.abs(x.astype(np.float64))
 
 
-def _run(rp, ci, v, x, ncols, ld_pad=0, ld_out_pad=0, algo="auto", window=0):
+def _run(rp, ci, v, x, ncols, ld_pad=0, ld_out_pad=0, algo="auto", window=0, stream_col=None):
     from paper_2303_01277_b200 import ops
     rows, d = len(rp) - 1, x.shape[1]
     A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
@@ -33,7 +33,7 @@ def _run(rp, ci, v, x, ncols, ld_pad=0, ld_out_pad=0, algo="auto", window=0):
     X = torch.zeros(ncols, ldx, device="cuda")
     X[:, :d] = torch.from_numpy(x)
     Y = torch.full((rows, d + ld_out_pad), 7.0, device="cuda")
-    ops.spmm(A, X, Y, d, algo=algo, window=window)
+    ops.spmm(A, X, Y, d, algo=algo, window=window, stream_col=stream_col)
     torch.cuda.synchronize()
     out = Y.cpu().numpy()
     if ld_out_pad:
@@ -41,8 +41,10 @@ def _run(rp, ci, v, x, ncols, ld_pad=0, ld_out_pad=0, algo="auto", window=0):
     return out[:, :d].astype(np.float64)
 
 
-@pytest.mark.parametrize("algo,window", [("rows", 0), ("rows", 4), ("rows", 16)])
-def test_spmm_matches_reference_golden(algo, window):
+@pytest.mark.parametrize("algo,window,halo", [("rows", 0, False), ("rows", 4, False), ("rows", 16, False),
+                                              ("rows", 0, True)])
+def test_spmm_matches_reference_golden(algo, window, halo):
+    """halo: the upper half of X's rows is read with the L2 evict-first hint."""
     meta, z = load_json("spmm_cases.json"), load_npz("spmm_cases.npz")
     for m in meta:
         k, name = m["key"], m["mat"]
@@ -50,7 +52,8 @@ def test_spmm_matches_reference_golden(algo, window):
         x, y = z[k + "_x"], z[k + "_y"]
         # 16-byte aligned rows (vector path) and unaligned rows (scalar path)
         for pad in ((-x.shape[1]) % 4, (-x.shape[1]) % 4 + 1):
-            got = _run(rp, ci, v, x, m["cols"], ld_pad=pad, ld_out_pad=pad, algo=algo, window=window)
+            got = _run(rp, ci, v, x, m["cols"], ld_pad=pad, ld_out_pad=pad, algo=algo, window=window,
+                       stream_col=m["cols"] // 2 if halo else None)
             tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
             assert np.all(np.abs(got - y) <= tol), (k, pad, np.abs(got - y).max())
 

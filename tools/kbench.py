@@ -87,8 +87,8 @@ def spmm(args):
     At = _transpose_device(A)
     print(json.dumps({"setup_s": time.time() - t0, "NL": lay.NL, "NH": lay.NH, "nnz": A.nnz}), flush=True)
     tiled = {}
-    cases = (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("A", A, 64), ("A", A, 41),
-             ("At", At, 41))
+    cases = (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("At", At, 128), ("A", A, 100),
+             ("A", A, 64), ("A", A, 41), ("At", At, 41), ("A", A, 47), ("At", At, 47))
     if args.d_list:
         cases = tuple(c for c in cases if c[2] in args.d_list)
     for name, M, d in cases:
@@ -96,7 +96,8 @@ def spmm(args):
         X = torch.randn(M.cols, ld, device="cuda")
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
-        variants = [("rows", 0), ("tiled", 0)] + ([("rows", 4), ("rows", 16)] if d <= 64 else [])
+        variants = [("rows", 0)] + ([("tiled", 0)] if args.config == "reddit" else []) + \
+            ([("rows", 4), ("rows", 16)] if d <= 64 else [])
         for algo, win in variants:
             if algo == "tiled":
                 if name not in tiled:
@@ -109,7 +110,8 @@ def spmm(args):
                 T = tiled[name]
                 ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
             else:
-                ms = _time(lambda: ops.spmm(M, X, Y, d, algo=algo, window=win), reps=5)
+                sc = lay.NL if name == "A" else None
+                ms = _time(lambda: ops.spmm(M, X, Y, d, algo=algo, window=win, stream_col=sc), reps=5)
             print(json.dumps({"kernel": "spmm", "mat": name, "d": d, "algo": algo, "window": win,
                               "ms": round(ms, 3), "compulsory_gbps": round(comp / ms / 1e6, 1),
                               "gather_gbps": round((8 * M.nnz + 4 * M.nnz * d) / ms / 1e6, 1),
