@@ -250,9 +250,9 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
 #define HB_S(NV, G, U) spmm_rows_vec_kernel<NV, G, U><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, stream_col, hint, next_row, chunk)
     if (d4 <= 8) HB_S(1, 8, 8);
     else if (d4 <= 16) {
-      // short rows (few nonzeros per row): fewer loads in flight per group,
-      // more resident warps; long rows: 16 per group
-      const int w = window > 0 ? window : (nnz >= 0 && nnz < (int64_t)64 * nrows ? 4 : 16);
+      // 4 nonzeros in flight per 16-lane group (8 per warp) and more resident
+      // warps beat deeper per-group windows on both short and long rows
+      const int w = window > 0 ? window : 4;
       if (w == 4) HB_S(1, 16, 4);
       else if (w == 8) HB_S(1, 16, 8);
       else HB_S(1, 16, 16);
