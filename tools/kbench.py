@@ -133,6 +133,11 @@ def gemm(args):
                  ("Y=H W   (l3 bot)", NL, 47, 128, "nn"), ("G=P^T m (l2 half)", 128, 128, NL, "tn"),
                  ("T=m W^T (l2)", NL, 128, 128, "nt"), ("dual Z=[H|AH] W (l1)", NL, 128, 100, "dual"),
                  ("dual Z=[H|AH] W (l2)", NL, 128, 128, "dual"), ("dual j=[S|m] W^T (l3)", NL, 128, 47, "dualt"), ("dual j=[S|m] W^T (l2)", NL, 128, 128, "dualt")]
+    if args.config == "yelp":
+        NL = 716_847
+        cases = [("Z=AH W (l1)", NL, 512, 300, "nn"), ("Z=AH W (l2)", NL, 512, 512, "nn"),
+                 ("Y=H W (l4)", NL, 100, 512, "nn"), ("G=P^T m (l2)", 512, 512, NL, "tn"),
+                 ("T=m W^T (l2)", NL, 512, 512, "nt"), ("T=m W^T (l4)", NL, 512, 100, "nt")]
     ws = torch.empty(64 * 602 * 256, device="cuda")
     def mat(r, c):   # row-major with a 16-byte row stride, like the trainer's buffers
         return torch.randn(r, (c + 3) // 4 * 4, device="cuda", generator=g)[:, :c]
@@ -165,8 +170,9 @@ def gemm(args):
         ops.gemm_set_path(0)
         ms_cb = _time(lambda: torch.mm(A, B, out=C), reps=5)
         fl = 2.0 * M * N * K
-        if args.config == "ogbn":
+        if args.config in ("ogbn", "yelp"):
             print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "tcgen05_ms": round(ms, 4),
+                              "tf32x3_frac": round(3 * fl / ms / 1e9 / 826.0, 3),
                               "hbm_gbps": round(4 * (M * K + M * N + K * N) / ms / 1e6, 1),
                               "cublas_fp32_ms": round(ms_cb, 4)}), flush=True)
             continue
