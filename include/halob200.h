@@ -129,7 +129,8 @@ int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* 
  *   A(m, k) = A[m*lda_m + k*lda_k],  B(k, n) = B[k*ldb_k + n*ldb_n]  (any strides)
  * relu_out (optional, not with split-K): relu_out[m*ldr + n] = max(C[m, n], 0).
  * ws (optional, ws_floats capacity): enables a deterministic split-K for
- * small M*N with long K (the weight gradient G = P^T m). */
+ * small M*N with long K (the weight gradient G = P^T m).  C may be NULL with
+ * beta 0 and relu_out given: only relu(A B) is stored (A-in-TMEM kernel). */
 int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k,
                 const float* B, int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta,
                 float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream);
@@ -140,7 +141,10 @@ int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, 
  * materialising the concatenation.  One pass of the A-in-TMEM kernel over
  * both K ranges (C written once, never read back) when all operands are
  * TMA-describable with matching major order; otherwise two hb_gemm_f32
- * passes.  Operand conventions as hb_gemm_f32; K1, K2 > 0. */
+ * passes.  Operand conventions as hb_gemm_f32; K1, K2 > 0.  C may be NULL
+ * (beta 0, relu_out given): only the ReLU copy is written — a hidden layer's
+ * pre-activation is not needed after the forward; returns HB_ECUDA
+ * (cudaErrorNotSupported) if the single-pass kernel cannot take the operands. */
 int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1_m, int64_t lda1_k,
                  const float* B1, int64_t ldb1_k, int64_t ldb1_n, int32_t K2, const float* A2,
                  int64_t lda2_m, int64_t lda2_k, const float* B2, int64_t ldb2_k, int64_t ldb2_n,

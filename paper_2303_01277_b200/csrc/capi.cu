@@ -134,7 +134,8 @@ int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* 
 int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
                 int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr,
                 float* ws, int64_t ws_floats, void* stream) {
-  if (M < 0 || N < 0 || K < 0 || (M > 0 && N > 0 && (!A || !B || !C || K == 0)) || ldc < N)
+  if (M < 0 || N < 0 || K < 0 || (M > 0 && N > 0 && (!A || !B || K == 0)) || (C && ldc < N) ||
+      (!C && (!relu_out || beta != 0.f)))
     return fail(HB_EINVAL, "hb_gemm_f32: bad arguments");
   return check(hb::launch_gemm_tf32x3(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                       ws_floats, S(stream)),
@@ -145,8 +146,8 @@ int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1
                  int64_t ldb1_k, int64_t ldb1_n, int32_t K2, const float* A2, int64_t lda2_m, int64_t lda2_k,
                  const float* B2, int64_t ldb2_k, int64_t ldb2_n, float* C, int64_t ldc, float beta,
                  float* relu_out, int64_t ldr, float* ws, int64_t ws_floats, void* stream) {
-  if (M < 0 || N < 0 || K1 <= 0 || K2 <= 0 || ldc < N ||
-      (M > 0 && N > 0 && (!A1 || !B1 || !A2 || !B2 || !C)))
+  if (M < 0 || N < 0 || K1 <= 0 || K2 <= 0 || (C && ldc < N) || (!C && (!relu_out || beta != 0.f)) ||
+      (M > 0 && N > 0 && (!A1 || !B1 || !A2 || !B2)))
     return fail(HB_EINVAL, "hb_gemm2_f32: bad arguments");
   return check(hb::launch_gemm2_tf32x3(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2,
                                        ldb2_k, ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, S(stream)),

@@ -297,11 +297,16 @@ int g_gemm_path = 0;   // 0: TMA warp-specialised kernel when operands allow; 1:
 int g_gemm_pair = 0;   // 1: use the CTA-pair (cta_group::2) kernel for 128 < N <= 256
 int g_gemm_ts = 0;     // 1: A split into TMEM (tcgen05.mma A-from-TMEM) kernel
 
+cudaError_t launch_gemm_ts(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
+                           int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+
 cudaError_t launch_gemm_tf32x3(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
                                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
                                int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K <= 0) return cudaErrorInvalidValue;
+  if (C == nullptr)   // ReLU copy only: the A-in-TMEM kernel's TMA-store epilogue
+    return launch_gemm_ts(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   if (g_gemm_path == 0) {
     const cudaError_t e = launch_gemm_tma(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr,
                                           ws, ws_floats, st);
@@ -329,11 +334,12 @@ cudaError_t launch_gemm2_tf32x3(int M, int N, int K1, const float* A1, int64_t l
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K1 <= 0 || K2 <= 0) return cudaErrorInvalidValue;
   static const bool no_dual = getenv("HB_GEMM_NO_DUAL") != nullptr;
+  if (C == nullptr && (no_dual || g_gemm_path != 0 || g_gemm_pair)) return cudaErrorNotSupported;
   if (!no_dual && g_gemm_path == 0 && !g_gemm_pair) {
     const cudaError_t e = launch_gemm_ts_dual(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m,
                                               lda2_k, B2, ldb2_k, ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats,
                                               st);
-    if (e != cudaErrorNotSupported) return e;
+    if (e != cudaErrorNotSupported || C == nullptr) return e;
   }
   cudaError_t e = launch_gemm_tf32x3(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, C, ldc, beta, nullptr, 0, ws,
                                      ws_floats, st);

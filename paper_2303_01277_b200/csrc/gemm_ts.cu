@@ -365,8 +365,10 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]);
         if (p.tma_store) {
-          stage_and_store(stg + sb * 4096, v, &tmC, n0 + c0, row0, lane);
-          sb ^= 1;
+          if (p.C) {
+            stage_and_store(stg + sb * 4096, v, &tmC, n0 + c0, row0, lane);
+            sb ^= 1;
+          }
           if (p.relu_out) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = (v[e] > 0.f || v[e] != v[e]) ? v[e] : 0.f;
@@ -527,12 +529,17 @@ static cudaError_t launch_ts_bn(int M, int N, int K1, const float* A1, int64_t l
     tbl = tb;
   }
   // TMA-store epilogue: plain overwrite of a TMA-describable C (and ReLU copy)
+  // C == nullptr: only the ReLU copy is stored (a hidden layer's z is not
+  // needed after the forward: the backward masks with h = relu(z) > 0)
   static const bool no_tma_store = getenv("HB_GEMM_NO_TMA_STORE") != nullptr;
-  p.tma_store = !no_tma_store && beta == 0.f && p.splits == 1 && gemm_tma_ok(C, ldc, 1) &&
-                (!p.relu_out || gemm_tma_ok(p.relu_out, ldr, 1)) && gemm_make_map(&tc, C, N, M, ldc, 32, false) &&
+  p.tma_store = !no_tma_store && beta == 0.f && p.splits == 1 && (C == nullptr || gemm_tma_ok(C, ldc, 1)) &&
+                (!p.relu_out || gemm_tma_ok(p.relu_out, ldr, 1)) &&
+                (C == nullptr || gemm_make_map(&tc, C, N, M, ldc, 32, false)) &&
                 (!p.relu_out || gemm_make_map(&tr, p.relu_out, N, M, ldr, 32, false));
+  if (C == nullptr && (!p.tma_store || !p.relu_out)) return cudaErrorNotSupported;
   if (!p.tma_store) tc = tr = ta;
   else if (!p.relu_out) tr = tc;
+  else if (C == nullptr) tc = tr;
   const int total = tiles * p.splits;
   const int grid = total < sms ? total : sms;
   static bool attr_set = false;

@@ -4,6 +4,8 @@
 // argmax accuracy (trainer.py:129-144) and keyed dropout (trainer.py:285-289).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
+#include <vector>
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -24,13 +26,40 @@ __global__ void xent_rows_kernel(const float* __restrict__ logits, int64_t ld, i
       continue;
     }
     const float* z = logits + (int64_t)row * ld;
+    const int y = labels[row];
+    if (C <= 128) {
+      // one f64 exp per class: the (up to 4) logits of this lane stay in registers
+      float zv[4];
+      float m = -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = lane + 32 * k;
+        zv[k] = c < C ? z[c] : 0.f;
+        if (c < C) m = fmaxf(m, zv[k]);
+      }
+      m = warp_max(m);
+      double ev[4], s = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ev[k] = (lane + 32 * k < C) ? exp((double)zv[k] - (double)m) : 0.0;
+        s += ev[k];
+      }
+      s = warp_sum_d(s);
+      const double inv = 1.0 / s;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = lane + 32 * k;
+        if (c < C) g[c] = (float)((ev[k] * inv - (c == y ? 1.0 : 0.0)) / norm);
+      }
+      if (lane == 0) row_loss[row] = -(((double)z[y] - (double)m) - log(s)) / norm;
+      continue;
+    }
     float m = -__int_as_float(0x7f800000);
     for (int c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
     m = warp_max(m);
     double s = 0.0;
     for (int c = lane; c < C; c += 32) s += exp((double)z[c] - (double)m);
     s = warp_sum_d(s);
-    const int y = labels[row];
     const double inv = 1.0 / s;
     for (int c = lane; c < C; c += 32) {
       const double p = exp((double)z[c] - (double)m) * inv;
@@ -40,19 +69,54 @@ __global__ void xent_rows_kernel(const float* __restrict__ logits, int64_t ld, i
   }
 }
 
-// Deterministic fixed-order sum of row_loss: one CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) sum_f64_kernel(const double* __restrict__ x, int n,
-                                                       double* __restrict__ out) {
-  __shared__ double sh[1024];
+// Deterministic fixed-order sum of row_loss in two passes: block b reduces
+// the contiguous slice [b*chunk, (b+1)*chunk) into part[b] (fixed tree), then
+// one block sums the parts in order.  The block count depends on n only, so
+// the result is run-to-run bit-identical.
+constexpr int kSumBlocks = 256;
+__global__ void __launch_bounds__(256) sum_f64_part_kernel(const double* __restrict__ x, int n, int chunk,
+                                                           double* __restrict__ part) {
+  __shared__ double sh[256];
+  const int b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += 1024) acc += x[i];
+  for (int i = b0 + threadIdx.x; i < b1; i += 256) acc += x[i];
   sh[threadIdx.x] = acc;
   __syncthreads();
-  for (int s = 512; s; s >>= 1) {
+  for (int s = 128; s; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) sum_f64_kernel(const double* __restrict__ x, int n,
+                                                      double* __restrict__ out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) acc += x[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s; s >>= 1) {
     if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = sh[0];
+}
+
+// kSumBlocks doubles of scratch per (device, stream): launches on one stream are ordered
+static double* sum_scratch(cudaStream_t st) {
+  struct Slot { int dev; cudaStream_t st; double* p; };
+  static std::mutex mu;
+  static std::vector<Slot> slots;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  for (const Slot& s : slots)
+    if (s.dev == dev && s.st == st) return s.p;
+  double* p = nullptr;
+  if (cudaMalloc(&p, kSumBlocks * sizeof(double)) != cudaSuccess) return nullptr;
+  slots.push_back({dev, st, p});
+  return p;
 }
 
 // ---- ReLU and relu' product ----------------------------------------------------
@@ -196,7 +260,15 @@ cudaError_t launch_xent(const float* logits, int64_t ld, int n, int C, const int
                         const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
                         double* loss_out, cudaStream_t st) {
   if (n > 0) xent_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss);
-  sum_f64_kernel<<<1, 1024, 0, st>>>(row_loss, n, loss_out);
+  if (n <= 16 * 1024) {
+    sum_f64_kernel<<<1, 256, 0, st>>>(row_loss, n, loss_out);
+  } else {
+    double* part = sum_scratch(st);
+    if (!part) return cudaErrorMemoryAllocation;
+    const int chunk = (n + kSumBlocks - 1) / kSumBlocks;
+    sum_f64_part_kernel<<<kSumBlocks, 256, 0, st>>>(row_loss, n, chunk, part);
+    sum_f64_kernel<<<1, 256, 0, st>>>(part, kSumBlocks, loss_out);
+  }
   return cudaGetLastError();
 }
 

@@ -137,9 +137,13 @@ def gemm(A, B, C, beta: float = 0.0, relu_out=None, ws=None, stream=None):
     (trainer.py:294,313,318-321).  Returns C."""
     M, K = A.shape
     K2, N = B.shape
-    assert K == K2 and C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
+    assert K == K2
+    if C is None:       # store only relu(A B)
+        assert relu_out is not None and beta == 0.0
+    else:
+        assert C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
     _lib.call("hb_gemm_f32", M, N, K, ptr(A), A.stride(0), A.stride(1), ptr(B), B.stride(0),
-              B.stride(1), ptr(C), C.stride(0), float(beta), ptr(relu_out),
+              B.stride(1), ptr(C), C.stride(0) if C is not None else 0, float(beta), ptr(relu_out),
               relu_out.stride(0) if relu_out is not None else 0, ptr(ws),
               ws.numel() if ws is not None else 0, stream_handle(stream))
     return C
@@ -153,9 +157,13 @@ def gemm2(A1, B1, A2, B2, C, beta: float = 0.0, relu_out=None, ws=None, stream=N
     M2, K2 = A2.shape
     assert M == M2 and B1.shape[0] == K1 and B2.shape[0] == K2 and B1.shape[1] == B2.shape[1]
     N = B1.shape[1]
-    assert C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
+    if C is None:       # store only relu(A1 B1 + A2 B2)
+        assert relu_out is not None and beta == 0.0
+    else:
+        assert C.shape[0] == M and C.shape[1] == N and C.stride(1) == 1
     _lib.call("hb_gemm2_f32", M, N, K1, ptr(A1), A1.stride(0), A1.stride(1), ptr(B1), B1.stride(0), B1.stride(1),
-              K2, ptr(A2), A2.stride(0), A2.stride(1), ptr(B2), B2.stride(0), B2.stride(1), ptr(C), C.stride(0),
+              K2, ptr(A2), A2.stride(0), A2.stride(1), ptr(B2), B2.stride(0), B2.stride(1), ptr(C),
+              C.stride(0) if C is not None else 0,
               float(beta), ptr(relu_out), relu_out.stride(0) if relu_out is not None else 0, ptr(ws),
               ws.numel() if ws is not None else 0, stream_handle(stream))
     return C

@@ -424,8 +424,9 @@ class DeviceRank:
 
     # -- dense combine + aggregation of one layer --------------------------------
     def _mm(self, a, b, out, accumulate: bool = False, relu_out=None):
-        """out (+)= a @ b (trainer.py:294,313,318-321)."""
-        nl, nc = out.shape
+        """out (+)= a @ b (trainer.py:294,313,318-321).  out None: only
+        relu_out = relu(a @ b) is stored (tcgen05 path)."""
+        nl, nc = a.shape[0], b.shape[1]
         with self.timer("gemm", 0, 2 * a.shape[0] * a.shape[1] * b.shape[1]):
             if self.gemm_impl == "cublas":
                 if accumulate:
@@ -441,8 +442,9 @@ class DeviceRank:
 
     def _mm2(self, a1, b1, a2, b2, out, relu_out=None):
         """out = a1 @ b1 + a2 @ b2: the SAGE combine over [h | A h] (trainer.py:294,318-321)
-        in one GEMM pass, without materialising the concatenation."""
-        nl, nc = out.shape
+        in one GEMM pass, without materialising the concatenation.  out None:
+        only relu_out = relu(...) is stored (tcgen05 path)."""
+        nl, nc = a1.shape[0], b1.shape[1]
         with self.timer("gemm", 0, 2 * a1.shape[0] * (a1.shape[1] + a2.shape[1]) * b1.shape[1]):
             if self.gemm_impl == "cublas":
                 self.torch.mm(a1, b1, out=out)
@@ -490,10 +492,13 @@ class DeviceRank:
         hout = self.Ht[l + 1][:NL, :dout] if l < self.L else None
         if not self.post[l]:
             self._spmm(self.A, Hd, agg, d)
+            # a hidden layer's z is never read again (the backward masks with
+            # h > 0): the tcgen05 epilogue stores only h = relu(z)
+            zout = None if (hout is not None and self.gemm_impl != "cublas") else Z
             if sage:
-                self._mm2(Hd[:NL, :d], Wtop, agg[:, :d], Wbot, Z, relu_out=hout)
+                self._mm2(Hd[:NL, :d], Wtop, agg[:, :d], Wbot, zout, relu_out=hout)
             else:
-                self._mm(agg[:, :d], Wbot, Z, relu_out=hout)
+                self._mm(agg[:, :d], Wbot, zout, relu_out=hout)
             return
         Y = self.Y[l]
         self._mm(Hd[:, :d], Wbot, Y[:, :dout])

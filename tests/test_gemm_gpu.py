@@ -200,3 +200,24 @@ def test_gemm2_dual(M, ws_on):
     J0 = J.clone()
     ops.gemm2(S, W[d:].t(), m, W[:d].t(), J, beta=1.0, ws=ws)
     _check(torch.cat([S, m], 1), torch.cat([W[d:].t(), W[:d].t()], 0), J, beta=1.0, C0=J0)
+
+
+def test_relu_only_store():
+    """C = NULL: only relu(A B) / relu(A1 B1 + A2 B2) is written."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(9)
+    M, K, N = 40000, 100, 128
+    A1 = torch.randn(M, 104, device="cuda", generator=g)[:, :K]
+    A2 = torch.randn(M, 104, device="cuda", generator=g)[:, :K]
+    W = torch.randn(2 * K, N, device="cuda", generator=g)
+    ws = torch.empty(4 << 20, device="cuda")
+    R = torch.full((M, N + 4), 3.0, device="cuda")
+    ops.gemm2(A1, W[:K], A2, W[K:], None, relu_out=R[:, :N], ws=ws)
+    Z = torch.empty(M, N, device="cuda")
+    ops.gemm2(A1, W[:K], A2, W[K:], Z, ws=ws)
+    assert torch.equal(R[:, :N], torch.clamp(Z, min=0))
+    assert bool((R[:, N:] == 3.0).all())
+    R2 = torch.full((M, N), 3.0, device="cuda")
+    ops.gemm(A1, W[:K], None, relu_out=R2, ws=ws)
+    ops.gemm(A1, W[:K], Z, ws=ws)
+    assert torch.equal(R2, torch.clamp(Z, min=0))
