@@ -1203,6 +1203,126 @@ dequant_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int nu
   }
 }
 
+// K2 backward, 1 bit, ascending-peer accumulate (trainer.py:339-350 order):
+// out[t] = fp32( f64(out[t]) + sum_k (f64(sc_k) * code + f64(mn_k)) ), the
+// same operation sequence as dequant_batched_kernel — with code in {0, 1} the
+// per-source term is one of two per-source constants v0 = 0 + mn, v1 = sc + mn
+// (f64 mul by 0/1 is exact), so each element costs one f64 add per source.
+// The destination rows' current values are read as float4 one row ahead of
+// the row being accumulated (software-pipelined), so the read-modify-write
+// latency of consecutive rows overlaps.
+template <int NCH>
+__global__ void __launch_bounds__(kQWarps * 32)
+dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_dst,
+                      const int32_t* __restrict__ dst_rows, const int32_t* __restrict__ src_ptr,
+                      const int32_t* __restrict__ src_rows, int d, float* __restrict__ dst, int64_t ld) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  const int rb = (d + 7) >> 3;
+  int cs = 0;
+  float my_mn = 0.f, my_sc = 0.f;
+  uint64_t my_pay = 0;
+  auto prepare = [&](int w0, int s1) {
+    const int k = w0 + lane;
+    my_mn = 0.f;
+    my_sc = 0.f;
+    my_pay = 0;
+    if (k < s1) {
+      const int q = src_rows[k];
+      if (!(q >= seg_begin[cs] && q < seg_begin[cs + 1])) cs = find_segment_smem(seg_begin, nseg, q);
+      const hb_segment_t& sg = segs_s[cs];
+      const int r = q - sg.row_begin;
+      const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+      const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
+      my_mn = mp[0];
+      my_sc = mp[1];
+      my_pay = reinterpret_cast<uint64_t>(blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb);
+    }
+  };
+  auto load_row = [&](int t, float4 (&o)[NCH]) {
+    const float* row = dst + (int64_t)t * ld;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c0 = ch * 128 + 4 * lane;
+      o[ch] = c0 + 3 < d ? *reinterpret_cast<const float4*>(row + c0)
+                         : make_float4(c0 < d ? row[c0] : 0.f, c0 + 1 < d ? row[c0 + 1] : 0.f,
+                                       c0 + 2 < d ? row[c0 + 2] : 0.f, 0.f);
+    }
+  };
+  for (int i0 = (blockIdx.x * kQWarps + warp) * 32; i0 < num_dst; i0 += gridDim.x * kQWarps * 32) {
+    const int i = i0 + lane;
+    const bool valid = i < num_dst;
+    const int my_t = valid ? dst_rows[i] : 0;
+    const int my_k0 = valid ? src_ptr[i] : 0;
+    const int my_k1 = valid ? src_ptr[i + 1] : 0;
+    const int n = min(32, num_dst - i0);
+    const int s0 = __shfl_sync(0xffffffffu, my_k0, 0);
+    const int s1 = __shfl_sync(0xffffffffu, my_k1, n - 1);
+    int w0 = s0;
+    prepare(w0, s1);
+    float4 cur[NCH];
+    load_row(__shfl_sync(0xffffffffu, my_t, 0), cur);
+    for (int j = 0; j < n; ++j) {
+      const int t = __shfl_sync(0xffffffffu, my_t, j);
+      const int tn = __shfl_sync(0xffffffffu, my_t, (j + 1) & 31);
+      const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
+      float4 nxt[NCH];
+      if (j + 1 < n) load_row(tn, nxt);
+      double acc[NCH][4];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        acc[ch][0] = (double)cur[ch].x; acc[ch][1] = (double)cur[ch].y;
+        acc[ch][2] = (double)cur[ch].z; acc[ch][3] = (double)cur[ch].w;
+      }
+      for (int k = k0; k < k1; ++k) {
+        if (k >= w0 + 32) {           // warp-uniform: slide the source window
+          w0 = k;
+          prepare(w0, s1);
+        }
+        const int sl = k - w0;
+        const double mn = (double)__shfl_sync(0xffffffffu, my_mn, sl);
+        const double sc = (double)__shfl_sync(0xffffffffu, my_sc, sl);
+        const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, sl));
+        const double v0 = __dadd_rn(__dmul_rn(sc, 0.0), mn), v1 = __dadd_rn(__dmul_rn(sc, 1.0), mn);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c0 = ch * 128 + 4 * lane;
+          if (c0 >= d) continue;
+          const uint32_t nib = (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[ch][e] = __dadd_rn(acc[ch][e], ((nib >> e) & 1u) ? v1 : v0);
+        }
+      }
+      float* out = dst + (int64_t)t * ld;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        if (c0 >= d) continue;
+        const float4 v = make_float4(__double2float_rn(acc[ch][0]), __double2float_rn(acc[ch][1]),
+                                     __double2float_rn(acc[ch][2]), __double2float_rn(acc[ch][3]));
+        if (c0 + 3 < d) {
+          *reinterpret_cast<float4*>(out + c0) = v;
+        } else {
+          out[c0] = v.x;
+          if (c0 + 1 < d) out[c0 + 1] = v.y;
+          if (c0 + 2 < d) out[c0 + 2] = v.z;
+        }
+      }
+      if (j + 1 < n) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) cur[ch] = nxt[ch];
+      }
+    }
+  }
+}
+
 __global__ void philox_uniforms_kernel(uint64_t k0, uint64_t k1, uint64_t start, int64_t n,
                                        double* __restrict__ out) {
   const uint64_t first_blk = start >> 2;
@@ -1292,6 +1412,8 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
   const int grid = want < num_sms() * 8 ? want : num_sms() * 8;
   const int nch = (d + 127) / 128;
   static const bool legacy = getenv("HB_K2_LEGACY") != nullptr;
+  static const bool no_acc = getenv("HB_K2_NO_B1ACC") != nullptr;
+  const bool vec_dst = !no_acc && ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
   if (!legacy && nseg <= kMaxSmemSegs && nch <= 8) {
 #define HB_K2(N, F) dequant_rows_kernel<N, F><<<grid, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, \
                                                                        src_ptr, src_rows, d, bits, dst, ld, accumulate)
@@ -1307,6 +1429,17 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
       else if (nch <= 5) HB_K2B(5);
       else HB_K2B(8);
 #undef HB_K2B
+    } else if (accumulate && bits == 1 && vec_dst) {
+      const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
+      const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
+#define HB_K2A(N) dequant_b1_acc_kernel<N><<<g32, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, \
+                                                                      src_rows, d, dst, ld)
+      if (nch <= 1) HB_K2A(1);
+      else if (nch <= 2) HB_K2A(2);
+      else if (nch <= 4) HB_K2A(4);
+      else if (nch <= 5) HB_K2A(5);
+      else HB_K2A(8);
+#undef HB_K2A
     } else if (bits != 32 && nch <= 4) {
       const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
       const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
