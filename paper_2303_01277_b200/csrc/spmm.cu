@@ -204,9 +204,10 @@ spmm_rows_scalar_kernel(int nrows, const int64_t* __restrict__ row_ptr, const in
 // algo: 0 auto, 1 row gather (the same kernel: the TMA-tiled path is a
 // separate entry point, hb_spmm_tiled).  `window` > 0 overrides the number of
 // nonzeros a lane group keeps in flight (tuning only).
-// Per-(device, stream) pair of ints {next row, warps finished}: launches on one
+// Per-(device, stream) pair of ints {next work item, workers finished} for the
+// dynamically scheduled kernels (row-gather and tiled SpMM): launches on one
 // stream are ordered, and each launch leaves the pair at zero for the next.
-static int* row_counter(cudaStream_t st) {
+int* work_counter(cudaStream_t st) {
   struct Slot { int dev; cudaStream_t st; int* p; };
   static std::mutex mu;
   static std::vector<Slot> slots;
@@ -239,7 +240,7 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
   int* next_row = nullptr;
   int chunk = 1;
   if (dyn) {
-    next_row = row_counter(st);
+    next_row = work_counter(st);
     if (!next_row) return cudaErrorMemoryAllocation;
     // ~256 nonzeros per grab
     const int64_t avg = nnz > 0 ? (nnz + nrows - 1) / nrows : 32;

@@ -7,7 +7,11 @@
 //     holding >= a threshold of nonzeros, stored as row-sorted (col - c0, val)
 //     records plus kTRB+1 row offsets per tile;
 //   * a residual CSR with every other nonzero.
-// A persistent CTA takes (row block, feature panel) work items.  A producer
+// A persistent CTA takes (row block, feature panel) work items in ascending
+// order from a global counter (dynamic: the CTAs finish within one item of
+// each other, and all of them work on neighbouring row blocks, whose X windows
+// share L2), passed from the producer warp to the consumers through a small
+// smem queue.  A producer
 // warp streams the block's tiles through a 2-stage smem ring: one TMA 2-D
 // box load of the X window (kTW rows x panel columns) plus two bulk copies of
 // the tile's records and row offsets, all completing on one mbarrier.  Sixteen
@@ -32,9 +36,11 @@ constexpr int kRPW = 4;          // rows per consumer warp
 constexpr int kMaxRec = 1024;    // records per tile (ops.TiledCsr splits denser tiles)
 constexpr int kConsumers = kTRB / kRPW;
 constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int kQ = 4;            // work-item queue depth (producer -> consumers)
 
 struct Args {
   int nrows, nblocks, npanels, d;
+  int* next_item;                // {next item, CTAs finished}: self-resetting counter pair
   int pw;                        // staged panel width (floats): min(P, d rounded up to 4)
   const int32_t* tile_ptr;       // [nblocks + 1]
   const int32_t* tile_win;       // [ntiles]
@@ -91,13 +97,18 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   constexpr int NG = 32 / G;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  __shared__ __align__(8) uint64_t full[S], empty[S];
+  __shared__ __align__(8) uint64_t full[S], empty[S], ifull[kQ], iempty[kQ];
+  __shared__ int item_q[kQ];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hg = lane / G, gl = lane % G;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
+    }
+    for (int q = 0; q < kQ; ++q) {
+      mbar_init(&ifull[q], 1);
+      mbar_init(&iempty[q], kConsumers);
     }
     fence_mbar_init();
   }
@@ -110,24 +121,40 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
     // in stage s, so each barrier is still waited on in phase order by a
     // single thread): the tiles' metadata loads (tile_off / tile_win,
     // dependent global reads) are then S deep in flight ahead of the ring
-    if (lane < S) {
-      int it = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int b = item / a.npanels, pn = item % a.npanels;
-        const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
-        for (int t = t0; t < t1; ++t, ++it) {
-          if (it % S != lane) continue;
-          const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          uint8_t* st = smem + s * S_::STAGE;
-          const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
-          const uint32_t nzb = (uint32_t)((o1 - o0) * 8);
-          mbar_expect_tx(&full[s], (uint32_t)(kTW * a.pw * 4) + nzb + S_::RO_BYTES);
-          tma_2d(st, &tmX, pn * P, a.tile_win[t] * kTW, &full[s]);
-          if (nzb) tma_load_1d(st + S_::X_BYTES, a.tile_nz + o0, nzb, &full[s]);
-          tma_load_1d(st + S_::X_BYTES + S_::NZ_BYTES, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES,
-                      &full[s]);
+    int it = 0;
+    for (int qi = 0;; ++qi) {
+      // lane 0 claims the next item and publishes it to the consumers
+      int item = 0;
+      if (lane == 0) {
+        item = atomicAdd(a.next_item, 1);
+        const int q = qi % kQ;
+        mbar_wait(&iempty[q], ((qi / kQ) & 1) ^ 1);
+        item_q[q] = item;
+        mbar_arrive_cta(&ifull[q]);
+        if (item >= items && atomicAdd(a.next_item + 1, 1) == (int)gridDim.x - 1) {
+          atomicExch(a.next_item, 0);      // last CTA out re-arms the counter pair
+          atomicExch(a.next_item + 1, 0);
         }
+      }
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= items) break;
+      const int b = item / a.npanels, pn = item % a.npanels;
+      const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
+      // lane s issues every tile that lands in ring stage s (each barrier is
+      // waited on in phase order by a single thread); the tiles' metadata
+      // loads are then S deep in flight ahead of the ring
+      for (int t = t0; t < t1; ++t, ++it) {
+        if (lane >= S || it % S != lane) continue;
+        const int s = it % S;
+        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        uint8_t* st = smem + s * S_::STAGE;
+        const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
+        const uint32_t nzb = (uint32_t)((o1 - o0) * 8);
+        mbar_expect_tx(&full[s], (uint32_t)(kTW * a.pw * 4) + nzb + S_::RO_BYTES);
+        tma_2d(st, &tmX, pn * P, a.tile_win[t] * kTW, &full[s]);
+        if (nzb) tma_load_1d(st + S_::X_BYTES, a.tile_nz + o0, nzb, &full[s]);
+        tma_load_1d(st + S_::X_BYTES + S_::NZ_BYTES, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES,
+                    &full[s]);
       }
     }
     __syncwarp();
@@ -137,7 +164,13 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   // ---------------- consumers ----------------
   int it = 0;
   const int pw4 = a.pw / 4;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+  for (int qi = 0;; ++qi) {
+    const int q = qi % kQ;
+    mbar_wait(&ifull[q], (qi / kQ) & 1);
+    const int item = item_q[q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&iempty[q]);
+    if (item >= items) break;
     const int b = item / a.npanels, pn = item % a.npanels;
     const int r0 = b * kTRB + warp * kRPW;
     const int col0 = pn * P;
@@ -282,6 +315,8 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
 
 }  // namespace st
 
+int* work_counter(cudaStream_t st);
+
 cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
                               const int64_t* tile_off, const uint16_t* tile_rowoff, const int2* tile_nz,
                               const int64_t* res_ptr, const int32_t* res_col, const float* res_val, const float* X,
@@ -293,6 +328,8 @@ cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* 
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_nz = tile_nz; a.res_ptr = res_ptr; a.res_col = res_col; a.res_val = res_val;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
+  a.next_item = work_counter(stream);
+  if (!a.next_item) return cudaErrorMemoryAllocation;
   if (d <= 64) return st::launch_nv<1, 16, 8>(a, xrows, stream);     // 24 KB stages
   if (d <= 128) return st::launch_nv<1, 32, 5>(a, xrows, stream);    // 40 KB stages
   return st::launch_nv<2, 32, 3>(a, xrows, stream);                  // 72 KB stages, 256-column panels
