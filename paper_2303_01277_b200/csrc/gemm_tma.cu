@@ -541,6 +541,8 @@ extern int g_gemm_ts;
 extern int g_gemm_path;
 cudaError_t launch_gemm_ts(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
                            int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
+cudaError_t launch_gemm_dw(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
+                           int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 
 // Returns cudaErrorNotSupported when an operand is not TMA-describable (the
 // caller then uses the SIMT-staged kernel).
@@ -558,6 +560,16 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
   const bool use_ts = ts_env >= 0 ? ts_env == 1 : (g_gemm_ts || (g_gemm_path == 0 && !g_gemm_pair && tall));
   if (use_ts) {
     const cudaError_t e = launch_gemm_ts(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
+                                         ws_floats, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  // long-K weight gradients (few output tiles, split-K): A-in-TMEM kernel with
+  // decoupled A / B rings
+  static const int dw_env = getenv("HB_GEMM_DW") ? atoi(getenv("HB_GEMM_DW")) : 1;
+  const int tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
+  if (dw_env && g_gemm_path == 0 && !g_gemm_pair && !g_gemm_ts && ws != nullptr && tiles128 < num_sms() &&
+      (K + 31) / 32 >= 8) {
+    const cudaError_t e = launch_gemm_dw(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                          ws_floats, st);
     if (e != cudaErrorNotSupported) return e;
   }

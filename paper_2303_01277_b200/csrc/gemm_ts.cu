@@ -443,6 +443,273 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Weight-gradient variant (G = P^T m: small M x N, K = rows, split-K): A in
+// TMEM as above, but the raw A tiles have their own ring, released by the
+// converter warps as soon as they hold the rows in registers, while B (raw
+// fp32, split in place into hi | lo) sits in a separate ring released by the
+// MMA commit.  Each split owns one output tile, so the accumulator is single
+// (BN columns) and the freed TMEM holds CB A-slots; BN = 256 keeps B re-reads
+// low.  The all-smem kernel keeps raw A/B and their hi/lo in one 2-stage ring
+// and measured ~48 % tensor-pipe activity on these shapes (latency-bound).
+template <int BN>
+struct DwCfg {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int CB = BN == 256 ? 3 : 4;                 // B (+ TMEM A slot) stages
+  static constexpr int RA = BN == 256 ? 2 : (BN == 128 ? 3 : 4);  // raw A stages
+  static constexpr int SMEM = CB * 2 * B_BYTES + RA * A_BYTES + 1024;
+  static constexpr uint32_t ACC = BN;
+  static_assert(ACC + CB * 64 <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024, "smem budget");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_dw_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  using C_ = DwCfg<BN>;
+  constexpr int CB = C_::CB, RA = C_::RA;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* bring = smem;                                   // CB x (B hi | B lo)
+  uint8_t* aring = smem + CB * 2 * C_::B_BYTES;            // RA x raw A
+  __shared__ __align__(8) uint64_t afull[RA], aempty[RA], bfull[CB], conv[CB], bempty[CB], tfull, tempty;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = p.mt * p.nt * p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 4);
+    }
+    for (int s = 0; s < CB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mi, ni, si;
+        tile_coords(p, t, mi, ni, si);
+        const int kb0 = si * p.kb_per_split, kb1 = min(p.nkb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int ra = it % RA, sb = it % CB;
+          const int k0 = kb * BK;
+          mbar_wait(&aempty[ra], ((it / RA) & 1) ^ 1);
+          uint8_t* a_raw = aring + ra * C_::A_BYTES;
+          mbar_expect_tx(&afull[ra], C_::A_BYTES);
+          if (p.a_mn) {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) tma_2d(a_raw + j * 4096, &tmA, mi * BM + 32 * j, k0, &afull[ra]);
+          } else {
+            tma_2d(a_raw, &tmA, k0, mi * BM, &afull[ra]);
+          }
+          mbar_wait(&bempty[sb], ((it / CB) & 1) ^ 1);
+          uint8_t* b_hi = bring + sb * 2 * C_::B_BYTES;
+          mbar_expect_tx(&bfull[sb], C_::B_BYTES);
+          if (p.b_mn) {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) tma_2d(b_hi + j * 4096, &tmB, ni * BN + 32 * j, k0, &bfull[sb]);
+          } else {
+            tma_2d(b_hi, &tmB, k0, ni * BN, &bfull[sb]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.b_mn << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      const uint32_t b_step = p.b_mn ? 1024u : 32u, b_lbo = p.b_mn ? 4096u : 16u;
+      const uint32_t b_sbo = p.b_mn ? 512u : 1024u, b_lay = p.b_mn ? 1u : 2u;
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
+        int mi, ni, si;
+        tile_coords(p, t, mi, ni, si);
+        const int kb0 = si * p.kb_per_split, kb1 = min(p.nkb, kb0 + p.kb_per_split);
+        mbar_wait(&tempty, (tc & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int sb = it % CB;
+          mbar_wait(&conv[sb], (it / CB) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a_hi_t = tmem + C_::ACC + (uint32_t)(sb * 64);
+          const uint32_t a_lo_t = a_hi_t + 32;
+          const uint32_t b_hi = smem_u32(bring + sb * 2 * C_::B_BYTES), b_lo = b_hi + C_::B_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t dbh = sw_desc(b_hi + kk * b_step, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = sw_desc(b_lo + kk * b_step, b_lbo, b_sbo, b_lay);
+            umma_ts(tmem, a_lo_t + 8 * kk, dbh, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            umma_ts(tmem, a_hi_t + 8 * kk, dbl, idesc, 1u);
+            umma_ts(tmem, a_hi_t + 8 * kk, dbh, idesc, 1u);
+          }
+          umma_commit(&bempty[sb]);
+        }
+        umma_commit(&tfull);
+      }
+    }
+    __syncwarp();
+  } else if (warp < kEpi0) {
+    // ---------------- converters: A -> TMEM hi/lo, B split in place ----------------
+    const int lg = warp & 3;
+    const int r = lg * 32 + lane;
+    const int ct = threadIdx.x - kConv0 * 32;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mi, ni, si;
+      tile_coords(p, t, mi, ni, si);
+      const int kb0 = si * p.kb_per_split, kb1 = min(p.nkb, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int ra = it % RA, sb = it % CB;
+        mbar_wait(&afull[ra], (it / RA) & 1);
+        const uint8_t* st = aring + ra * C_::A_BYTES;
+        float x[32];
+        if (!p.a_mn) {
+          const uint4* row = reinterpret_cast<const uint4*>(st + r * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = row[c ^ (r & 7)];
+            x[4 * c] = __uint_as_float(v.x); x[4 * c + 1] = __uint_as_float(v.y);
+            x[4 * c + 2] = __uint_as_float(v.z); x[4 * c + 3] = __uint_as_float(v.w);
+          }
+        } else {
+          const uint8_t* box = st + (r >> 5) * 4096;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const uint32_t o = (uint32_t)(k * 128 + (r & 31) * 4);
+            x[k] = *reinterpret_cast<const float*>(box + (o ^ (((o >> 7) & 3u) << 5)));
+          }
+        }
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          hi[k] = rna_tf32(x[k]);
+          lo[k] = rna_tf32(x[k] - __uint_as_float(hi[k]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(&aempty[ra]);      // raw A consumed: the producer may refill it
+        mbar_wait(&bfull[sb], (it / CB) & 1);                // also orders the TMEM slot's previous MMAs
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + C_::ACC + (uint32_t)(sb * 64);
+        tmem_st32(taddr, hi);
+        tmem_st32(taddr + 32, lo);
+        uint4* b_hi = reinterpret_cast<uint4*>(bring + sb * 2 * C_::B_BYTES);
+        uint4* b_lo = reinterpret_cast<uint4*>(bring + sb * 2 * C_::B_BYTES + C_::B_BYTES);
+#pragma unroll 4
+        for (int i = ct; i < C_::B_BYTES / 16; i += 128) {
+          const uint4 v = b_hi[i];
+          uint4 h, l;
+          h.x = rna_tf32(__uint_as_float(v.x)); l.x = rna_tf32(__uint_as_float(v.x) - __uint_as_float(h.x));
+          h.y = rna_tf32(__uint_as_float(v.y)); l.y = rna_tf32(__uint_as_float(v.y) - __uint_as_float(h.y));
+          h.z = rna_tf32(__uint_as_float(v.z)); l.z = rna_tf32(__uint_as_float(v.z) - __uint_as_float(h.z));
+          h.w = rna_tf32(__uint_as_float(v.w)); l.w = rna_tf32(__uint_as_float(v.w) - __uint_as_float(h.w));
+          b_hi[i] = h;
+          b_lo[i] = l;
+        }
+        fence_proxy_async_smem();
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(&conv[sb]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: split-K partial (or C with beta / ReLU) ----------------
+    const int lg = warp & 3;
+    int tc = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
+      int mi, ni, si;
+      tile_coords(p, t, mi, ni, si);
+      mbar_wait(&tfull, tc & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = mi * BM + lg * 32 + lane;
+      const int n0 = ni * BN;
+      const int ncols = min(BN, p.N - n0);
+      const bool split = p.splits > 1;
+      float* crow = split ? p.ws + ((int64_t)si * p.M + row) * p.N : p.C + (int64_t)row * p.ldc;
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        uint32_t rr[32];
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+              "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
+              "=r"(rr[14]), "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]), "=r"(rr[18]), "=r"(rr[19]), "=r"(rr[20]),
+              "=r"(rr[21]), "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]), "=r"(rr[26]), "=r"(rr[27]),
+              "=r"(rr[28]), "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
+            : "r"(taddr)
+            : "memory");
+        if (c0 + 32 >= ncols) {
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(&tempty);
+        }
+        if (row >= p.M) continue;
+        const int nb = n0 + c0;
+        const int nv = min(32, p.N - nb);
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]);
+        if (split) {
+          const bool vec = ((p.N & 3) == 0);
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            if (vec && e + 3 < nv) {
+              *reinterpret_cast<float4*>(crow + nb + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (e + u < nv) crow[nb + e + u] = v[e + u];
+            }
+          }
+          continue;
+        }
+        float* rrow = p.relu_out ? p.relu_out + (int64_t)row * p.ldr + nb : nullptr;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (e < nv) {
+            float o = v[e];
+            if (p.beta != 0.f) o += p.beta * crow[nb + e];
+            crow[nb + e] = o;
+            if (rrow) rrow[e] = (o > 0.f || o != o) ? o : 0.f;
+          }
+        }
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 }  // namespace gts
 
 bool gemm_make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld, int box_outer,
@@ -581,6 +848,63 @@ cudaError_t launch_gemm_ts_dual(int M, int N, int K1, const float* A1, int64_t l
                             ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
   return launch_ts_bn<128>(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m, lda2_k, B2, ldb2_k,
                            ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+}
+
+
+// Split-K weight-gradient GEMM on the A-in-TMEM kernel with decoupled A / B
+// rings (gemm_dw_kernel).  cudaErrorNotSupported: caller uses the all-smem kernel.
+template <int BN>
+static cudaError_t launch_dw_bn(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
+                                int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
+                                int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
+  using C_ = gts::DwCfg<BN>;
+  gts::Params p{};
+  p.M = M; p.N = N; p.K = K;
+  p.a_mn = lda_k == 1 ? 0 : 1;
+  p.b_mn = ldb_k == 1 ? 0 : 1;
+  CUtensorMap ta, tb;
+  bool ok = p.a_mn ? gemm_make_map(&ta, A, M, K, lda_k, 32, true) : gemm_make_map(&ta, A, K, M, lda_m, gts::BM, false);
+  ok = ok && (p.b_mn ? gemm_make_map(&tb, B, N, K, ldb_k, 32, true) : gemm_make_map(&tb, B, K, N, ldb_n, BN, false));
+  if (!ok) return cudaErrorNotSupported;
+  p.mt = (M + gts::BM - 1) / gts::BM;
+  p.nt = (N + BN - 1) / BN;
+  p.nkb = (K + gts::BK - 1) / gts::BK;
+  p.nkb1 = p.nkb;
+  const int sms = num_sms();
+  const int tiles = p.mt * p.nt;
+  int splits = sms / tiles;
+  if (splits > p.nkb / 4) splits = p.nkb / 4;
+  const int64_t by_ws = ws_floats / ((int64_t)M * N);
+  if (splits > by_ws) splits = (int)by_ws;
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.nkb + splits - 1) / splits;
+  p.splits = (p.nkb + p.kb_per_split - 1) / p.kb_per_split;
+  p.C = C; p.ldc = ldc; p.beta = beta; p.relu_out = p.splits > 1 ? nullptr : relu_out; p.ldr = ldr;
+  p.ws = p.splits > 1 ? ws : nullptr;
+  const int total = tiles * p.splits;
+  const int grid = total < sms ? total : sms;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gts::gemm_dw_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C_::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  gts::gemm_dw_kernel<BN><<<grid, gts::kThreads, C_::SMEM, st>>>(ta, tb, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (p.splits > 1) e = gemm_splitk_reduce(ws, p.splits, M, N, C, ldc, beta, relu_out, ldr, st);
+  return e;
+}
+
+cudaError_t launch_gemm_dw(int M, int N, int K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
+                           int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out, int64_t ldr,
+                           float* ws, int64_t ws_floats, cudaStream_t st) {
+  if (N <= 64)
+    return launch_dw_bn<64>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+  if (N <= 128)
+    return launch_dw_bn<128>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
+  return launch_dw_bn<256>(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws, ws_floats, st);
 }
 
 }  // namespace hb
