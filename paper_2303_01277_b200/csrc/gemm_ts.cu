@@ -148,7 +148,9 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   using C_ = Cfg<BN>;
   constexpr int S = C_::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the __shared__ array (an integer round
+  // trip would hide the address space and turn every access generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full[S], conv[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
 
@@ -471,7 +473,9 @@ gemm_dw_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   using C_ = DwCfg<BN>;
   constexpr int CB = C_::CB, RA = C_::RA;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the __shared__ array (an integer round
+  // trip would hide the address space and turn every access generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* bring = smem;                                   // CB x (B hi | B lo)
   uint8_t* aring = smem + CB * 2 * C_::B_BYTES;            // RA x raw A
   __shared__ __align__(8) uint64_t afull[RA], aempty[RA], bfull[CB], conv[CB], bempty[CB], tfull, tempty;

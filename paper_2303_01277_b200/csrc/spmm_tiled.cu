@@ -96,7 +96,9 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   constexpr int P = S_::P;
   constexpr int NG = 32 / G;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // aligned by pointer arithmetic on the __shared__ array (an integer round
+  // trip would hide the address space and turn every access generic)
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   __shared__ __align__(8) uint64_t full[S], empty[S], ifull[kQ], iempty[kQ];
   __shared__ int item_q[kQ];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
