@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdint>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace hb {
@@ -89,8 +90,8 @@ __device__ __forceinline__ void fma_row(float4 (&acc)[NV], float v, const float4
   }
 }
 
-template <int NV, int G, int S>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NV, int G, int S, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   using S_ = Smem<NV, G, S>;
   constexpr int P = S_::P;
@@ -176,6 +177,68 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
     const int b = item / a.npanels, pn = item % a.npanels;
     const int r0 = b * kTRB + warp * kRPW;
     const int col0 = pn * P;
+    if constexpr (G == 8) {
+      // narrow panels (P = 64): lane group hg (8 lanes x NV float4) owns row
+      // r0 + hg outright, so a warp walks its 4 short rows in parallel instead
+      // of splitting each row's few records between groups
+      static_assert(NG == kRPW, "one group per row");
+      float4 acc1[NV];
+#pragma unroll
+      for (int qv = 0; qv < NV; ++qv) acc1[qv] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
+        const int s = it % S;
+        mbar_wait(&full[s], (it / S) & 1);
+        const uint8_t* st = smem + s * S_::STAGE;
+        const float4* xs = reinterpret_cast<const float4*>(st) + gl;
+        const int2* nz = reinterpret_cast<const int2*>(st + S_::X_BYTES);
+        const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + S_::NZ_BYTES) + warp * kRPW;
+        const int k1 = ro[hg + 1];
+        int k = ro[hg];
+        for (; k + 1 < k1; k += 2) {
+          const int2 e0 = nz[k], e1 = nz[k + 1];
+          fma_row<NV, G>(acc1, __int_as_float(e0.y), xs + e0.x * pw4);
+          fma_row<NV, G>(acc1, __int_as_float(e1.y), xs + e1.x * pw4);
+        }
+        if (k < k1) {
+          const int2 e = nz[k];
+          fma_row<NV, G>(acc1, __int_as_float(e.y), xs + e.x * pw4);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&empty[s]);
+      }
+      const int r = r0 + hg;
+      if (r < a.nrows) {
+        const float* Xp = a.X + col0;
+        const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
+        for (int64_t k = e0; k < e1; ++k) {
+          const int c = __ldg(a.res_col + k);
+          const float v = __ldg(a.res_val + k);
+          const float4* xr = reinterpret_cast<const float4*>(Xp + (int64_t)c * a.ldx) + gl;
+#pragma unroll
+          for (int qv = 0; qv < NV; ++qv) {
+            if (col0 + (qv * G + gl) * 4 < a.d) {
+              const float4 t4 = __ldg(xr + qv * G);
+              acc1[qv].x = fmaf(v, t4.x, acc1[qv].x); acc1[qv].y = fmaf(v, t4.y, acc1[qv].y);
+              acc1[qv].z = fmaf(v, t4.z, acc1[qv].z); acc1[qv].w = fmaf(v, t4.w, acc1[qv].w);
+            }
+          }
+        }
+        float* y = a.Y + (int64_t)r * a.ldy + col0;
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv) {
+          const int col = (qv * G + gl) * 4;
+          const int rem = a.d - col0 - col;
+          if (rem >= 4) {
+            *reinterpret_cast<float4*>(y + col) = acc1[qv];
+          } else if (rem > 0) {
+            y[col] = acc1[qv].x;
+            if (rem > 1) y[col + 1] = acc1[qv].y;
+            if (rem > 2) y[col + 2] = acc1[qv].z;
+          }
+        }
+      }
+      continue;
+    }
     float4 acc[kRPW][NV];
 #pragma unroll
     for (int i = 0; i < kRPW; ++i)
@@ -284,7 +347,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int NV, int G, int S>
+template <int NV, int G, int S, int MINB = 1>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   using S_ = Smem<NV, G, S>;
   static_assert(S_::TOTAL <= 227 * 1024, "smem");
@@ -304,14 +367,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_tiled_kernel<NV, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         S_::TOTAL);
+    cudaError_t e = cudaFuncSetAttribute(spmm_tiled_kernel<NV, G, S, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
-  const int grid = items < num_sms() ? items : num_sms();
-  if (grid > 0) spmm_tiled_kernel<NV, G, S><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
+  if (grid > 0) spmm_tiled_kernel<NV, G, S, MINB><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -332,8 +395,13 @@ cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* 
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
   a.next_item = work_counter(stream);
   if (!a.next_item) return cudaErrorMemoryAllocation;
-  if (d <= 64) return st::launch_nv<1, 16, 8>(a, xrows, stream);     // 24 KB stages
-  if (d <= 128) return st::launch_nv<1, 32, 5>(a, xrows, stream);    // 40 KB stages
+  // d <= 64: a lane group of 8 lanes per row (4 rows of a warp in parallel),
+  // 2 CTAs per SM; wider panels: HB_TILED_ROWPAR=1 selects the same row-per-
+  // group consumer (8 lanes x NV float4)
+  static const int rowpar = getenv("HB_TILED_ROWPAR") ? atoi(getenv("HB_TILED_ROWPAR")) : 0;
+  if (d <= 64) return st::launch_nv<2, 8, 4, 2>(a, xrows, stream);
+  if (d <= 128) return rowpar ? st::launch_nv<4, 8, 5>(a, xrows, stream) : st::launch_nv<1, 32, 5>(a, xrows, stream);
+  if (rowpar) return st::launch_nv<8, 8, 3>(a, xrows, stream);
   return st::launch_nv<2, 32, 3>(a, xrows, stream);                  // 72 KB stages, 256-column panels
 }
 

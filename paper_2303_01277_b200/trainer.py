@@ -466,9 +466,12 @@ class DeviceRank:
         return self._tiles[key]
 
     def _spmm(self, a, x, y, d: int):
-        """K3/K4: the TMA-staged tiled kernel for wide rows of community-
-        structured blocks, the row-gather kernel otherwise."""
-        t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and d > 128)) else None
+        """K3/K4: the TMA-staged tiled kernel where the matrix has dense
+        (community) blocks, the row-gather kernel otherwise."""
+        # auto: the tiled kernel for wide (> 128) and narrow (<= 64, row-per-
+        # lane-group consumers) panels of community-structured blocks
+        t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and (d > 128 or d <= 64))) \
+            else None
         with self.timer("spmm_tiled" if t is not None else "spmm_rows", *_spmm_cost(a, d)):
             if t is not None:
                 ops.spmm_tiled(t, x, y, d)
