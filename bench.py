@@ -299,6 +299,14 @@ def run_b200(args):
                 "philox_gelem_s": rate, "philox_ceiling_gelem_s": PHILOX_CEILING_GELEM_S,
                 "philox_frac": rate / PHILOX_CEILING_GELEM_S,
                 "note": "bit-exact Philox4x64-10 (one uniform per element) caps K1 below HBM speed"}
+        for k in ("spmm_tiled_narrow", "spmm_rows"):
+            if k in ksum and k != skey:
+                v = ksum[k]
+                sec = v["ms"] / 1e3
+                kroof[k] = {"bound": "hbm", "achieved": v["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": v["gbps"] / peaks["hbm_gbs"],
+                            "gathered_gbps": 2.0 * v["flops"] / sec / 1e9 if sec > 0 else 0.0,
+                            "avg_launch_ms": v["ms"] / v["launches"]}
         for k in ("dequant_gather", "elementwise"):
             if k in ksum:
                 v = ksum[k]

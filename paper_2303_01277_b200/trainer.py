@@ -472,7 +472,8 @@ class DeviceRank:
         # lane-group consumers) panels of community-structured blocks
         t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and (d > 128 or d <= 64))) \
             else None
-        with self.timer("spmm_tiled" if t is not None else "spmm_rows", *_spmm_cost(a, d)):
+        name = "spmm_rows" if t is None else ("spmm_tiled_narrow" if d <= 64 else "spmm_tiled")
+        with self.timer(name, *_spmm_cost(a, d)):
             if t is not None:
                 ops.spmm_tiled(t, x, y, d)
             else:
