@@ -171,6 +171,87 @@ spmm_rows_vec_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32
   }
 }
 
+// Row-parallel variant: each group of G lanes owns one row (32/G rows of a
+// warp in flight at once, no cross-group reduction).  The group reads its
+// row's (col, val) pairs G at a time with one coalesced load and broadcasts
+// them with width-G shuffles; U X rows in flight per group.  Rows come from
+// the same ascending chunk counter as spmm_rows_vec_kernel.
+template <int NV, int G, int U>
+__global__ void __launch_bounds__(kSpWarps * 32)
+spmm_rows_par_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                     const float* __restrict__ vals, const float* __restrict__ X, int64_t ldx, int d,
+                     float* __restrict__ Y, int64_t ldy, int* __restrict__ next_row, int chunk) {
+  constexpr int NG = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
+  const int nwarps = gridDim.x * kSpWarps;
+  int r0 = 0, r1 = 0;
+  for (;;) {
+    int got = 0;
+    if (lane == 0) got = atomicAdd(next_row, chunk);
+    r0 = __shfl_sync(0xffffffffu, got, 0);
+    if (r0 >= nrows) {
+      if (lane == 0 && atomicAdd(next_row + 1, 1) == nwarps - 1) {
+        atomicExch(next_row, 0);
+        atomicExch(next_row + 1, 0);
+      }
+      break;
+    }
+    r1 = min(nrows, r0 + chunk);
+    for (int row = r0 + grp; row < r1; row += NG) {
+      const int64_t start = row_ptr[row], end = row_ptr[row + 1];
+      float4 acc[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t base = start; base < end; base += G) {
+        const int64_t k = base + gl;
+        const int my_c = k < end ? __ldg(col_idx + k) : 0;
+        const float my_v = k < end ? __ldg(vals + k) : 0.f;
+        const int n = (int)min((int64_t)G, end - base);
+        for (int jj = 0; jj < n; jj += U) {
+          int c[U];
+          float v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            c[u] = __shfl_sync(gmask, my_c, (jj + u) % G, G);
+            v[u] = __shfl_sync(gmask, my_v, (jj + u) % G, G);
+          }
+          float4 x[U][NV];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float4* xr = reinterpret_cast<const float4*>(X + (int64_t)c[u] * ldx);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              const int col = (q * G + gl) * 4;
+              x[u][q] = (col >= d || jj + u >= n) ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(xr + q * G + gl);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              acc[q].x = fmaf(v[u], x[u][q].x, acc[q].x); acc[q].y = fmaf(v[u], x[u][q].y, acc[q].y);
+              acc[q].z = fmaf(v[u], x[u][q].z, acc[q].z); acc[q].w = fmaf(v[u], x[u][q].w, acc[q].w);
+            }
+        }
+      }
+      float* y = Y + (int64_t)row * ldy;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int col = (q * G + gl) * 4;
+        if (col + 3 < d) {
+          *reinterpret_cast<float4*>(y + col) = acc[q];
+        } else if (col < d) {
+          y[col] = acc[q].x;
+          if (col + 1 < d) y[col + 1] = acc[q].y;
+          if (col + 2 < d) y[col + 2] = acc[q].z;
+        }
+      }
+    }
+  }
+}
+
 // Generic (unaligned leading dimensions): scalar columns, lane-strided.
 __global__ void __launch_bounds__(kSpWarps * 32)
 spmm_rows_scalar_kernel(int nrows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
@@ -245,6 +326,14 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
     // ~256 nonzeros per grab
     const int64_t avg = nnz > 0 ? (nnz + nrows - 1) / nrows : 32;
     chunk = chunk_env > 0 ? chunk_env : (int)std::max<int64_t>(1, std::min<int64_t>(32, 256 / std::max<int64_t>(1, avg)));
+  }
+  static const int par = getenv("HB_SPMM_PAR") ? atoi(getenv("HB_SPMM_PAR")) : 1;
+  if (vec && dyn && par && d <= 128) {
+    // row-parallel lane groups (chunks rounded to whole groups of rows)
+    const int ch = (chunk + 3) & ~3;
+    if (d <= 64) spmm_rows_par_kernel<2, 8, 4><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, next_row, ch);
+    else spmm_rows_par_kernel<2, 16, 4><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, next_row, ch);
+    return cudaGetLastError();
   }
   if (vec && d <= 1024) {
     const int d4 = (d + 3) / 4;
