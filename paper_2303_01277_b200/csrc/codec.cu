@@ -79,10 +79,17 @@ __device__ __forceinline__ int quant_fast(float x, const QuantRowCtx& q, uint64_
 
 // b = 1: h in [0, 1 + eps]; a non-ambiguous element has floor(h) = 0, so the
 // code is just (u < h).
+// 1 bit: code = clip(floor(hbar) + (u < hbar - floor(hbar)), 0, 1) = (u < hbar)
+// for hbar in [0, 1) and 1 for hbar >= 1.  With |h - hbar| <= E and
+// ut <= u < ut + 2^-23, the fp32 decision (ut < h) can only differ from the
+// exact one when |h - ut| <= Eu = E + 2^-22 — including at the row maximum
+// (hbar ~ 1: ut <= 1 - 2^-23, so ut < h unless they are within Eu) and near
+// the minimum — so that single test routes every undecidable element to the
+// f64 path.
 __device__ __forceinline__ uint32_t quant_fast_b1(float x, const QuantRowCtx& q, uint64_t w, bool& amb) {
   const float h = __fmul_rn(__fsub_rn(x, q.mn), q.inv_s);
   const float ut = __fsub_rn(__uint_as_float(((uint32_t)(w >> 32) >> 9) | 0x3f800000u), 1.0f);
-  amb = (x != q.mn) & ((h <= q.E) | (h >= 1.0f - q.E) | (fabsf(__fsub_rn(h, ut)) <= q.Eu));
+  amb = (x != q.mn) & (fabsf(__fsub_rn(h, ut)) <= q.Eu);
   return ut < h ? 1u : 0u;
 }
 

@@ -150,3 +150,26 @@ def test_dequant_gather_multi_source_exact(d, bits, accumulate):
             acc = acc + recv[src_rows[k]]
         want[t, :d] = acc.astype(np.float32)
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("d", [2, 3, 37])
+def test_one_bit_row_maxima_vs_oracle(d):
+    """1 bit at the row extremes: every row's maximum has hbar = (mx - mn) /
+    f32(mx - mn) within an ulp of 1 (and rows with repeated maxima / ReLU
+    zeros repeat that), the case the fp32 fast decision must hand to the exact
+    path only when the uniform is within the error bound.  Many short rows,
+    wire bytes must equal the oracle's."""
+    from oracle import codec as oc
+    from oracle import rng as orng
+    from paper_2303_01277_b200.codec import QuantConfig, quantize_rows
+    from paper_2303_01277_b200.rngstream import RngStream
+    rows = 120_000 // d
+    rng = np.random.default_rng(77 + d)
+    x = (rng.standard_normal((rows, d)) * rng.uniform(1e-3, 1e3, (rows, 1))).astype(np.float32)
+    x[::5] = np.maximum(x[::5], 0)                       # ties at the minimum
+    x[1::5, : max(1, d // 2)] = x[1::5].max(axis=1, keepdims=True)   # repeated maxima
+    st = RngStream(3, 1, 4, 2, "backward")
+    q = quantize_rows(torch.from_numpy(x).cuda(), QuantConfig(1), st)
+    ost = orng.Stream(3, 1, 4, 2, "backward")
+    rmin, rscale, codes = oc.quantize(x.astype(np.float64), 1, ost.uniforms(rows * d))
+    assert q.to_bytes() == oc.wire_block(rmin, rscale, codes, 1, rows, d)
