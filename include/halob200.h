@@ -96,9 +96,10 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream);
 
 /* K3/K4 row-gather kernel with its knobs exposed: algo 0 = auto, 1 = row
- * gather (one warp, or an 8/16-lane group for d <= 64, per row, several
- * nonzeros in flight); window > 0 = nonzeros kept in flight per lane group
- * (tuning; 0 = default); nnz = stored entries (informational);
+ * gather (rows handed out in ascending chunks; d <= 128: an 8- or 16-lane
+ * group owns a row, wider rows a warp; several nonzeros in flight);
+ * window > 0 = nonzeros kept in flight per warp for d > 128 (tuning; 0 =
+ * default); nnz = stored entries (sizes the row chunks);
  * stream_col: X rows >= stream_col (the halo copies) are referenced a few
  * times each and are read L2-evict-first, like the CSR arrays and Y, so the
  * local rows being aggregated stay L2-resident (INT32_MAX: no hint).  Same
