@@ -323,9 +323,9 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
   if (dyn) {
     next_row = work_counter(st);
     if (!next_row) return cudaErrorMemoryAllocation;
-    // ~256 nonzeros per grab
+    // ~192 nonzeros per grab
     const int64_t avg = nnz > 0 ? (nnz + nrows - 1) / nrows : 32;
-    chunk = chunk_env > 0 ? chunk_env : (int)std::max<int64_t>(1, std::min<int64_t>(32, 256 / std::max<int64_t>(1, avg)));
+    chunk = chunk_env > 0 ? chunk_env : (int)std::max<int64_t>(1, std::min<int64_t>(32, 192 / std::max<int64_t>(1, avg)));
   }
   static const int par = getenv("HB_SPMM_PAR") ? atoi(getenv("HB_SPMM_PAR")) : 1;
   if (vec && dyn && par && d <= 128) {
