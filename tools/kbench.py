@@ -88,7 +88,8 @@ def spmm(args):
     print(json.dumps({"setup_s": time.time() - t0, "NL": lay.NL, "NH": lay.NH, "nnz": A.nnz}), flush=True)
     tiled = {}
     cases = (("A", A, 602), ("A", A, 256), ("At", At, 256), ("A", A, 128), ("At", At, 128), ("A", A, 100),
-             ("A", A, 64), ("A", A, 41), ("At", At, 41), ("A", A, 47), ("At", At, 47))
+             ("A", A, 64), ("A", A, 41), ("At", At, 41), ("A", A, 47), ("At", At, 47), ("A", A, 512),
+             ("At", At, 512), ("A", A, 300))
     if args.d_list:
         cases = tuple(c for c in cases if c[2] in args.d_list)
     for name, M, d in cases:
@@ -97,7 +98,7 @@ def spmm(args):
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
         variants = [("rows", 0)] + ([("tiled", 0)] if args.config == "reddit" else []) + \
-            ([("rows", 4), ("rows", 16)] if d <= 64 else [])
+            ([("rows", 4), ("rows", 16)] if d <= 64 else []) + ([("rows", 1), ("rows", 4)] if d > 256 else [])
         for algo, win in variants:
             if algo == "tiled":
                 if name not in tiled:
