@@ -287,7 +287,10 @@ def run_b200(args):
                     "fp32_simt_tflops": s["tflops"],
                     "l1_datapath": {"gathered_gbps": gather_gbps, "peak_gbps": dp_peak,
                                     "frac": gather_gbps / dp_peak,
-                                    "note": "gather model 4*nnz*d bytes per launch vs 148 SM x 128 B/clk"}}
+                                    "ncu_l1tex_pct_elapsed": _ncu_traffic("spmm_tiled_l1tex_pct_elapsed")
+                                    if skey == "spmm_tiled" else None,
+                                    "note": "gather model 4*nnz*d bytes per launch vs 148 SM x 128 B/clk; the "
+                                            "kernel is bound by this shared-memory datapath, not HBM"}}
         kroof = {}
         if "quantize_gather" in ksum:
             q = ksum["quantize_gather"]
