@@ -343,6 +343,9 @@ def run_b200(args):
                              "K1 writes each wire block straight into its receiver's buffer"},
             "gpu_launches": launches,
             "host_issue_ms_per_step": round(host_issue_ms, 3),
+            "host_issue_note": "wall time to issue an epoch; includes the waits on each exchange's two pinned "
+                               "descriptor slots that keep the host at most two epochs ahead of the GPU "
+                               "(tools/prof_host.py: ~3 ms/epoch of Python + ctypes issue at Reddit shape)",
             "clocks": clocks,
             "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 12},
