@@ -27,8 +27,11 @@ namespace gts {
 
 constexpr int BM = 128;
 constexpr int BK = 32;
-constexpr int kThreads = 320;
-constexpr int kConv0 = 2, kEpi0 = 6;
+// warps: 0 TMA producer, 1 MMA issuer, 2-9 two groups of 4 converter warps
+// (group g takes the k blocks with it % 2 == g, so two blocks are split into
+// TMEM at once), 10-13 epilogue
+constexpr int kThreads = 448;
+constexpr int kConv0 = 2, kEpi0 = 10;
 
 template <int BN>
 struct Cfg {
@@ -260,9 +263,12 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ---------------- split A into TMEM (and B in smem when raw) ----------------
     const int lg = warp & 3;                        // TMEM lanes 32*lg .. +31 = tile rows
     const int r = lg * 32 + lane;                   // this thread's A row within the tile
-    const int ct = threadIdx.x - kConv0 * 32;
+    const int ct = (threadIdx.x - kConv0 * 32) & 127;
+    // the tall kernel measured no faster with two converter groups (the
+    // weight-gradient kernel below is): group 1 idles here
+    const int cg = (warp - kConv0) >> 2;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = (cg == 0 ? blockIdx.x : num_tiles); t < num_tiles; t += gridDim.x) {
       int mi, ni, si;
       tile_coords(p, t, mi, ni, si);
       const int kb0 = si * p.kb_per_split, kb1 = min(p.nkb, kb0 + p.kb_per_split);
@@ -460,7 +466,7 @@ struct DwCfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int CB = BN == 256 ? 3 : 4;                 // B (+ TMEM A slot) stages
-  static constexpr int RA = BN == 256 ? 2 : (BN == 128 ? 3 : 4);  // raw A stages
+  static constexpr int RA = BN == 256 ? 2 : 4;                     // raw A stages
   static constexpr int SMEM = CB * 2 * B_BYTES + RA * A_BYTES + 1024;
   static constexpr uint32_t ACC = BN;
   static_assert(ACC + CB * 64 <= 512, "TMEM budget");
@@ -580,13 +586,21 @@ gemm_dw_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ---------------- converters: A -> TMEM hi/lo, B split in place ----------------
     const int lg = warp & 3;
     const int r = lg * 32 + lane;
-    const int ct = threadIdx.x - kConv0 * 32;
+    const int ct = (threadIdx.x - kConv0 * 32) & 127;
+    // two converter groups alternate k blocks when both rings are even (each
+    // barrier then always has the same group of waiters); otherwise group 1 idles
+    constexpr bool kTwo = (CB % 2 == 0) && (RA % 2 == 0);
+    const int cg = (warp - kConv0) >> 2;
+    if (!kTwo && cg == 1) {
+      // nothing to do
+    } else {
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mi, ni, si;
       tile_coords(p, t, mi, ni, si);
       const int kb0 = si * p.kb_per_split, kb1 = min(p.nkb, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        if (kTwo && (it & 1) != cg) continue;
         const int ra = it % RA, sb = it % CB;
         mbar_wait(&afull[ra], (it / RA) & 1);
         const uint8_t* st = aring + ra * C_::A_BYTES;
@@ -638,6 +652,7 @@ gemm_dw_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         __syncwarp();
         if (lane == 0) mbar_arrive_local(&conv[sb]);
       }
+    }
     }
   } else {
     // ---------------- epilogue: split-K partial (or C with beta / ReLU) ----------------
