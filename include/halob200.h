@@ -165,10 +165,13 @@ int hb_gemm_set_path(int32_t path);
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:
  * grad rows outside the mask are zero, masked rows get (softmax - onehot)/norm;
  * row_loss[i] = -log softmax[label] / norm (0 outside the mask) in f64.
- * *loss_out = fixed-order sum of row_loss (deterministic, one CTA). */
+ * *loss_out = fixed-order sum of row_loss (deterministic two-pass reduction).
+ * keep_unmasked = 1: rows outside the mask are not written (the caller's
+ * grad / row_loss rows there already hold zeros, e.g. from the previous
+ * epoch). */
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
                     const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                    double* loss_out, void* stream);
+                    double* loss_out, int32_t keep_unmasked, void* stream);
 
 /* ReLU epilogue (linalg.py:78-80): y = max(z, 0), in place allowed. */
 int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream);

@@ -14,7 +14,7 @@ cudaError_t launch_philox_uniforms(uint64_t, uint64_t, uint64_t, int64_t, double
 cudaError_t launch_spmm(int, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
                         float*, int64_t, int64_t, int, int, int, cudaStream_t);
 cudaError_t launch_xent(const float*, int64_t, int, int, const int32_t*, const uint8_t*, double, float*,
-                        int64_t, double*, double*, cudaStream_t);
+                        int64_t, double*, double*, int, cudaStream_t);
 cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaStream_t);
 cudaError_t launch_relu_grad_mul(const float*, int64_t, const float*, int64_t, int, int, float*, int64_t,
                                  cudaStream_t);
@@ -165,10 +165,11 @@ int hb_gemm_set_path(int32_t path) {
 
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
                     const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                    double* loss_out, void* stream) {
+                    double* loss_out, int32_t keep_unmasked, void* stream) {
   if (n < 0 || C <= 0 || norm <= 0 || !loss_out || (n > 0 && (!logits || !labels || !mask || !grad || !row_loss)))
     return fail(HB_EINVAL, "hb_softmax_xent: bad arguments");
-  return check(hb::launch_xent(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss, loss_out, S(stream)),
+  return check(hb::launch_xent(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss, loss_out, keep_unmasked,
+                               S(stream)),
                "hb_softmax_xent");
 }
 

@@ -15,12 +15,13 @@ namespace hb {
 __global__ void xent_rows_kernel(const float* __restrict__ logits, int64_t ld, int n, int C,
                                  const int32_t* __restrict__ labels, const uint8_t* __restrict__ mask,
                                  double norm, float* __restrict__ grad, int64_t ldg,
-                                 double* __restrict__ row_loss) {
+                                 double* __restrict__ row_loss, int keep_unmasked) {
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
        row += gridDim.x * (blockDim.x >> 5)) {
     float* g = grad + (int64_t)row * ldg;
     if (!mask[row]) {
+      if (keep_unmasked) continue;         // caller's buffers already hold the zeros
       for (int c = lane; c < C; c += 32) g[c] = 0.f;
       if (lane == 0) row_loss[row] = 0.0;
       continue;
@@ -258,8 +259,10 @@ static int grid_for(int64_t work, int per_block) {
 
 cudaError_t launch_xent(const float* logits, int64_t ld, int n, int C, const int32_t* labels,
                         const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                        double* loss_out, cudaStream_t st) {
-  if (n > 0) xent_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss);
+                        double* loss_out, int keep_unmasked, cudaStream_t st) {
+  if (n > 0)
+    xent_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss,
+                                                     keep_unmasked);
   if (n <= 16 * 1024) {
     sum_f64_kernel<<<1, 256, 0, st>>>(row_loss, n, loss_out);
   } else {

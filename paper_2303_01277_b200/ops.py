@@ -175,11 +175,13 @@ def gemm_set_path(path: int):
     _lib.call("hb_gemm_set_path", int(path))
 
 
-def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None):
-    """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device."""
+def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None,
+                 keep_unmasked: bool = False):
+    """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device.
+    keep_unmasked: grad / row_loss rows outside the mask already hold zeros."""
     n = labels.numel()
     _lib.call("hb_softmax_xent", ptr(logits), logits.stride(0), n, C, ptr(labels), ptr(mask),
-              float(norm), ptr(grad), grad.stride(0), ptr(row_loss), ptr(loss_out),
+              float(norm), ptr(grad), grad.stride(0), ptr(row_loss), ptr(loss_out), int(bool(keep_unmasked)),
               stream_handle(stream))
 
 

@@ -567,8 +567,10 @@ class DeviceRank:
         W, L, NL = self.cfg.widths, self.L, self.NL
         sync_variant = self.mode.variant == "sync"
         C = W[L]
+        # JL / row_loss rows outside the train mask are zero from allocation and
+        # never written: the CE kernel skips them
         ops.softmax_xent(logits, C, self.labels, self.train_mask, self.norm, self.JL,
-                         self.row_loss, self.loss_dev)
+                         self.row_loss, self.loss_dev, keep_unmasked=True)
         self.launches += 2
         J = self.JL
         for l in range(L, 0, -1):

@@ -35,7 +35,7 @@ def test_relu_and_relu_grad_mul(n, d, ld):
     np.testing.assert_array_equal(m[:, :d].cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("n,C", [(5000, 41), (300, 4), (64, 100)])
+@pytest.mark.parametrize("n,C", [(5000, 41), (300, 4), (64, 100), (20000, 47), (700, 160)])
 def test_softmax_xent_matches_oracle(n, C):
     from oracle.epoch import xent
     from paper_2303_01277_b200 import ops
@@ -48,13 +48,22 @@ def test_softmax_xent_matches_oracle(n, C):
     ld = (C + 3) // 4 * 4
     L = torch.zeros(n, ld, device="cuda")
     L[:, :C] = torch.from_numpy(logits).cuda()
-    grad = torch.zeros(n, ld, device="cuda")
-    row_loss = torch.zeros(n, dtype=torch.float64, device="cuda")
+    lab = torch.from_numpy(labels.astype(np.int32)).cuda()
+    msk = torch.from_numpy(mask.astype(np.uint8)).cuda()
+    # the unmasked rows are written (zeros) ...
+    grad = torch.full((n, ld), 5.0, device="cuda")
+    row_loss = torch.full((n,), 3.0, dtype=torch.float64, device="cuda")
     loss = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ops.softmax_xent(L, C, torch.from_numpy(labels.astype(np.int32)).cuda(),
-                     torch.from_numpy(mask.astype(np.uint8)).cuda(), norm, grad, row_loss, loss)
+    ops.softmax_xent(L, C, lab, msk, norm, grad, row_loss, loss)
     assert float(loss) == pytest.approx(loss_ref, rel=1e-6)
     np.testing.assert_allclose(grad[:, :C].cpu().numpy(), grad_ref, atol=1e-7)
+    # ... or kept (keep_unmasked: the trainer's buffers hold zeros there)
+    grad2 = torch.zeros(n, ld, device="cuda")
+    row_loss2 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    loss2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.softmax_xent(L, C, lab, msk, norm, grad2, row_loss2, loss2, keep_unmasked=True)
+    assert float(loss2) == float(loss)
+    assert torch.equal(grad2[:, :C], grad[:, :C])
 
 
 def test_adam_matches_oracle():
