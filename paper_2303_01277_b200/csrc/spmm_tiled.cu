@@ -177,14 +177,16 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
     const int b = item / a.npanels, pn = item % a.npanels;
     const int r0 = b * kTRB + warp * kRPW;
     const int col0 = pn * P;
-    if constexpr (G == 8) {
-      // narrow panels (P = 64): lane group hg (8 lanes x NV float4) owns row
-      // r0 + hg outright, so a warp walks its 4 short rows in parallel instead
-      // of splitting each row's few records between groups
-      static_assert(NG == kRPW, "one group per row");
-      float4 acc1[NV];
+    if constexpr (G < 32 && G * NG == 32 && kRPW % NG == 0 && (G == 8 || NV >= 4)) {
+      // row-parallel consumers: lane group hg (G lanes x NV float4) owns rows
+      // hg, hg + NG, ... of the warp's kRPW rows outright (no cross-group
+      // reduction), so the warp walks NG rows at once
+      constexpr int RPG = kRPW / NG;
+      float4 acc1[RPG][NV];
 #pragma unroll
-      for (int qv = 0; qv < NV; ++qv) acc1[qv] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < RPG; ++i)
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv) acc1[i][qv] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
@@ -192,22 +194,28 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         const float4* xs = reinterpret_cast<const float4*>(st) + gl;
         const int2* nz = reinterpret_cast<const int2*>(st + S_::X_BYTES);
         const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + S_::NZ_BYTES) + warp * kRPW;
-        const int k1 = ro[hg + 1];
-        int k = ro[hg];
-        for (; k + 1 < k1; k += 2) {
-          const int2 e0 = nz[k], e1 = nz[k + 1];
-          fma_row<NV, G>(acc1, __int_as_float(e0.y), xs + e0.x * pw4);
-          fma_row<NV, G>(acc1, __int_as_float(e1.y), xs + e1.x * pw4);
-        }
-        if (k < k1) {
-          const int2 e = nz[k];
-          fma_row<NV, G>(acc1, __int_as_float(e.y), xs + e.x * pw4);
+#pragma unroll
+        for (int i = 0; i < RPG; ++i) {
+          const int rr = hg + i * NG;
+          const int k1 = ro[rr + 1];
+          int k = ro[rr];
+          for (; k + 1 < k1; k += 2) {
+            const int2 e0 = nz[k], e1 = nz[k + 1];
+            fma_row<NV, G>(acc1[i], __int_as_float(e0.y), xs + e0.x * pw4);
+            fma_row<NV, G>(acc1[i], __int_as_float(e1.y), xs + e1.x * pw4);
+          }
+          if (k < k1) {
+            const int2 e = nz[k];
+            fma_row<NV, G>(acc1[i], __int_as_float(e.y), xs + e.x * pw4);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&empty[s]);
       }
-      const int r = r0 + hg;
-      if (r < a.nrows) {
+#pragma unroll
+      for (int i = 0; i < RPG; ++i) {
+        const int r = r0 + hg + i * NG;
+        if (r >= a.nrows) continue;
         const float* Xp = a.X + col0;
         const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
         for (int64_t k = e0; k < e1; ++k) {
@@ -218,8 +226,8 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
           for (int qv = 0; qv < NV; ++qv) {
             if (col0 + (qv * G + gl) * 4 < a.d) {
               const float4 t4 = __ldg(xr + qv * G);
-              acc1[qv].x = fmaf(v, t4.x, acc1[qv].x); acc1[qv].y = fmaf(v, t4.y, acc1[qv].y);
-              acc1[qv].z = fmaf(v, t4.z, acc1[qv].z); acc1[qv].w = fmaf(v, t4.w, acc1[qv].w);
+              acc1[i][qv].x = fmaf(v, t4.x, acc1[i][qv].x); acc1[i][qv].y = fmaf(v, t4.y, acc1[i][qv].y);
+              acc1[i][qv].z = fmaf(v, t4.z, acc1[i][qv].z); acc1[i][qv].w = fmaf(v, t4.w, acc1[i][qv].w);
             }
           }
         }
@@ -229,11 +237,11 @@ spmm_tiled_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
           const int col = (qv * G + gl) * 4;
           const int rem = a.d - col0 - col;
           if (rem >= 4) {
-            *reinterpret_cast<float4*>(y + col) = acc1[qv];
+            *reinterpret_cast<float4*>(y + col) = acc1[i][qv];
           } else if (rem > 0) {
-            y[col] = acc1[qv].x;
-            if (rem > 1) y[col + 1] = acc1[qv].y;
-            if (rem > 2) y[col + 2] = acc1[qv].z;
+            y[col] = acc1[i][qv].x;
+            if (rem > 1) y[col + 1] = acc1[i][qv].y;
+            if (rem > 2) y[col + 2] = acc1[i][qv].z;
           }
         }
       }
@@ -401,7 +409,8 @@ cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* 
   static const int rowpar = getenv("HB_TILED_ROWPAR") ? atoi(getenv("HB_TILED_ROWPAR")) : 0;
   if (d <= 64) return st::launch_nv<2, 8, 4, 2>(a, xrows, stream);
   if (d <= 128) return rowpar ? st::launch_nv<4, 8, 5>(a, xrows, stream) : st::launch_nv<1, 32, 5>(a, xrows, stream);
-  if (rowpar) return st::launch_nv<8, 8, 3>(a, xrows, stream);
+  if (rowpar == 1) return st::launch_nv<8, 8, 3>(a, xrows, stream);
+  if (rowpar == 2) return st::launch_nv<4, 16, 3>(a, xrows, stream);
   return st::launch_nv<2, 32, 3>(a, xrows, stream);                  // 72 KB stages, 256-column panels
 }
 
