@@ -1,6 +1,7 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck):
-one epoch of each model on a small graph (K1, K2, both SpMM kernels, tcgen05
-GEMMs, K8) plus a tiled SpMM and a split-K GEMM."""
+a few epochs of each model on a small graph (K1, K2, both SpMM kernels,
+tcgen05 GEMMs, K8) plus wide and narrow tiled SpMM, the row-parallel gather,
+dual / ReLU-only tall GEMMs and a split-K weight-gradient GEMM."""
 import sys
 from pathlib import Path
 
@@ -28,6 +29,18 @@ def main():
         X = torch.randn(eng.A.cols, 256, device="cuda")
         Y = torch.zeros(eng.A.rows, 256, device="cuda")
         ops.spmm_tiled(T, X, Y, 256)
+        ops.spmm_tiled(T, X, Y, 40)                       # narrow: a lane group per row
+        ops.spmm(eng.A, X, Y, 100)                        # row-parallel gather (d <= 128)
+    # tall GEMMs: dual operand, ReLU-only output, TMA-store epilogue
+    H = torch.randn(20000, 100, device="cuda")
+    AG = torch.randn(20000, 100, device="cuda")
+    W = torch.randn(200, 128, device="cuda")
+    Z = torch.empty(20000, 128, device="cuda")
+    R = torch.empty(20000, 128, device="cuda")
+    wsb = torch.empty(1 << 20, device="cuda")
+    ops.gemm2(H, W[:100], AG, W[100:], Z, relu_out=R, ws=wsb)
+    ops.gemm2(H, W[:100], AG, W[100:], None, relu_out=R, ws=wsb)
+    ops.gemm(H, W[:100], Z, relu_out=R, ws=wsb)
     A = torch.randn(5000, 300, device="cuda")
     m = torch.randn(5000, 64, device="cuda")
     G = torch.empty(300, 64, device="cuda")
