@@ -15,6 +15,12 @@
 // swizzled 16-byte chunks), MN-major ones from the SW128_BASE32B layout
 // (column reads), which also transposes them into the K-major order TMEM A
 // requires.
+//
+// The epilogue releases the accumulator after its last tcgen05.ld and writes
+// C (and/or the ReLU copy) through swizzled smem chunks and TMA bulk stores.
+// A dual GEMM C = A1 B1 + A2 B2 runs both K ranges through the same ring
+// (tmA2 / tmB2 for k blocks >= nkb1).  gemm_dw_kernel (below) is the
+// split-K weight-gradient variant with decoupled A / B rings.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -27,9 +33,10 @@ namespace gts {
 
 constexpr int BM = 128;
 constexpr int BK = 32;
-// warps: 0 TMA producer, 1 MMA issuer, 2-9 two groups of 4 converter warps
-// (group g takes the k blocks with it % 2 == g, so two blocks are split into
-// TMEM at once), 10-13 epilogue
+// warps: 0 TMA producer, 1 MMA issuer, 2-9 two groups of 4 converter warps,
+// 10-13 epilogue.  The weight-gradient kernel runs both converter groups (group
+// g takes the k blocks with it % 2 == g, so two blocks are split into TMEM at
+// once); the tall kernel measured no faster that way and leaves group 1 idle.
 constexpr int kThreads = 448;
 constexpr int kConv0 = 2, kEpi0 = 10;
 
