@@ -339,8 +339,12 @@ def run_b200(args):
             "halo": {"wire_bytes_per_epoch": wire,
                      "k1_k2_ms_per_epoch": halo_ms / args.steps,
                      "fp32_equiv_bytes_per_epoch": _fp32_equiv(eng),
-                     "note": "N=1: the 8 partitions share one GPU, so halo messages move HBM->HBM; "
-                             "K1 writes each wire block straight into its receiver's buffer"},
+                     "note": ("N=1: the 8 partitions share one GPU, so halo messages move HBM->HBM; "
+                              "K1 writes each wire block straight into its receiver's buffer") if world == 1 else
+                             ("rank 0's wire bytes; same-rank messages are written straight into the receiver's "
+                              "buffer, the rest move per peer rank over " +
+                              ("gloo with host staging (--share-gpu: all ranks on one GPU)" if args.share_gpu
+                               else "NCCL send/recv on the comm stream"))},
             "gpu_launches": launches,
             "host_issue_ms_per_step": round(host_issue_ms, 3),
             "host_issue_note": "wall time to issue an epoch; includes the waits on each exchange's two pinned "
