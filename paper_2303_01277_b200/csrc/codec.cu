@@ -1276,12 +1276,32 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
     prepare(w0, s1);
     float4 cur[NCH];
     load_row(__shfl_sync(0xffffffffu, my_t, 0), cur);
+    // the first source's payload bits of the next row are fetched while the
+    // current row accumulates (most destinations have a single source)
+    auto first_bits = [&](int jj, uint32_t (&nb)[NCH]) -> bool {
+      const int ka = __shfl_sync(0xffffffffu, my_k0, jj), kb = __shfl_sync(0xffffffffu, my_k1, jj);
+      if (!(ka < kb && ka >= w0 && ka < w0 + 32)) return false;      // warp-uniform
+      const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, ka - w0));
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        nb[ch] = c0 < d ? (uint32_t)(__ldg(pay + (c0 >> 3)) >> (c0 & 7)) : 0u;
+      }
+      return true;
+    };
+    uint32_t nib_cur[NCH];
+    bool have_cur = first_bits(0, nib_cur);
     for (int j = 0; j < n; ++j) {
       const int t = __shfl_sync(0xffffffffu, my_t, j);
       const int tn = __shfl_sync(0xffffffffu, my_t, (j + 1) & 31);
       const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
       float4 nxt[NCH];
-      if (j + 1 < n) load_row(tn, nxt);
+      uint32_t nib_nxt[NCH];
+      bool have_nxt = false;
+      if (j + 1 < n) {
+        load_row(tn, nxt);
+        have_nxt = first_bits(j + 1, nib_nxt);
+      }
       double acc[NCH][4];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
@@ -1298,11 +1318,12 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
         const double sc = (double)__shfl_sync(0xffffffffu, my_sc, sl);
         const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, sl));
         const double v0 = __dadd_rn(__dmul_rn(sc, 0.0), mn), v1 = __dadd_rn(__dmul_rn(sc, 1.0), mn);
+        const bool pre = have_cur && k == k0;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           const int c0 = ch * 128 + 4 * lane;
           if (c0 >= d) continue;
-          const uint32_t nib = (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+          const uint32_t nib = pre ? nib_cur[ch] : (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[ch][e] = __dadd_rn(acc[ch][e], ((nib >> e) & 1u) ? v1 : v0);
         }
@@ -1324,7 +1345,11 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
       }
       if (j + 1 < n) {
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) cur[ch] = nxt[ch];
+        for (int ch = 0; ch < NCH; ++ch) {
+          cur[ch] = nxt[ch];
+          nib_cur[ch] = nib_nxt[ch];
+        }
+        have_cur = have_nxt;
       }
     }
   }
