@@ -1085,11 +1085,20 @@ dequant_b1_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int
       const float mn = __shfl_sync(0xffffffffu, my_mn, j);
       const float one = __shfl_sync(0xffffffffu, my_one, j);
       const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, j));
+      // all of the row's payload bytes are loaded before the first store (a
+      // byte pointer may alias the fp32 stores, so the compiler would
+      // otherwise serialise one load latency per 128-column chunk)
+      uint32_t bits[NCH];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 128 + 4 * lane;
+        bits[ch] = c0 < d ? (uint32_t)__ldg(pay + (c0 >> 3)) : 0u;
+      }
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         const int c0 = ch * 128 + 4 * lane;
         if (c0 >= d) continue;
-        const uint32_t nib = (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+        const uint32_t nib = bits[ch] >> (c0 & 7);
         const float4 v = make_float4((nib & 1u) ? one : mn, (nib & 2u) ? one : mn, (nib & 4u) ? one : mn,
                                      (nib & 8u) ? one : mn);
         if (vec && c0 + 3 < d) {
