@@ -323,6 +323,14 @@ def run_b200(args):
                              "frac": 3.0 * g["tflops"] / tf32_peak,
                              "note": "3xTF32 (hi*hi + hi*lo + lo*hi per fp32 product); peak = dense TF32 = "
                                      "measured bf16 / 2"}
+        if dom == "gemm" and "gemm" in kroof and roof is not None:
+            # the GEMMs dominate (e.g. the Yelp-shaped GCN): the headline roofline
+            # is theirs; the SpMM's moves to kernel_rooflines
+            kroof[skey] = roof
+            g = ksum["gemm"]
+            roof = dict(kroof.pop("gemm"), kernel="hb_gemm_f32 / hb_gemm2_f32 (K5-K7, tcgen05 3xTF32)",
+                        traffic=_ncu_traffic("gemm"), avg_launch_ms=g["ms"] / g["launches"],
+                        peak_source=peaks["source"])
         wire = sum(b.wire_bytes_total() for b in list(eng.xf.values()) + list(eng.xb.values()))
         halo_ms = sum(ksum.get(k, {}).get("ms", 0.0) for k in ("quantize_gather", "dequant_gather"))
         line = {
