@@ -280,14 +280,14 @@ def run_b200(args):
             roof = {"kernel": {"spmm_tiled": "hb_spmm_tiled (K3/K4, TMA-staged tiles)",
                                "spmm_rows": "hb_spmm_csr_ex (K3/K4, row gather)"}[skey], "bound": "hbm",
                     "achieved": s["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": _ncu_traffic(skey),
+                    "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": _ncu_traffic(skey, args),
                     "algorithmic_bytes_per_launch": s["bytes"] / s["launches"],
                     "algorithmic_bytes_model": "compulsory: CSR + each X row once + Y once (SURVEY 8d)",
                     "avg_launch_ms": s["ms"] / s["launches"], "peak_source": peaks["source"],
                     "fp32_simt_tflops": s["tflops"],
                     "l1_datapath": {"gathered_gbps": gather_gbps, "peak_gbps": dp_peak,
                                     "frac": gather_gbps / dp_peak,
-                                    "ncu_l1tex_pct_elapsed": _ncu_traffic("spmm_tiled_l1tex_pct_elapsed")
+                                    "ncu_l1tex_pct_elapsed": _ncu_traffic("spmm_tiled_l1tex_pct_elapsed", args)
                                     if skey == "spmm_tiled" else None,
                                     "note": "gather model 4*nnz*d bytes per launch vs 148 SM x 128 B/clk; the "
                                             "kernel is bound by this shared-memory datapath, not HBM"}}
@@ -329,7 +329,7 @@ def run_b200(args):
             kroof[skey] = roof
             g = ksum["gemm"]
             roof = dict(kroof.pop("gemm"), kernel="hb_gemm_f32 / hb_gemm2_f32 (K5-K7, tcgen05 3xTF32)",
-                        traffic=_ncu_traffic("gemm"), avg_launch_ms=g["ms"] / g["launches"],
+                        traffic=_ncu_traffic("gemm", args), avg_launch_ms=g["ms"] / g["launches"],
                         peak_source=peaks["source"])
         wire = sum(b.wire_bytes_total() for b in list(eng.xf.values()) + list(eng.xb.values()))
         halo_ms = sum(ksum.get(k, {}).get("ms", 0.0) for k in ("quantize_gather", "dequant_gather"))
@@ -394,7 +394,11 @@ def _fp32_equiv(eng) -> int:
     return tot
 
 
-def _ncu_traffic(kernel: str):
+def _ncu_traffic(kernel: str, args=None):
+    """ncu-measured values of the full-scale Reddit-shaped epoch (the capture in
+    profiles/ncu_traffic.json); None for other workloads."""
+    if args is not None and (args.config != "reddit" or args.scale != 1.0):
+        return None
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
