@@ -37,7 +37,8 @@ sys.path.insert(0, str(ROOT))
 WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (300, 512, 512, 512, 100)}
 MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn"}
 PARTITIONS = 8
-CPU_SAMPLE_SCALE = 0.125       # the CPU oracle runs the same shape at 1/8 of the nodes/edges
+CPU_SAMPLE_SCALE = 0.125       # oracle-port fallback only (no baseline/_ref): 1/8 of the nodes/edges
+REF_EPOCHS = 2                 # timed halobit.train epochs per reference measurement (after 1 warm-up)
 # Bit-exact Philox4x64-10 throughput of the B200 at full occupancy (uniforms/s,
 # tools/probes/philox_probe.cu measured on the GPU box; profiles/ has the run)
 PHILOX_CEILING_GELEM_S = 414.0
@@ -118,9 +119,72 @@ class ClockSampler:
                 "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("", "[N/A]"))}
 
 
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _halobit():
+    """The unmodified reference package installed into baseline/_ref (pip
+    --target); None when it is absent."""
+    if not (REF_DIR / "halobit" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import halobit  # noqa: F401
+    from halobit import trainer
+    return trainer
+
+
+class _MaskOnlyGraph:
+    """``halobit.train`` reads ``graph.train_mask`` (the global CE normaliser,
+    trainer.py:392); the full graph itself only feeds the centralized
+    ``evaluate``, which is excluded from the timed epoch."""
+
+    def __init__(self, train_mask):
+        self.train_mask = train_mask
+
+
+def _to_halobit_partition(p, hb_graph, hb_linalg):
+    def csr(m):
+        if m is None:
+            return None
+        return hb_linalg.CsrMatrix(m.rows, m.cols, np.asarray(m.row_ptr, np.int64),
+                                   np.asarray(m.col_idx, np.int64), np.asarray(m.values, np.float64))
+    return hb_graph.Partition(
+        id=p.id, num_partitions=p.num_partitions, local_nodes=p.local_nodes, halo_nodes=p.halo_nodes,
+        send_sets=list(p.send_sets), recv_sets=list(p.recv_sets), adj_block=csr(p.adj_block),
+        mean_block=csr(p.mean_block), features=np.asarray(p.features, dtype=np.float64),
+        labels=p.labels, train_mask=p.train_mask, val_mask=p.val_mask, test_mask=p.test_mask)
+
+
+def reference_epochs(name: str, parts: dict, train_mask, bits: int, mode: str, staleness: int,
+                     epochs: int, seed: int):
+    """``halobit.train`` (trainer.py:386-465, one worker thread per partition)
+    on the bench's own partitions for `epochs` epochs; returns (per-epoch ms,
+    metrics).  The centralized full-graph evaluation (and the full-graph
+    Â / M it needs, trainer.py:392-394) is stubbed out for the run: SURVEY
+    8(d) times the training epoch without it."""
+    ht = _halobit()
+    if ht is None:
+        return None
+    from halobit import codec as hc, graph as hg, linalg as hl
+    hparts = [_to_halobit_partition(parts[k], hg, hl) for k in sorted(parts)]
+    saved = (ht.evaluate, ht.normalize_adjacency, ht.mean_adjacency)
+    ht.evaluate = lambda *a, **k: {"train_acc": 0.0, "val_acc": 0.0, "test_acc": 0.0}
+    ht.normalize_adjacency = lambda *a, **k: None
+    ht.mean_adjacency = lambda *a, **k: None
+    try:
+        res = ht.train(_MaskOnlyGraph(np.asarray(train_mask, bool)), hparts,
+                       ht.ModelConfig(WIDTHS[name], MODEL[name]), ht.TrainMode(mode, staleness),
+                       hc.QuantConfig(bits), epochs, seed, timeout=3600.0)
+    finally:
+        ht.evaluate, ht.normalize_adjacency, ht.mean_adjacency = saved
+    return list(res.timings_ms), res.metrics
+
+
 def cpu_epoch_sample(name: str, threads: int, epochs: int = 1, warmup: int = 0):
-    """Oracle epochs on the same-shape graph at CPU_SAMPLE_SCALE; returns
-    (seconds per full-scale epoch, sample description, cores)."""
+    """Fallback when baseline/_ref is absent: the numpy oracle port on the
+    same-shape graph at CPU_SAMPLE_SCALE; returns (seconds per epoch of the
+    sample, sample description, times, scale)."""
     from oracle.epoch import OracleTrainer
     g, parts = build_graph(name, CPU_SAMPLE_SCALE)
     o = OracleTrainer([parts[k] for k in sorted(parts)], WIDTHS[name], MODEL[name], "sync", 0, 1, 0,
@@ -133,25 +197,66 @@ def cpu_epoch_sample(name: str, threads: int, epochs: int = 1, warmup: int = 0):
         o.run_epoch(e)
         times.append(time.perf_counter() - t0)
     nnz = sum(p.mean_block.nnz if p.mean_block is not None else p.adj_block.nnz for p in parts.values())
-    per = statistics.mean(times) / CPU_SAMPLE_SCALE
+    per = statistics.mean(times)
     sample = (f"{epochs} oracle epoch(s) (numpy/scipy f64, {threads} worker threads) of the {name}-shaped "
               f"graph at {CPU_SAMPLE_SCALE:g} scale ({g.num_nodes} nodes, {len(g.edges)} edges, "
-              f"{nnz} aggregation nnz, same widths/partitions/cut), time x {1 / CPU_SAMPLE_SCALE:g}")
-    return per, sample, times
+              f"{nnz} aggregation nnz, same widths/partitions/cut); NOT extrapolated")
+    return per, sample, times, CPU_SAMPLE_SCALE
+
+
+def _cpu_info() -> dict:
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"cpu_count": os.cpu_count(), "affinity": aff,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def reference_line(args, parts=None, train_mask=None, epochs=REF_EPOCHS):
+    """The reference's own CPU implementation on this workload: ``halobit.train``
+    from baseline/_ref at full scale (one warm-up epoch + `epochs` timed
+    epochs).  Returns the cpu_baseline dict (value = mean timed epoch, s)."""
+    if _halobit() is not None:
+        t0 = time.perf_counter()
+        if parts is None:
+            g, parts = build_graph(args.config, args.scale)
+            train_mask = g.train_mask
+            del g
+        setup = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        ms, _ = reference_epochs(args.config, parts, train_mask, args.bits, args.mode, args.staleness,
+                                 1 + epochs, args.seed)
+        run = time.perf_counter() - t1
+        timed = ms[1:]
+        per = statistics.mean(timed) / 1e3
+        return {"value": per, "unit": "s", "cores": os.cpu_count(), "kind": "reference",
+                "sample": (f"halobit.train (baseline/_ref, unmodified reference, f64, {PARTITIONS} partition "
+                           f"worker threads + OpenBLAS) on the {'full-scale ' if args.scale == 1.0 else ''}{args.config}-shaped graph "
+                           f"(scale {args.scale:g}), {len(timed)} timed epoch(s) after 1 warm-up epoch, "
+                           f"centralized evaluate stubbed out"),
+                "epochs_ms": [round(x, 1) for x in ms], "timed_epochs": len(timed),
+                "scale": args.scale, "setup_s": round(setup, 1), "train_call_s": round(run, 1),
+                "host": _cpu_info()}
+    threads = os.cpu_count() or 1
+    per, sample, times, scale = cpu_epoch_sample(args.config, threads, epochs=epochs, warmup=1)
+    return {"value": per, "unit": "s", "cores": threads, "kind": "port", "sample": sample,
+            "timed_epochs": len(times), "scale": scale, "host": _cpu_info()}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    per, sample, times = cpu_epoch_sample(args.config, threads, epochs=args.steps, warmup=args.warmup)
+    cb = reference_line(args, epochs=min(args.steps, REF_EPOCHS))
+    per = cb["value"]
+    cfg = workload_config(args)
+    cfg["scale"] = cb["scale"]
     line = {
         "impl": "reference", "metric": "full-graph epoch time", "value": per, "unit": "s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "n_gpus": args.gpus, "steps": cb["timed_epochs"], "warmup": 1,
+        "requested": {"steps": args.steps, "warmup": args.warmup},
+        "ms_per_step": per * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args),
-        "cpu_baseline": {"value": per, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": cb,
         "e2e": {"value": per, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,6 +304,7 @@ def run_b200(args):
     t0 = time.perf_counter()
     g, parts = build_graph(args.config, args.scale, mine)
     gnorm = int(g.train_mask.sum())
+    train_mask = g.train_mask
     layout = RankLayout(parts, owner, rank)
     eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config]),
                      TrainMode(args.mode, args.staleness), QuantConfig(args.bits), args.seed, 0.01, gnorm,
@@ -365,10 +471,7 @@ def run_b200(args):
             "final_loss": eng.epoch_loss,
         }
         if world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            per, sample, _ = cpu_epoch_sample(args.config, threads)
-            line["cpu_baseline"] = {"value": per, "unit": "s", "cores": threads, "kind": "port",
-                                    "sample": sample}
+            line["cpu_baseline"] = reference_line(args, parts, train_mask, epochs=1)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -261,7 +261,9 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
   const int gm = (M + kGM - 1) / kGM, gn = (N + BN - 1) / BN;
   int splits = 1;
   const int ctas = gm * gn;
-  if (ws != nullptr && ctas < num_sms() && K >= 4 * kGK) {
+  // split-K reduces into C without the ReLU copy: keep one split when a
+  // ReLU output is requested
+  if (ws != nullptr && relu_out == nullptr && ctas < num_sms() && K >= 4 * kGK) {
     splits = num_sms() / ctas;
     const int max_by_k = (K + 4 * kGK - 1) / (4 * kGK);
     if (splits > max_by_k) splits = max_by_k;
@@ -285,7 +287,6 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
     splitk_reduce_kernel<<<g, 256, 0, st>>>(ws, splits, M, N, C, ldc, beta);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (relu_out) return cudaErrorInvalidValue;  // relu epilogue is not supported with split-K
   }
   return cudaSuccess;
 }

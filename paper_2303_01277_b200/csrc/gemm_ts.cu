@@ -778,7 +778,9 @@ static cudaError_t launch_ts_bn(int M, int N, int K1, const float* A1, int64_t l
   const int sms = num_sms();
   int splits = 1;
   const int tiles = p.mt * p.nt;
-  if (!dual && ws != nullptr && tiles < sms && p.nkb >= 8) {
+  // split-K needs C for the reduction: a ReLU-only store (C == nullptr) keeps
+  // one split
+  if (!dual && C != nullptr && ws != nullptr && tiles < sms && p.nkb >= 8) {
     splits = sms / tiles;
     if (splits > p.nkb / 4) splits = p.nkb / 4;
     const int64_t by_ws = ws_floats / ((int64_t)M * N);

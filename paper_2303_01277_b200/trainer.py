@@ -311,7 +311,7 @@ class DeviceRank:
                 quantize_gather(src, bufs.plan.dev["send_rows"], segs, bufs.n_send, bufs.d,
                                 bufs.bits, self.flags)
             self.launches += 1
-            if self.probe:
+            if self.probe and count:      # the evaluation forward is centralized in the reference: no events
                 self._probe_out(bufs, epoch, layer)
         if self.world > 1:
             ev = torch.cuda.current_stream().record_event()
@@ -562,6 +562,21 @@ class DeviceRank:
             self.probe("halo_consumed", part=p.id, epoch=epoch, layer=layer, phase=FORWARD,
                        tag=tag, data=data)
 
+    def _probe_grads(self, bufs, parity, epoch, layer, tag):
+        """Sylvie-A backward 'halo_consumed' (trainer.py:333-337): the stale
+        per-peer gradient rows each hosted partition integrates, decoded from
+        the wire blocks in its receive buffer."""
+        from .codec import QuantizedBlock, dequantize_rows, wire_bytes
+        raw = bufs.recv[parity]
+        per = {q: {} for q in self.layout.ids}
+        for m in bufs.plan.recv_msgs:
+            o = bufs.recv_off[(m.src, m.dst)]
+            blk = raw[o:o + wire_bytes(m.rows, bufs.d, bufs.bits)].cpu().numpy().tobytes()
+            per[m.dst][m.src] = dequantize_rows(QuantizedBlock.from_bytes(blk))
+        for q in self.layout.ids:
+            self.probe("halo_consumed", part=q, epoch=epoch, layer=layer, phase=BACKWARD, tag=tag,
+                       data=per[q])
+
     def backward(self, epoch: int, epoch_mode: str, logits):
         torch = self.torch
         W, L, NL = self.cfg.widths, self.L, self.NL
@@ -599,8 +614,10 @@ class DeviceRank:
                 self.slots[(l, BACKWARD)] = epoch
             else:
                 if epoch > 1:
-                    self._consume(epoch, l, BACKWARD)
+                    tag = self._consume(epoch, l, BACKWARD)
                     self._recv(bufs, (epoch - 1) % 2, JF, True)
+                    if self.probe:
+                        self._probe_grads(bufs, (epoch - 1) % 2, epoch, l, tag)
                 self._send(bufs, JF, epoch, l, epoch % 2, defer=True)
                 self.slots[(l, BACKWARD)] = epoch
             J = JF[:NL]

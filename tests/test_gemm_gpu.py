@@ -221,3 +221,35 @@ def test_relu_only_store():
     ops.gemm(A1, W[:K], None, relu_out=R2, ws=ws)
     ops.gemm(A1, W[:K], Z, ws=ws)
     assert torch.equal(R2, torch.clamp(Z, min=0))
+
+
+@pytest.mark.parametrize("M,K,N", [(2000, 512, 256), (1500, 1204, 256), (700, 256, 41)])
+def test_relu_only_store_small_m_long_k(M, K, N):
+    """C = NULL on shapes where split-K would be chosen (tiles < SMs, many K
+    blocks): the launcher must keep one split and store only the ReLU copy."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + K + N)
+    Kp, Np = (K + 3) // 4 * 4, (N + 3) // 4 * 4
+    A = torch.randn(M, Kp, device="cuda", generator=g)[:, :K]
+    W = torch.randn(K, Np, device="cuda", generator=g)[:, :N]
+    ws = torch.empty(64 * K * Np, device="cuda")
+    R = torch.full((M, Np), 3.0, device="cuda")
+    ops.gemm(A, W, None, relu_out=R[:, :N], ws=ws)
+    Z = torch.empty(M, N, device="cuda")
+    ops.gemm(A, W, Z, ws=ws)
+    _check(A, W, Z)
+    assert torch.equal(R[:, :N], torch.clamp(Z, min=0))
+
+
+def test_simt_split_k_relu_out(gemm_path):
+    """SIMT-staged path with a ReLU copy on a small-M, long-K shape: C and the
+    ReLU copy both written (split-K is not taken when relu_out is set)."""
+    from paper_2303_01277_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(23)
+    A, B = _pad(600, 1024, g), _pad(1024, 64, g)
+    C = torch.empty(600, 64, device="cuda")
+    R = torch.full((600, 64), 7.0, device="cuda")
+    ws = torch.empty(64 * 600 * 64, device="cuda")
+    ops.gemm(A, B, C, ws=ws, relu_out=R)
+    _check(A, B, C)
+    assert torch.equal(R, torch.clamp(C, min=0))

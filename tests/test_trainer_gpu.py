@@ -163,13 +163,25 @@ def test_async_epoch_one_zero_halo_and_tags():
         if event == "halo_consumed":
             consumed.append(kw)
     train(g, parts, ModelConfig((32, 8, 4)), TrainMode("async", 0), QuantConfig(1), 5, 10, probe=probe)
-    assert consumed
-    for e in consumed:
+    fwd = [e for e in consumed if e["phase"] == "forward"]
+    bwd = [e for e in consumed if e["phase"] == "backward"]
+    assert fwd and bwd
+    for e in fwd:
         if e["epoch"] == 1:
             assert e["tag"] == 0
             np.testing.assert_array_equal(e["data"], 0.0)
         else:
             assert e["tag"] == e["epoch"] - 1
+    # backward (trainer.py:333-337): only from epoch 2, one decoded matrix per
+    # sending peer, shaped like the receiver's send set S_k to that peer
+    by_part = {p.id: p for p in parts}
+    assert {e["epoch"] for e in bwd} == {2, 3, 4, 5}
+    for e in bwd:
+        assert e["tag"] == e["epoch"] - 1 and e["layer"] == 2
+        p = by_part[e["part"]]
+        assert set(e["data"]) == {k for k in range(4) if k != p.id and len(p.send_sets[k])}
+        for k, rows in e["data"].items():
+            assert rows.shape == (len(p.send_sets[k]), 32) and np.isfinite(rows).all()
 
 
 def test_unit_staleness_collapses_to_sync():
@@ -285,3 +297,15 @@ def test_reddit_shaped_small_accuracy_vs_oracle():
         logits = full_forward(np.asarray(g.features, np.float64), a, o.weights, "sage", m)
         ref.append(accuracies(logits, g.labels, (g.train_mask, g.val_mask, g.test_mask))["test_acc"])
     assert abs(np.mean(dev) - np.mean(ref)) <= 0.005, (dev, ref)
+
+
+@pytest.mark.parametrize("model", ["gcn", "sage"])
+def test_wide_hidden_small_graph_pre_order(model):
+    """256-wide hidden layers on a graph with few local rows, pre order: the
+    hidden layers' GEMMs store only relu(z) (C = NULL) on small-M / long-K
+    shapes where the launcher would otherwise pick split-K."""
+    g = _graph(seed=21, npc=250, d=300)
+    res, o, losses, _ = _run_both(g, 1, (300, 256, 256, 4), model, "sync", 0, 32, 4, 5, agg_order="pre")
+    for m, lo in zip(res.metrics, losses):
+        assert m.train_loss == pytest.approx(lo, rel=5e-5)
+    assert _wdiff(res.final_weights, o.weights) < 1e-4
