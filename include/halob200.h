@@ -14,8 +14,9 @@
  *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
  *     and returns 0 on success or a negative HB_E* code; hb_last_error()
  *     returns a thread-local message for the last failure.
- *   - No call allocates persistent device memory; the caller (PyTorch) owns
- *     every buffer.
+ *   - No call allocates device memory; the caller (PyTorch) owns every
+ *     buffer, scratch included (`work` counter pairs, xent partials, the
+ *     column-scaled X copy of hb_spmm_tiled_bin).
  */
 #ifndef HALOB200_H_
 #define HALOB200_H_
@@ -40,6 +41,9 @@ extern "C" {
  * bits == 32 (passthrough): header + rows*dim fp32 (the accounting basis,
  * codec.py:110-114).                                                         */
 #define HB_HEADER_BYTES 12
+
+/* Doubles of caller scratch hb_softmax_xent needs for n > 16384 rows. */
+#define HB_XENT_PARTIALS 256
 
 /* One message = one (source partition -> destination partition) block of an
  * exchange (transport.py:184-192).  40 bytes, 8-byte aligned. */
@@ -102,11 +106,14 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
  * default); nnz = stored entries (sizes the row chunks);
  * stream_col: X rows >= stream_col (the halo copies) are referenced a few
  * times each and are read L2-evict-first, like the CSR arrays and Y, so the
- * local rows being aggregated stay L2-resident (INT32_MAX: no hint).  Same
- * result contract as hb_spmm_csr. */
+ * local rows being aggregated stay L2-resident (INT32_MAX: no hint).
+ * work: a device pair of int32 {next row chunk, warps finished}, zero on
+ * entry and left at zero (one pair per stream serves every launch, graph
+ * replays included); NULL = static grid-stride row schedule.  Same result
+ * contract as hb_spmm_csr. */
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
-                   int32_t window, int32_t stream_col, void* stream);
+                   int32_t window, int32_t stream_col, int32_t* work, void* stream);
 
 /* K3/K4 tiled path (same result contract as hb_spmm_csr, fp32 accumulation
  * in tile-then-residual order).  The matrix is pre-split (ops.TiledCsr, built
@@ -118,11 +125,30 @@ int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx
  * tile_rowoff[t*72 .. +65) the records' row offsets — and a residual CSR
  * (res_ptr / res_col / res_val over all nrows) for every other nonzero.
  * X windows (64 rows x 128/256-column panels) are staged in shared memory by
- * TMA; xrows = rows of X.  X and Y rows must be 16-byte aligned. */
+ * TMA; xrows = rows of X.  X and Y rows must be 16-byte aligned.  work: the
+ * (row block, panel) item counter pair, as hb_spmm_csr_ex (required). */
 int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
                   const int64_t* tile_off, const uint16_t* tile_rowoff, const void* tile_nz, const int64_t* res_ptr,
                   const int32_t* res_col, const float* res_val, const float* X, int64_t ldx, int32_t d, float* Y,
-                  int64_t ldy, void* stream);
+                  int64_t ldy, int32_t* work, void* stream);
+
+/* K3/K4 factored tiled path for the trainer's aggregation operators, whose
+ * values are diagonal scalings of a 0/1 pattern (graph.py:120-141: SAGE mean
+ * D^-1 A, its transpose A^T D^-1, GCN D^-1/2 (A+I) D^-1/2):
+ *   Y[i, 0:d) = r[i] * sum_{(i,j) in pattern} c[j] * X[j, 0:d)
+ * row_scale r / col_scale c may each be NULL (= 1).  Tiles are 128 rows x 64
+ * columns (nblocks = ceil(nrows / 128)); a record is one byte, the column
+ * inside the tile's window; tile_rec[tile_off[t] .. tile_off[t+1]) (byte
+ * offsets, multiples of 16) are tile t's row-sorted records and
+ * tile_rowoff[t*136 .. +129) their row offsets; res_ptr / res_col the
+ * residual pattern.  With col_scale, c X is first written to xs (xrows x
+ * ldxs floats, 16-byte aligned rows).  fp32 accumulation, tile-then-residual
+ * order (same fp32 tolerance contract as hb_spmm_csr).  work as hb_spmm_tiled. */
+int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr,
+                      const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
+                      const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
+                      const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
+                      float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, void* stream);
 
 /* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
  * tensor cores with the 3xTF32 split (fp32 accuracy):
@@ -168,10 +194,11 @@ int hb_gemm_set_path(int32_t path);
  * *loss_out = fixed-order sum of row_loss (deterministic two-pass reduction).
  * keep_unmasked = 1: rows outside the mask are not written (the caller's
  * grad / row_loss rows there already hold zeros, e.g. from the previous
- * epoch). */
+ * epoch).  partials: HB_XENT_PARTIALS doubles of device scratch, required
+ * when n > 16384 (NULL otherwise allowed). */
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
                     const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                    double* loss_out, int32_t keep_unmasked, void* stream);
+                    double* loss_out, int32_t keep_unmasked, double* partials, void* stream);
 
 /* ReLU epilogue (linalg.py:78-80): y = max(z, 0), in place allowed. */
 int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream);

@@ -12,9 +12,9 @@ cudaError_t launch_dequant_gather(const hb_segment_t*, int, int, const int32_t*,
                                   const int32_t*, int, int, float*, int64_t, int, cudaStream_t);
 cudaError_t launch_philox_uniforms(uint64_t, uint64_t, uint64_t, int64_t, double*, cudaStream_t);
 cudaError_t launch_spmm(int, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
-                        float*, int64_t, int64_t, int, int, int, cudaStream_t);
+                        float*, int64_t, int64_t, int, int, int, int*, cudaStream_t);
 cudaError_t launch_xent(const float*, int64_t, int, int, const int32_t*, const uint8_t*, double, float*,
-                        int64_t, double*, double*, int, cudaStream_t);
+                        int64_t, double*, double*, int, double*, cudaStream_t);
 cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaStream_t);
 cudaError_t launch_relu_grad_mul(const float*, int64_t, const float*, int64_t, int, int, float*, int64_t,
                                  cudaStream_t);
@@ -35,7 +35,10 @@ extern int g_gemm_pair;
 extern int g_gemm_ts;
 cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                               const int2*, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
-                              float*, int64_t, cudaStream_t);
+                              float*, int64_t, int*, cudaStream_t);
+cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
+                                  const uint8_t*, const int64_t*, const int32_t*, const float*, const float*,
+                                  const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, cudaStream_t);
 
 int num_sms() {
   static int cached = 0;
@@ -102,33 +105,50 @@ int hb_spmm_csr(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, c
                 const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)))
     return fail(HB_EINVAL, "hb_spmm_csr: bad arguments");
-  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, -1, 1, 0, INT32_MAX, S(stream)),
+  return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, -1, 1, 0, INT32_MAX, nullptr,
+                               S(stream)),
                "hb_spmm_csr");
 }
 
 int hb_spmm_csr_ex(int32_t nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                    const float* X, int64_t ldx, int32_t d, float* Y, int64_t ldy, int64_t nnz, int32_t algo,
-                   int32_t window, int32_t stream_col, void* stream) {
+                   int32_t window, int32_t stream_col, int32_t* work, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || (nrows > 0 && (!row_ptr || !Y)) || algo < 0 || algo > 1)
     return fail(HB_EINVAL, "hb_spmm_csr_ex: bad arguments");
   return check(hb::launch_spmm(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, nnz, algo, window, stream_col,
-                               S(stream)),
+                               work, S(stream)),
                "hb_spmm_csr_ex");
 }
 
 int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
                   const int64_t* tile_off, const uint16_t* tile_rowoff, const void* tile_nz, const int64_t* res_ptr,
                   const int32_t* res_col, const float* res_val, const float* X, int64_t ldx, int32_t d, float* Y,
-                  int64_t ldy, void* stream) {
+                  int64_t ldy, int32_t* work, void* stream) {
   if (nrows < 0 || d < 0 || ldx < d || ldy < d || nblocks != (nrows + 63) / 64 ||
-      (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y)))
+      (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y || !work)))
     return fail(HB_EINVAL, "hb_spmm_tiled: bad arguments");
   const cudaError_t e = hb::launch_spmm_tiled(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_rowoff,
                                               reinterpret_cast<const int2*>(tile_nz), res_ptr, res_col, res_val, X,
-                                              ldx, d, Y, ldy, S(stream));
+                                              ldx, d, Y, ldy, work, S(stream));
   if (e == cudaErrorNotSupported)
     return fail(HB_EINVAL, "hb_spmm_tiled: X/Y need 16-byte aligned rows (ld % 4 == 0)");
   return check(e, "hb_spmm_tiled");
+}
+
+int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr,
+                      const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
+                      const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
+                      const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
+                      float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || nblocks != (nrows + 127) / 128 ||
+      (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y || !work)) || (col_scale && (!xs || ldxs < d)))
+    return fail(HB_EINVAL, "hb_spmm_tiled_bin: bad arguments");
+  const cudaError_t e = hb::launch_spmm_tiled_bin(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_rowoff,
+                                                  tile_rec, res_ptr, res_col, row_scale, col_scale, X, ldx, d, Y,
+                                                  ldy, xs, ldxs, work, S(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(HB_EINVAL, "hb_spmm_tiled_bin: X/Y need 16-byte aligned rows (ld % 4 == 0)");
+  return check(e, "hb_spmm_tiled_bin");
 }
 
 int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,
@@ -165,11 +185,12 @@ int hb_gemm_set_path(int32_t path) {
 
 int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,
                     const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                    double* loss_out, int32_t keep_unmasked, void* stream) {
-  if (n < 0 || C <= 0 || norm <= 0 || !loss_out || (n > 0 && (!logits || !labels || !mask || !grad || !row_loss)))
+                    double* loss_out, int32_t keep_unmasked, double* partials, void* stream) {
+  if (n < 0 || C <= 0 || norm <= 0 || !loss_out || (n > 0 && (!logits || !labels || !mask || !grad || !row_loss)) ||
+      (n > 16 * 1024 && !partials))
     return fail(HB_EINVAL, "hb_softmax_xent: bad arguments");
   return check(hb::launch_xent(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss, loss_out, keep_unmasked,
-                               S(stream)),
+                               partials, S(stream)),
                "hb_softmax_xent");
 }
 

@@ -12,8 +12,6 @@
 #include <cstdint>
 #include <cstdlib>
 #include <algorithm>
-#include <mutex>
-#include <vector>
 #include "common.cuh"
 
 namespace hb {
@@ -285,28 +283,12 @@ spmm_rows_scalar_kernel(int nrows, const int64_t* __restrict__ row_ptr, const in
 // algo: 0 auto, 1 row gather (the same kernel: the TMA-tiled path is a
 // separate entry point, hb_spmm_tiled).  `window` > 0 overrides the number of
 // nonzeros a lane group keeps in flight (tuning only).
-// Per-(device, stream) pair of ints {next work item, workers finished} for the
-// dynamically scheduled kernels (row-gather and tiled SpMM): launches on one
-// stream are ordered, and each launch leaves the pair at zero for the next.
-int* work_counter(cudaStream_t st) {
-  struct Slot { int dev; cudaStream_t st; int* p; };
-  static std::mutex mu;
-  static std::vector<Slot> slots;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> g(mu);
-  for (const Slot& s : slots)
-    if (s.dev == dev && s.st == st) return s.p;
-  int* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-  if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-  slots.push_back({dev, st, p});
-  return p;
-}
-
+// `work`: caller-provided pair of ints {next work item, workers finished},
+// zero on entry, left at zero by the last worker out (so one pair serves every
+// launch on a stream, graph replays included).  NULL: static grid-stride rows.
 cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
                         const float* X, int64_t ldx, int d, float* Y, int64_t ldy, int64_t nnz, int algo,
-                        int window, int stream_col, cudaStream_t st) {
+                        int window, int stream_col, int* work, cudaStream_t st) {
   (void)nnz;
   (void)algo;
   if (nrows <= 0 || d <= 0) return cudaSuccess;
@@ -316,13 +298,13 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
   const bool vec = (ldx % 4 == 0) && (ldy % 4 == 0) && ((((uintptr_t)X) & 15) == 0) &&
                    ((((uintptr_t)Y) & 15) == 0);
   static const int hint = getenv("HB_SPMM_HINT") ? atoi(getenv("HB_SPMM_HINT")) : 0;
-  static const int dyn = getenv("HB_SPMM_DYN") ? atoi(getenv("HB_SPMM_DYN")) : 1;
+  static const int dyn_env = getenv("HB_SPMM_DYN") ? atoi(getenv("HB_SPMM_DYN")) : 1;
+  const int dyn = dyn_env && work != nullptr;
   static const int chunk_env = getenv("HB_SPMM_CHUNK") ? atoi(getenv("HB_SPMM_CHUNK")) : 0;
   int* next_row = nullptr;
   int chunk = 1;
   if (dyn) {
-    next_row = work_counter(st);
-    if (!next_row) return cudaErrorMemoryAllocation;
+    next_row = work;
     // ~192 nonzeros per grab
     const int64_t avg = nnz > 0 ? (nnz + nrows - 1) / nrows : 32;
     chunk = chunk_env > 0 ? chunk_env : (int)std::max<int64_t>(1, std::min<int64_t>(32, 192 / std::max<int64_t>(1, avg)));

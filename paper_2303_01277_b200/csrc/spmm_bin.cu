@@ -1,0 +1,354 @@
+// K3/K4 factored tiled path: SpMM with a 0/1 pattern and diagonal scalings,
+//
+//   Y[i, :] = r[i] * sum_{(i,j) in pattern} c[j] X[j, :]
+//
+// which is what the trainer's aggregation operators are (linalg.spmm,
+// linalg.py:71-75, on the blocks of graph.py:120-141):
+//   * SAGE mean        M  = D^-1 A           -> r = 1/deg,  c = 1
+//   * its transpose    M^T = A^T D^-1        -> r = 1,      c = 1/deg
+//   * GCN              Â  = D^-1/2 (A+I) D^-1/2 -> r = c = dinv.
+// With the values factored out a tile record is the nonzero's column inside
+// its 64-column window: ONE BYTE (the general kernel, spmm_tiled.cu, moves an
+// 8-byte (col, val) record per nonzero through shared memory).  Records are
+// read 16 at a time with one broadcast LDS.128 and unpacked in registers, so
+// the shared-memory datapath — the binding resource of a SIMT SpMM — carries
+// only the gathered X rows: 8 wavefronts per nonzero at d = 256 instead of 9.
+// Row blocks are 128 rows tall (16 consumer warps x 8 rows): the TMA-staged
+// 64-row X window is reused by twice as many rows as in the general kernel,
+// halving the staging traffic per nonzero.  c is applied by a pre-pass into a
+// caller-provided scratch copy of X (one HBM read + write of X), r to the
+// accumulators before the store.
+//
+// Work items (row block, feature panel) are handed out in ascending order
+// from a caller-provided counter pair {next item, CTAs finished} that must be
+// zero on entry; the last CTA out re-arms it, so the same pair serves the
+// next launch on the stream (and graph replays).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdint>
+#include <cstdlib>
+#include "common.cuh"
+
+namespace hb {
+namespace sb {
+
+constexpr int kRB = 128;          // rows per block
+constexpr int kW = 64;            // columns per window (a record is col - c0 < 64)
+constexpr int kRowOff = 136;      // u16 row offsets per tile (129 used; 272 bytes)
+constexpr int kRPW = 8;           // rows per consumer warp
+constexpr int kMaxRec = 2048;     // record bytes per tile (ops.TiledCsr splits denser tiles)
+constexpr int kConsumers = kRB / kRPW;
+constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int kQ = 4;
+
+struct Args {
+  int nrows, nblocks, npanels, d, pw;
+  int* work;
+  const int32_t* tile_ptr;
+  const int32_t* tile_win;
+  const int64_t* tile_off;        // byte offsets of each tile's records (multiples of 16)
+  const uint16_t* tile_rowoff;    // [ntiles][kRowOff]
+  const uint8_t* tile_rec;
+  const int64_t* res_ptr;         // residual pattern (CSR without values)
+  const int32_t* res_col;
+  const float* row_scale;         // nullable
+  const float* X;
+  int64_t ldx;
+  float* Y;
+  int64_t ldy;
+};
+
+template <int NV, int G, int S>
+struct Smem {
+  static constexpr int P = 4 * G * NV;
+  static constexpr int X_BYTES = kW * P * 4;
+  static constexpr int RO_BYTES = kRowOff * 2;
+  static constexpr int STAGE = X_BYTES + kMaxRec + RO_BYTES + 112;   // 16-byte multiple
+  static constexpr int TOTAL = S * STAGE + 128;
+  static_assert(STAGE % 16 == 0, "stage alignment");
+};
+
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// byte p (0..15) of a 16-byte record chunk
+__device__ __forceinline__ int rec_byte(const uint4& c, int p) {
+  const uint32_t w = (p & 8) ? ((p & 4) ? c.w : c.z) : ((p & 4) ? c.y : c.x);
+  return (int)__byte_perm(w, 0u, 0x4440u | (uint32_t)(p & 3));
+}
+
+template <int NV, int G>
+__device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restrict__ x, int nlast) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    if (q < NV - 1 || nlast) {
+      const float4 t = x[q * G];
+      acc[q].x += t.x; acc[q].y += t.y; acc[q].z += t.z; acc[q].w += t.w;
+    }
+  }
+}
+
+// 1 CTA/SM: up to 120 registers per thread (17 warps); 2 CTAs/SM: 56
+template <int NV, int G, int S, int MINB>
+__global__ void __maxnreg__(MINB == 1 ? 120 : 56)
+spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
+  using S_ = Smem<NV, G, S>;
+  constexpr int P = S_::P;
+  constexpr int NG = 32 / G;             // lane groups per warp (each owns whole rows)
+  constexpr int RPG = kRPW / NG;         // rows per lane group
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full[S], empty[S], ifull[kQ], iempty[kQ];
+  __shared__ int item_q[kQ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hg = lane / G, gl = lane % G;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    for (int q = 0; q < kQ; ++q) {
+      mbar_init(&ifull[q], 1);
+      mbar_init(&iempty[q], kConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int items = a.nblocks * a.npanels;
+
+  if (warp == kConsumers) {
+    // ---------------- producer: lane 0 claims items, lane s feeds ring stage s
+    int it = 0;
+    for (int qi = 0;; ++qi) {
+      int item = 0;
+      if (lane == 0) {
+        item = atomicAdd(a.work, 1);
+        const int q = qi % kQ;
+        mbar_wait(&iempty[q], ((qi / kQ) & 1) ^ 1);
+        item_q[q] = item;
+        mbar_arrive_cta(&ifull[q]);
+        if (item >= items && atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
+          atomicExch(a.work, 0);
+          atomicExch(a.work + 1, 0);
+        }
+      }
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= items) break;
+      const int b = item / a.npanels, pn = item % a.npanels;
+      const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
+      for (int t = t0; t < t1; ++t, ++it) {
+        if (lane >= S || it % S != lane) continue;
+        const int s = it % S;
+        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        uint8_t* st = smem + s * S_::STAGE;
+        const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
+        const uint32_t rb = (uint32_t)(o1 - o0);
+        mbar_expect_tx(&full[s], (uint32_t)(kW * a.pw * 4) + rb + S_::RO_BYTES);
+        tma_2d(st, &tmX, pn * P, a.tile_win[t] * kW, &full[s]);
+        if (rb) tma_load_1d(st + S_::X_BYTES, a.tile_rec + o0, rb, &full[s]);
+        tma_load_1d(st + S_::X_BYTES + kMaxRec, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES, &full[s]);
+      }
+    }
+    __syncwarp();
+    return;
+  }
+
+  // ---------------- consumers: lane group hg owns rows hg, hg + NG, ... of
+  // the warp's kRPW rows; lane gl holds NV float4 columns of the panel
+  const int pw4 = a.pw / 4;
+  // the last float4 of a lane may fall beyond the staged width (narrow panels)
+  const int nlast = ((NV - 1) * G + gl) * 4 < a.pw;
+  int it = 0;
+  for (int qi = 0;; ++qi) {
+    const int q = qi % kQ;
+    mbar_wait(&ifull[q], (qi / kQ) & 1);
+    const int item = item_q[q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&iempty[q]);
+    if (item >= items) break;
+    const int b = item / a.npanels, pn = item % a.npanels;
+    const int r0 = b * kRB + warp * kRPW;
+    const int col0 = pn * P;
+    float4 acc[RPG][NV];
+#pragma unroll
+    for (int i = 0; i < RPG; ++i)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[i][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint8_t* st = smem + s * S_::STAGE;
+      const float4* xs = reinterpret_cast<const float4*>(st) + gl;
+      const uint8_t* rec = st + S_::X_BYTES;
+      const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + kMaxRec) + warp * kRPW;
+#pragma unroll
+      for (int i = 0; i < RPG; ++i) {
+        const int rr = hg + i * NG;
+        const int k = ro[rr], k1 = ro[rr + 1];
+        for (int kb = k & ~15; kb < k1; kb += 16) {
+          const uint4 c = *reinterpret_cast<const uint4*>(rec + kb);       // 16 records, one broadcast
+          int p = k > kb ? k - kb : 0;
+          const int pe = k1 - kb < 16 ? k1 - kb : 16;
+          if constexpr (NV >= 2 && G == 32) {
+            // wide rows: one X row (NV float4 per lane) in flight per record
+            for (; p < pe; ++p) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
+          } else {
+            for (; p + 1 < pe; p += 2) {
+              const int j0 = rec_byte(c, p), j1 = rec_byte(c, p + 1);
+              float4 x0[NV], x1[NV];
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                if (v < NV - 1 || nlast) {
+                  x0[v] = xs[j0 * pw4 + v * G];
+                  x1[v] = xs[j1 * pw4 + v * G];
+                }
+              }
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                if (v < NV - 1 || nlast) {
+                  acc[i][v].x += x0[v].x; acc[i][v].y += x0[v].y; acc[i][v].z += x0[v].z; acc[i][v].w += x0[v].w;
+                  acc[i][v].x += x1[v].x; acc[i][v].y += x1[v].y; acc[i][v].z += x1[v].z; acc[i][v].w += x1[v].w;
+                }
+              }
+            }
+          }
+          if (p < pe) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
+    }
+    // residual pattern entries gathered from global X, row scale, store
+#pragma unroll
+    for (int i = 0; i < RPG; ++i) {
+      const int r = r0 + hg + i * NG;
+      if (r >= a.nrows) continue;
+      const float* Xp = a.X + col0;
+      const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
+      for (int64_t k = e0; k < e1; ++k) {
+        const float4* xr = reinterpret_cast<const float4*>(Xp + (int64_t)__ldg(a.res_col + k) * a.ldx) + gl;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if (col0 + (v * G + gl) * 4 < a.d) {
+            const float4 t4 = __ldg(xr + v * G);
+            acc[i][v].x += t4.x; acc[i][v].y += t4.y; acc[i][v].z += t4.z; acc[i][v].w += t4.w;
+          }
+        }
+      }
+      const float sc = a.row_scale ? __ldg(a.row_scale + r) : 1.f;
+      float* y = a.Y + (int64_t)r * a.ldy + col0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int col = (v * G + gl) * 4;
+        const int rem = a.d - col0 - col;
+        const float4 o = make_float4(acc[i][v].x * sc, acc[i][v].y * sc, acc[i][v].z * sc, acc[i][v].w * sc);
+        if (rem >= 4) {
+          *reinterpret_cast<float4*>(y + col) = o;
+        } else if (rem > 0) {
+          y[col] = o.x;
+          if (rem > 1) y[col + 1] = o.y;
+          if (rem > 2) y[col + 2] = o.z;
+        }
+      }
+    }
+  }
+}
+
+// Xs[j, :d] = c[j] * X[j, :d]  (float4 rows: ld % 4 == 0, 16-byte aligned)
+__global__ void scale_rows_kernel(const float* __restrict__ X, int64_t ldx, int rows, int d4,
+                                  const float* __restrict__ c, float* __restrict__ Xs, int64_t ldxs) {
+  const int64_t total = (int64_t)rows * d4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d4, q = e - r * d4;
+    const float s = __ldg(c + r);
+    float4 v = __ldg(reinterpret_cast<const float4*>(X + r * ldx) + q);
+    v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+    reinterpret_cast<float4*>(Xs + r * ldxs)[q] = v;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+template <int NV, int G, int S, int MINB = 1>
+static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
+  using S_ = Smem<NV, G, S>;
+  static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
+  Args a = a0;
+  a.npanels = (a.d + S_::P - 1) / S_::P;
+  a.pw = a.npanels > 1 ? S_::P : (a.d + 3) / 4 * 4;
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)xrows};
+  cuuint64_t strides[1] = {(cuuint64_t)(a.ldx * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)a.pw, (cuuint32_t)kW};
+  cuuint32_t es[2] = {1u, 1u};
+  if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.X), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<NV, G, S, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = a.nblocks * a.npanels;
+  const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
+  if (grid > 0) spmm_bin_kernel<NV, G, S, MINB><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  return cudaGetLastError();
+}
+
+}  // namespace sb
+
+cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32_t* tile_ptr,
+                                  const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
+                                  const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
+                                  const float* row_scale, const float* col_scale, const float* X, int64_t ldx,
+                                  int d, float* Y, int64_t ldy, float* xs, int64_t ldxs, int* work,
+                                  cudaStream_t stream) {
+  if (nrows <= 0 || d <= 0) return cudaSuccess;
+  if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
+  if (col_scale) {
+    if (!xs || (ldxs & 3) || (((uintptr_t)xs) & 15) || ldxs < d) return cudaErrorInvalidValue;
+    const int d4 = (d + 3) / 4;
+    const int64_t total = (int64_t)xrows * d4;
+    int grid = (int)((total + 255) / 256);
+    if (grid > num_sms() * 16) grid = num_sms() * 16;
+    if (grid > 0) sb::scale_rows_kernel<<<grid, 256, 0, stream>>>(X, ldx, xrows, d4, col_scale, xs, ldxs);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    X = xs;
+    ldx = ldxs;
+  }
+  sb::Args a{};
+  a.nrows = nrows; a.nblocks = nblocks; a.d = d; a.work = work;
+  a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
+  a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
+  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
+  if (d <= 64) return sb::launch_nv<2, 8, 4, 2>(a, xrows, stream);      // 4 rows of a warp in parallel
+  if (d <= 128) return sb::launch_nv<1, 32, 5>(a, xrows, stream);
+  return sb::launch_nv<2, 32, 3>(a, xrows, stream);                        // 256-column panels
+}
+
+}  // namespace hb

@@ -41,7 +41,7 @@ constexpr int kQ = 4;            // work-item queue depth (producer -> consumers
 
 struct Args {
   int nrows, nblocks, npanels, d;
-  int* next_item;                // {next item, CTAs finished}: self-resetting counter pair
+  int* next_item;                // {next item, CTAs finished}: caller's self-resetting counter pair
   int pw;                        // staged panel width (floats): min(P, d rounded up to 4)
   const int32_t* tile_ptr;       // [nblocks + 1]
   const int32_t* tile_win;       // [ntiles]
@@ -388,12 +388,10 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
 
 }  // namespace st
 
-int* work_counter(cudaStream_t st);
-
 cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* tile_ptr, const int32_t* tile_win,
                               const int64_t* tile_off, const uint16_t* tile_rowoff, const int2* tile_nz,
                               const int64_t* res_ptr, const int32_t* res_col, const float* res_val, const float* X,
-                              int64_t ldx, int d, float* Y, int64_t ldy, cudaStream_t stream) {
+                              int64_t ldx, int d, float* Y, int64_t ldy, int* work, cudaStream_t stream) {
   if (nrows <= 0 || d <= 0) return cudaSuccess;
   if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
   st::Args a{};
@@ -401,8 +399,8 @@ cudaError_t launch_spmm_tiled(int nrows, int xrows, int nblocks, const int32_t* 
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_nz = tile_nz; a.res_ptr = res_ptr; a.res_col = res_col; a.res_val = res_val;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-  a.next_item = work_counter(stream);
-  if (!a.next_item) return cudaErrorMemoryAllocation;
+  a.next_item = work;
+  if (!a.next_item) return cudaErrorInvalidValue;
   // d <= 64: a lane group of 8 lanes per row (4 rows of a warp in parallel),
   // 2 CTAs per SM; wider panels: HB_TILED_ROWPAR=1 selects the same row-per-
   // group consumer (8 lanes x NV float4)

@@ -4,8 +4,6 @@
 // argmax accuracy (trainer.py:129-144) and keyed dropout (trainer.py:285-289).
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <mutex>
-#include <vector>
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -102,22 +100,6 @@ __global__ void __launch_bounds__(256) sum_f64_kernel(const double* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = sh[0];
-}
-
-// kSumBlocks doubles of scratch per (device, stream): launches on one stream are ordered
-static double* sum_scratch(cudaStream_t st) {
-  struct Slot { int dev; cudaStream_t st; double* p; };
-  static std::mutex mu;
-  static std::vector<Slot> slots;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> g(mu);
-  for (const Slot& s : slots)
-    if (s.dev == dev && s.st == st) return s.p;
-  double* p = nullptr;
-  if (cudaMalloc(&p, kSumBlocks * sizeof(double)) != cudaSuccess) return nullptr;
-  slots.push_back({dev, st, p});
-  return p;
 }
 
 // ---- ReLU and relu' product ----------------------------------------------------
@@ -259,15 +241,15 @@ static int grid_for(int64_t work, int per_block) {
 
 cudaError_t launch_xent(const float* logits, int64_t ld, int n, int C, const int32_t* labels,
                         const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
-                        double* loss_out, int keep_unmasked, cudaStream_t st) {
+                        double* loss_out, int keep_unmasked, double* partials, cudaStream_t st) {
   if (n > 0)
     xent_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss,
                                                      keep_unmasked);
   if (n <= 16 * 1024) {
     sum_f64_kernel<<<1, 256, 0, st>>>(row_loss, n, loss_out);
   } else {
-    double* part = sum_scratch(st);
-    if (!part) return cudaErrorMemoryAllocation;
+    double* part = partials;            // caller's HB_XENT_PARTIALS doubles
+    if (!part) return cudaErrorInvalidValue;
     const int chunk = (n + kSumBlocks - 1) / kSumBlocks;
     sum_f64_part_kernel<<<kSumBlocks, 256, 0, st>>>(row_loss, n, chunk, part);
     sum_f64_kernel<<<1, 256, 0, st>>>(part, kSumBlocks, loss_out);

@@ -12,7 +12,9 @@ from ._lib import ptr, stream_handle
 
 
 class DeviceCsr:
-    """CSR matrix resident in HBM: int64 row_ptr, int32 col_idx, fp32 values."""
+    """CSR matrix resident in HBM: int64 row_ptr, int32 col_idx, fp32 values,
+    plus the {next row chunk, warps finished} counter pair its dynamically
+    scheduled SpMM launches use (zero between launches)."""
 
     def __init__(self, rows: int, cols: int, row_ptr, col_idx, values, device):
         import torch
@@ -21,35 +23,110 @@ class DeviceCsr:
         self.col_idx = torch.from_numpy(np.ascontiguousarray(col_idx, dtype=np.int32)).to(device)
         self.values = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(device)
         self.nnz = int(self.col_idx.numel())
+        self.work = torch.zeros(2, dtype=torch.int32, device=device)
 
     @classmethod
     def from_csr(cls, m, device):
         return cls(m.rows, m.cols, m.row_ptr, m.col_idx, m.values, device)
 
 
+def factor_scales(a: DeviceCsr):
+    """Diagonal factorisation of the values, if there is one:
+    values[i, j] == r[i] * c[j] over a 0/1 pattern, for the trainer's
+    aggregation operators (graph.py:120-141):
+
+    * row-constant rows (SAGE mean D^-1 A):          r = row value, c = None;
+    * column-constant columns (its transpose A^T D^-1): r = None, c = column value;
+    * GCN D^-1/2 (A+I) D^-1/2 and its partition blocks / their transposes
+      (self loops on the square part): r = c = sqrt(diag) there, the other
+      rows' / columns' factors from their nonzeros; values within 2^-21
+      relative of r[i] c[j].
+
+    Returns (r, c) fp32 device tensors (either may be None), or None when the
+    values do not factor (general matrices keep per-nonzero values)."""
+    import torch
+    if a.nnz == 0:
+        return None
+    dev = a.row_ptr.device
+    v = a.values
+    counts = a.row_ptr[1:] - a.row_ptr[:-1]
+    rows = torch.repeat_interleave(torch.arange(a.rows, device=dev, dtype=torch.int64), counts)
+    col = a.col_idx.long()
+    nonempty = counts > 0
+    first = torch.zeros(a.rows, dtype=v.dtype, device=dev)
+    first[nonempty] = v[a.row_ptr[:-1][nonempty]]
+    if bool((v == first[rows]).all()):
+        return first, None
+    cfirst = torch.zeros(a.cols, dtype=v.dtype, device=dev).scatter_(0, col, v)
+    if bool((v == cfirst[col]).all()):
+        return None, cfirst
+    # GCN: the self loops give r = c = sqrt(diag) on the square part; rows /
+    # columns without a diagonal entry (the halo columns of a partition block,
+    # the halo rows of its transpose) take their factor from any nonzero whose
+    # other factor is known
+    m = min(a.rows, a.cols)
+    dmask = col == rows
+    if not bool(dmask.any()):
+        return None
+    vd = v.double()
+    nan = float("nan")
+    r = torch.full((a.rows,), nan, dtype=torch.float64, device=dev)
+    c = torch.full((a.cols,), nan, dtype=torch.float64, device=dev)
+    di = rows[dmask]
+    if bool((vd[dmask] <= 0).any()):
+        return None
+    r[di] = vd[dmask].sqrt()
+    c[di] = r[di]
+    del m
+    sel = torch.isnan(r[rows]) & ~torch.isnan(c[col])
+    r.scatter_(0, rows[sel], vd[sel] / c[col[sel]])
+    sel = torch.isnan(c[col]) & ~torch.isnan(r[rows])
+    c.scatter_(0, col[sel], vd[sel] / r[rows[sel]])
+    rr, cc = r[rows], c[col]
+    if bool(torch.isnan(rr).any() | torch.isnan(cc).any()):
+        return None
+    if not bool(((vd - rr * cc).abs() <= 2.0 ** -21 * vd.abs()).all()):
+        return None
+    return torch.nan_to_num(r, nan=0.0).float(), torch.nan_to_num(c, nan=0.0).float()
+    return None
+
+
 class TiledCsr:
     """The K3/K4 tiled layout of a ``DeviceCsr`` (built on the device, once per
-    matrix): dense (64-row block x 64-column window) tiles holding at least
+    matrix): dense (row block x 64-column window) tiles holding at least
     ``threshold`` nonzeros — their X windows are staged in shared memory by TMA
     and reused across the block's rows — and a residual CSR for the rest.
     Tile records keep the CSR's (row, column) order, so each row still sums its
-    tile contributions in ascending column order, then its residual ones."""
+    tile contributions in ascending column order, then its residual ones.
 
-    RB = 64
+    Two record formats:
+    * general (``hb_spmm_tiled``): 64-row blocks, 8-byte {col, val} records;
+    * factored (``hb_spmm_tiled_bin``, when ``factor_scales`` finds the values
+      to be r[i] c[j] over a 0/1 pattern — the trainer's aggregation
+      operators): 128-row blocks, one-byte column records, r / c applied as
+      diagonal scalings."""
+
     W = 64
-    ROWOFF = 72
-    MAXREC = 1024
 
-    def __init__(self, a: DeviceCsr, threshold: int = 64):
+    def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None):
         import torch
         dev = a.row_ptr.device
+        scales = factor_scales(a) if factored in (None, True) else None
+        if factored is True and scales is None:
+            raise ValueError("matrix values do not factor into diagonal scalings of a 0/1 pattern")
+        self.binary = scales is not None
+        self.row_scale, self.col_scale = scales if self.binary else (None, None)
+        self.RB, self.ROWOFF, self.MAXREC = (128, 136, 2048) if self.binary else (64, 72, 1024)
         self.rows, self.cols, self.nnz = a.rows, a.cols, a.nnz
-        self.nblocks = (a.rows + self.RB - 1) // self.RB
-        nwin = (a.cols + self.W - 1) // self.W
+        self.work = torch.zeros(2, dtype=torch.int32, device=dev)
+        self._xs = {}
+        RB, W = self.RB, self.W
+        self.nblocks = (a.rows + RB - 1) // RB
+        nwin = (a.cols + W - 1) // W
         counts_row = a.row_ptr[1:] - a.row_ptr[:-1]
         rows = torch.repeat_interleave(torch.arange(a.rows, device=dev, dtype=torch.int64), counts_row)
         col = a.col_idx.long()
-        key = (rows // self.RB) * nwin + col // self.W
+        key = (rows // RB) * nwin + col // W
         order = torch.sort(key, stable=True).indices          # (block, window) groups, CSR order inside
         skey = key[order]
         del key
@@ -73,10 +150,10 @@ class TiledCsr:
         tp = torch.zeros(self.nblocks + 1, dtype=torch.int64, device=dev)
         tp[1:] = torch.cumsum(torch.bincount(tile_blk, minlength=self.nblocks), 0)
         self.tile_ptr = tp.to(torch.int32)
-        padded = (tile_cnt + 1) // 2 * 2                      # 16-byte aligned record runs
+        align = 16 if self.binary else 2                      # record runs start 16-byte aligned
+        padded = (tile_cnt + align - 1) // align * align
         off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
         off[1:] = torch.cumsum(padded, 0)
-        self.tile_off = off
         didx = order[dense_nz]                                # original nonzero ids, tile order
         grp_of = (torch.cumsum(dense_g.long(), 0) - 1)[gid[dense_nz]]
         gstart = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
@@ -85,15 +162,23 @@ class TiledCsr:
         tile_of = first_sub[grp_of] + grank // self.MAXREC
         rank = grank % self.MAXREC
         pos = off[tile_of] + rank
-        nz = torch.zeros((int(off[-1].item()), 2), dtype=torch.int32, device=dev)
-        nz[pos, 0] = (col[didx] - self.tile_win.long()[tile_of] * self.W).to(torch.int32)
-        nz[pos, 1] = a.values[didx].view(torch.int32)
-        self.tile_nz = nz
-        lr = rows[didx] % self.RB
-        per = torch.bincount(tile_of * self.RB + lr, minlength=self.ntiles * self.RB).view(self.ntiles, self.RB)
+        rel = col[didx] - self.tile_win.long()[tile_of] * W
+        if self.binary:
+            rec = torch.zeros(max(16, int(off[-1].item())), dtype=torch.uint8, device=dev)
+            rec[pos] = rel.to(torch.uint8)
+            self.tile_nz = rec
+            self.tile_off = off                               # byte offsets
+        else:
+            nz = torch.zeros((int(off[-1].item()), 2), dtype=torch.int32, device=dev)
+            nz[pos, 0] = rel.to(torch.int32)
+            nz[pos, 1] = a.values[didx].view(torch.int32)
+            self.tile_nz = nz
+            self.tile_off = off                               # record (8-byte) offsets
+        lr = rows[didx] % RB
+        per = torch.bincount(tile_of * RB + lr, minlength=self.ntiles * RB).view(self.ntiles, RB)
         ro = torch.zeros((self.ntiles, self.ROWOFF), dtype=torch.int32, device=dev)
-        ro[:, 1:self.RB + 1] = torch.cumsum(per, 1)
-        self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= 4096, read as uint16
+        ro[:, 1:RB + 1] = torch.cumsum(per, 1)
+        self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= MAXREC, read as uint16
         keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
         keep[didx] = False
         rp = torch.zeros(a.rows + 1, dtype=torch.int64, device=dev)
@@ -107,13 +192,28 @@ class TiledCsr:
     def tiled_fraction(self) -> float:
         return self.tiled_nnz / max(1, self.nnz)
 
+    def col_scaled_scratch(self, ld: int, device):
+        """The c X copy hb_spmm_tiled_bin writes when there is a column scale."""
+        import torch
+        if ld not in self._xs:
+            self._xs[ld] = torch.empty((self.cols, ld), dtype=torch.float32, device=device)
+        return self._xs[ld]
+
 
 def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
-    """``linalg.spmm`` (linalg.py:71-75) through the TMA-staged tiled kernel."""
+    """``linalg.spmm`` (linalg.py:71-75) through the TMA-staged tiled kernel
+    (the factored one-byte-record kernel when ``t.binary``)."""
     d = x.shape[1] if d is None else d
+    if t.binary:
+        xs = t.col_scaled_scratch(x.stride(0), x.device) if t.col_scale is not None else None
+        _lib.call("hb_spmm_tiled_bin", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),
+                  ptr(t.tile_off), ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col),
+                  ptr(t.row_scale), ptr(t.col_scale), ptr(x), x.stride(0), d, ptr(out), out.stride(0),
+                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), stream_handle(stream))
+        return out
     _lib.call("hb_spmm_tiled", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win), ptr(t.tile_off),
               ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col), ptr(t.res_val), ptr(x),
-              x.stride(0), d, ptr(out), out.stride(0), stream_handle(stream))
+              x.stride(0), d, ptr(out), out.stride(0), ptr(t.work), stream_handle(stream))
     return out
 
 
@@ -128,7 +228,7 @@ def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "a
     sc = 2**31 - 1 if stream_col is None else int(stream_col)
     _lib.call("hb_spmm_csr_ex", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
               x.stride(0), d, ptr(out), out.stride(0), a.nnz, SPMM_ALGOS[algo], int(window), sc,
-              stream_handle(stream))
+              ptr(getattr(a, "work", None)), stream_handle(stream))
     return out
 
 
@@ -175,14 +275,21 @@ def gemm_set_path(path: int):
     _lib.call("hb_gemm_set_path", int(path))
 
 
+XENT_PARTIALS = 256      # HB_XENT_PARTIALS
+
+
 def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None,
-                 keep_unmasked: bool = False):
+                 keep_unmasked: bool = False, partials=None):
     """``linalg.softmax_cross_entropy`` (linalg.py:87-112) on device.
-    keep_unmasked: grad / row_loss rows outside the mask already hold zeros."""
+    keep_unmasked: grad / row_loss rows outside the mask already hold zeros.
+    partials: XENT_PARTIALS doubles of scratch (allocated here if omitted)."""
+    import torch
     n = labels.numel()
+    if partials is None and n > 16 * 1024:
+        partials = torch.empty(XENT_PARTIALS, dtype=torch.float64, device=logits.device)
     _lib.call("hb_softmax_xent", ptr(logits), logits.stride(0), n, C, ptr(labels), ptr(mask),
               float(norm), ptr(grad), grad.stride(0), ptr(row_loss), ptr(loss_out), int(bool(keep_unmasked)),
-              stream_handle(stream))
+              ptr(partials), stream_handle(stream))
 
 
 def relu(z, y, n: int, d: int, stream=None):

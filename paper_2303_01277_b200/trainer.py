@@ -233,6 +233,7 @@ class DeviceRank:
         self.JL = torch.zeros((NL, _ld(W[L])), dtype=f32, device=dev)
         self.row_loss = torch.zeros(max(1, NL), dtype=torch.float64, device=dev)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.xent_partials = torch.zeros(ops.XENT_PARTIALS, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(6, dtype=torch.int64, device=dev)
         labels = np.concatenate([np.asarray(p.labels) for p in layout.parts]).astype(np.int32)
@@ -585,7 +586,7 @@ class DeviceRank:
         # JL / row_loss rows outside the train mask are zero from allocation and
         # never written: the CE kernel skips them
         ops.softmax_xent(logits, C, self.labels, self.train_mask, self.norm, self.JL,
-                         self.row_loss, self.loss_dev, keep_unmasked=True)
+                         self.row_loss, self.loss_dev, keep_unmasked=True, partials=self.xent_partials)
         self.launches += 2
         J = self.JL
         for l in range(L, 0, -1):

@@ -57,8 +57,25 @@ def test_argument_validation_without_a_device():
     lib.hb_gemm_f32.argtypes = [i32, i32, i32, P, i64, i64, P, i64, i64, P, i64, f32, P, i64, P, i64, P]
     rc = lib.hb_gemm_f32(8, 8, 4, 1, 4, 1, 1, 8, 1, None, 8, 1.0, 1, 8, None, 0, None)
     assert rc == -1 and b"hb_gemm_f32" in lib.hb_last_error()
-    lib.hb_spmm_csr_ex.argtypes = [i32, P, P, P, P, i64, i32, P, i64, i64, i32, i32, i32, P]
-    rc = lib.hb_spmm_csr_ex(4, 1, 1, 1, 1, 2, 8, 1, 8, 10, 0, 0, 2**31 - 1, None)   # ldx < d
+    lib.hb_spmm_csr_ex.argtypes = [i32, P, P, P, P, i64, i32, P, i64, i64, i32, i32, i32, P, P]
+    rc = lib.hb_spmm_csr_ex(4, 1, 1, 1, 1, 2, 8, 1, 8, 10, 0, 0, 2**31 - 1, None, None)   # ldx < d
     assert rc == -1 and b"hb_spmm_csr_ex" in lib.hb_last_error()
-    rc = lib.hb_spmm_csr_ex(4, 1, 1, 1, 1, 8, 8, 1, 8, 10, 7, 0, 2**31 - 1, None)   # unknown algo
+    rc = lib.hb_spmm_csr_ex(4, 1, 1, 1, 1, 8, 8, 1, 8, 10, 7, 0, 2**31 - 1, None, None)   # unknown algo
     assert rc == -1
+    # the tiled kernels need their caller-provided work counter pair
+    lib.hb_spmm_tiled.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, i64, i32, P, i64, P, P]
+    rc = lib.hb_spmm_tiled(64, 64, 1, 1, 1, 1, 1, 1, 1, 1, 1, 16, 8, 8, 16, 8, None, None)
+    assert rc == -1 and b"hb_spmm_tiled" in lib.hb_last_error()
+    lib.hb_spmm_tiled_bin.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, P, i64, i32, P, i64, P, i64, P, P]
+    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, None, None)
+    assert rc == -1 and b"hb_spmm_tiled_bin" in lib.hb_last_error()
+    # a column scale needs the scratch copy of X
+    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, 16, 16, 8, 8, 16, 8, None, 0, 16, None)
+    assert rc == -1
+    # 128-row blocks
+    rc = lib.hb_spmm_tiled_bin(128, 128, 2, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, 16, None)
+    assert rc == -1
+    # > 16384 rows: the loss reduction needs the caller's partials
+    lib.hb_softmax_xent.argtypes = [P, i64, i32, i32, P, P, ctypes.c_double, P, i64, P, P, i32, P, P]
+    rc = lib.hb_softmax_xent(16, 8, 20000, 8, 16, 16, 1.0, 16, 8, 16, 16, 0, None, None)
+    assert rc == -1 and b"hb_softmax_xent" in lib.hb_last_error()

@@ -1,5 +1,6 @@
 """Host-side planning logic (no GPU)."""
 
+import numpy as np
 import pytest
 
 
@@ -119,3 +120,60 @@ def test_tiled_csr_decomposition_is_exact():
     np.testing.assert_array_equal(rebuilt, dense)
     assert T.tiled_nnz + len(rc) == a.nnz
     assert T.ntiles > int((tp[1:] - tp[:-1] > 0).sum())                # the dense block was split
+
+
+def _tile_dense(T):
+    """Rebuild the dense matrix a TiledCsr describes (tiles + residual)."""
+    import torch
+    out = np.zeros((T.rows, T.cols))
+    tp, win = T.tile_ptr.numpy(), T.tile_win.numpy()
+    off, ro = T.tile_off.numpy(), T.tile_rowoff.numpy().astype(np.int64) & 0xFFFF
+    rs = T.row_scale.double().numpy() if T.row_scale is not None else np.ones(T.rows)
+    cs = T.col_scale.double().numpy() if T.col_scale is not None else np.ones(T.cols)
+    for b in range(T.nblocks):
+        for t in range(tp[b], tp[b + 1]):
+            for lr in range(T.RB):
+                r = b * T.RB + lr
+                for k in range(ro[t, lr], ro[t, lr + 1]):
+                    if T.binary:
+                        c = win[t] * T.W + int(T.tile_nz[off[t] + k])
+                        out[r, c] += rs[r] * cs[c]
+                    else:
+                        c = win[t] * T.W + int(T.tile_nz[off[t] + k, 0])
+                        out[r, c] += float(T.tile_nz[off[t] + k, 1:2].view(torch.float32))
+    rp, rc, rv = T.res_ptr.numpy(), T.res_col.numpy(), T.res_val.numpy()
+    for r in range(T.rows):
+        for k in range(rp[r], rp[r + 1]):
+            out[r, rc[k]] += rs[r] * cs[rc[k]] if T.binary else rv[k]
+    return out
+
+
+@pytest.mark.parametrize("kind", ["general", "mean", "mean_T", "gcn"])
+def test_tiled_layout_reconstructs_matrix(kind):
+    """ops.TiledCsr (built with torch ops, no kernel) describes exactly the
+    input matrix: 64-row / 8-byte-record tiles for general values, 128-row /
+    one-byte-record tiles plus diagonal scalings for the trainer's operators
+    (graph.py:120-141)."""
+    import scipy.sparse as sp
+    from paper_2303_01277_b200 import ops
+    rng = np.random.default_rng(3)
+    rows, cols = 300, 420
+    pat = (rng.random((rows, cols)) < 0.01)
+    pat[130:250, 64:128] |= rng.random((120, 64)) < 0.5
+    pat = pat.astype(np.float64)
+    if kind == "general":
+        a = pat * rng.standard_normal(pat.shape)
+    elif kind.startswith("mean"):
+        a = pat / np.maximum(pat.sum(1), 1)[:, None]
+        if kind == "mean_T":
+            a = a.T.copy()
+    else:
+        np.fill_diagonal(pat, 1.0)
+        dinv = 1 / np.sqrt(rng.integers(1, 50, cols))
+        a = dinv[:rows, None] * pat * dinv[None, :]
+    m = sp.csr_matrix(a.astype(np.float32))
+    A = ops.DeviceCsr(m.shape[0], m.shape[1], m.indptr, m.indices, m.data, "cpu")
+    T = ops.TiledCsr(A, threshold=100)
+    assert T.binary == (kind != "general")
+    assert T.RB == (128 if T.binary else 64) and 0 < T.tiled_fraction < 1
+    np.testing.assert_allclose(_tile_dense(T), m.toarray(), rtol=3e-7, atol=0)

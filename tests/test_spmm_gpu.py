@@ -76,11 +76,11 @@ def test_spmm_random_power_law_rows(d):
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0):
+def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None):
     from paper_2303_01277_b200 import ops
     rows, d = len(rp) - 1, x.shape[1]
     A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
-    T = ops.TiledCsr(A, threshold=threshold)
+    T = ops.TiledCsr(A, threshold=threshold, factored=factored)
     X = torch.zeros(ncols, d + ld_pad, device="cuda")
     X[:, :d] = torch.from_numpy(x)
     Y = torch.full((rows, d + ld_pad), 7.0, device="cuda")
@@ -91,17 +91,96 @@ def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0):
     return out[:, :d].astype(np.float64), T
 
 
+@pytest.mark.parametrize("factored", [None, False])
 @pytest.mark.parametrize("threshold", [1, 64, 10**9])
-def test_spmm_tiled_matches_reference_golden(threshold):
-    """All-tiles / mixed / all-residual splits against the reference's spmm."""
+def test_spmm_tiled_matches_reference_golden(threshold, factored):
+    """All-tiles / mixed / all-residual splits against the reference's spmm.
+    factored None: the reference's own aggregation blocks (Â block, its
+    transpose, the SAGE mean block) take the one-byte-record kernel with
+    their diagonal scalings; False: every matrix through the general kernel."""
     meta, z = load_json("spmm_cases.json"), load_npz("spmm_cases.npz")
     for m in meta:
         k, name = m["key"], m["mat"]
         rp, ci, v = z[name + "_rp"], z[name + "_ci"], z[name + "_v"]
         x, y = z[k + "_x"], z[k + "_y"]
-        got, _ = _tiled_run(rp, ci, v, x, m["cols"], threshold, ld_pad=(-x.shape[1]) % 4)
+        got, T = _tiled_run(rp, ci, v, x, m["cols"], threshold, ld_pad=(-x.shape[1]) % 4, factored=factored)
+        assert T.binary == (factored is None and name in ("ahat_block", "ahat_block_T", "mean_block")), name
         tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
         assert np.all(np.abs(got - y) <= tol), (k, threshold, np.abs(got - y).max())
+
+
+def _community_pattern(rng, rows, comm, halo_cols, lo=20, hi=120):
+    ci, rp = [], [0]
+    for r in range(rows):
+        c0 = (r // comm) * comm
+        intra = rng.choice(comm, size=rng.integers(lo, hi), replace=False) + c0
+        halo = rows + rng.choice(halo_cols, size=rng.integers(0, 4), replace=False)
+        c = np.sort(np.concatenate([intra, halo]))
+        ci.append(c)
+        rp.append(rp[-1] + len(c))
+    return np.asarray(rp, dtype=np.int64), np.concatenate(ci).astype(np.int64)
+
+
+@pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn", "gcn_T"])
+@pytest.mark.parametrize("d", [41, 100, 128, 256, 602])
+@pytest.mark.parametrize("threshold", [1, 64])
+def test_spmm_tiled_factored_operators(kind, d, threshold):
+    """The trainer's aggregation operators on community blocks (the Reddit
+    shape in miniature): SAGE mean D^-1 A (row scale), its transpose (column
+    scale, applied through the scratch copy of X), GCN Â = D^-1/2 (A+I)
+    D^-1/2 blocks with halo columns and their transposes (both scales), vs
+    scipy f64 at the fp32 tolerance."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(31 + d)
+    rows, comm, halo = 1500, 300, 2000
+    rp, ci = _community_pattern(rng, rows, comm, halo)
+    cols = rows + halo
+    pat = sp.csr_matrix((np.ones(len(ci)), ci, rp), shape=(rows, cols))
+    if kind.startswith("mean"):
+        deg = np.maximum(np.diff(rp), 1).astype(np.float64)
+        a = sp.diags(1.0 / deg) @ pat
+    else:
+        pat = pat.tolil()
+        pat.setdiag(1.0)                          # self loops on the square part
+        pat = pat.tocsr()
+        dinv = 1.0 / np.sqrt(rng.integers(1, 400, cols).astype(np.float64))
+        a = sp.diags(dinv[:rows]) @ pat @ sp.diags(dinv)
+    if kind.endswith("_T"):
+        a = a.T
+    a = sp.csr_matrix(a)
+    a.sort_indices()
+    v = a.data.astype(np.float32)
+    rp2, ci2 = a.indptr.astype(np.int64), a.indices.astype(np.int64)
+    x = rng.standard_normal((a.shape[1], d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
+    got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True)
+    assert T.binary
+    assert (T.row_scale is None) == (kind == "mean_T") and (T.col_scale is None) == (kind == "mean")
+    tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
+    assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("d", [41, 256])
+def test_spmm_tiled_factored_splits_dense_tiles(d):
+    """A fully dense 128x64 block (8192 one-byte records) exceeds a factored
+    tile's 2048-record slot and becomes several tiles of the same window;
+    the second launch reuses the self-resetting work counter."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5 + d)
+    rows, cols = 300, 400
+    pat = (rng.random((rows, cols)) < 0.05).astype(np.float64)
+    pat[128:256, 64:128] = 1.0
+    deg = np.maximum(pat.sum(1), 1.0)
+    a = sp.csr_matrix(pat / deg[:, None])
+    rp, ci, v = a.indptr.astype(np.int64), a.indices.astype(np.int64), a.data.astype(np.float32)
+    x = rng.standard_normal((cols, d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci, rp), shape=a.shape) @ x.astype(np.float64)
+    for _ in range(2):
+        got, T = _tiled_run(rp, ci, v, x, cols, 64, ld_pad=(-d) % 4, factored=True)
+        assert T.ntiles > int((T.tile_ptr[1:] - T.tile_ptr[:-1]).gt(0).sum())
+        tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
+        assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
+        assert int(T.work.abs().sum()) == 0       # counter pair re-armed by the last CTA
 
 
 @pytest.mark.parametrize("d", [41, 100, 128, 256, 602])
