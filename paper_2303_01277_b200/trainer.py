@@ -764,6 +764,63 @@ def _dist_initialized() -> bool:
         return False
 
 
+def full_forward(features, a_hat, weights: list, cfg: ModelConfig, mean_hat=None, device=None):
+    """``halobit.trainer.full_forward`` (trainer.py:115-126) on the device:
+    the single-machine full-precision forward (no dropout) through the
+    row-gather SpMM and the tcgen05 GEMMs; returns the logits as a float32
+    device tensor (n x C).  ``a_hat`` / ``mean_hat`` are ``CsrMatrix`` (or
+    ``ops.DeviceCsr``); ``weights`` the (fan_in x d_out) arrays."""
+    import torch
+    dev = torch.device(device or "cuda")
+    def dcsr(m):
+        return m if isinstance(m, ops.DeviceCsr) else ops.DeviceCsr.from_csr(m, dev)
+    agg = dcsr(mean_hat if cfg.model == "sage" else a_hat)
+    x = np.asarray(features)
+    n = x.shape[0]
+    h = torch.zeros((n, _ld(x.shape[1])), dtype=torch.float32, device=dev)
+    h[:, :x.shape[1]] = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+    for l, w in enumerate(weights, start=1):
+        din, dout = cfg.widths[l - 1], cfg.widths[l]
+        wp = torch.zeros((w.shape[0], _ld(dout)), dtype=torch.float32, device=dev)
+        wp[:, :dout] = torch.from_numpy(np.asarray(w, dtype=np.float32)).to(dev)
+        p = torch.zeros((n, _ld(din)), dtype=torch.float32, device=dev)
+        ops.spmm(agg, h, p, din)
+        z = torch.zeros((n, _ld(dout)), dtype=torch.float32, device=dev)
+        if cfg.model == "sage":
+            ops.gemm2(h[:, :din], wp[:din, :dout], p[:, :din], wp[din:, :dout], z[:, :dout])
+        else:
+            ops.gemm(p[:, :din], wp[:, :dout], z[:, :dout])
+        if l < cfg.num_layers:
+            ops.relu(z, z, n, dout)
+        h = z
+    return h[:, :cfg.widths[-1]]
+
+
+def evaluate(weights: list, graph: Graph, cfg: ModelConfig, a_hat=None, mean_hat=None,
+             device=None) -> dict:
+    """``halobit.trainer.evaluate`` (trainer.py:129-144): centralized argmax
+    accuracy on the train / val / test masks, computed on the device."""
+    import torch
+    from .graph import mean_adjacency, normalize_adjacency
+    if a_hat is None and cfg.model != "sage":
+        a_hat = normalize_adjacency(graph)
+    if cfg.model == "sage" and mean_hat is None:
+        mean_hat = mean_adjacency(graph)
+    dev = torch.device(device or "cuda")
+    logits = full_forward(graph.features, a_hat, weights, cfg, mean_hat, device=dev)
+    n, C = logits.shape
+    em = np.zeros(n, dtype=np.uint8)
+    em[np.asarray(graph.train_mask, bool)] = 1
+    em[np.asarray(graph.val_mask, bool)] = 2
+    em[np.asarray(graph.test_mask, bool)] = 3
+    counts = torch.zeros(6, dtype=torch.int64, device=dev)
+    labels = torch.from_numpy(np.asarray(graph.labels).astype(np.int32)).to(dev)
+    ops.argmax_accuracy(logits, C, labels, torch.from_numpy(em).to(dev), counts)
+    c = counts.cpu().numpy()
+    names = ("train_acc", "val_acc", "test_acc")
+    return {nm: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0) for k, nm in enumerate(names)}
+
+
 def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMode,
           quant_cfg: QuantConfig, epochs: int, seed: int, lr: float = 0.01, probe=None,
           timeout: float = 60.0, device=None, evaluate_each_epoch: bool = True,
