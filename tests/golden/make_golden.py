@@ -247,9 +247,39 @@ def train_traces():
     (OUT / "train_traces.json").write_text(json.dumps(traces))
 
 
+CLI_CASES = {
+    # name: halobit.cli.ExperimentConfig fields (out is set per case)
+    "cli_config1_b1": dict(synthetic="sbm:k=4,n=2500,pin=0.006,pout=0.0006,d=64,noise=1.0", parts=2,
+                           model="gcn", layers=2, hidden=32, bits=1, epochs=12, seed=1, warmup=3),
+    "cli_config1_b32": dict(synthetic="sbm:k=4,n=2500,pin=0.006,pout=0.0006,d=64,noise=1.0", parts=2,
+                            model="gcn", layers=2, hidden=32, bits=32, epochs=12, seed=1, warmup=3),
+    "cli_sage_async_b2": dict(synthetic="sbm:k=4,n=60,pin=0.2,pout=0.02,d=24", parts=3, partition="hash",
+                              model="sage", layers=3, hidden=16, bits=2, mode="async", staleness=2,
+                              epochs=6, seed=4, warmup=2),
+}
+
+
+def cli_cases():
+    """``halobit.cli.run_experiment`` artefacts (cli.py:122-198): metrics.csv
+    verbatim, summary.json without the wall-clock field."""
+    import tempfile
+    from halobit.cli import ExperimentConfig, run_experiment
+    for name, kw in CLI_CASES.items():
+        with tempfile.TemporaryDirectory() as d:
+            run_experiment(ExperimentConfig(out=d, **kw))
+            (OUT / f"{name}_metrics.csv").write_text((Path(d) / "metrics.csv").read_text())
+            summ = json.loads((Path(d) / "summary.json").read_text())
+            summ.pop("total_wall_ms")
+            summ["config"].pop("out")
+            (OUT / f"{name}_summary.json").write_text(json.dumps(summ, indent=1) + "\n")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["spmm"]:
         spmm_cases()
+        sys.exit(0)
+    if sys.argv[1:] == ["cli"]:
+        cli_cases()
         sys.exit(0)
     spmm_cases()
     stream_cases()
@@ -257,4 +287,5 @@ if __name__ == "__main__":
     multi_peer_case()
     graph_cases()
     train_traces()
+    cli_cases()
     print("golden vectors written to", OUT)
