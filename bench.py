@@ -36,6 +36,7 @@ sys.path.insert(0, str(ROOT))
 
 WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (300, 512, 512, 512, 100)}
 MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn"}
+LOSS = {"reddit": "softmax", "ogbn": "softmax", "yelp": "multilabel"}   # BASELINE configs[3]: multilabel 100
 PARTITIONS = 8
 CPU_SAMPLE_SCALE = 0.125       # oracle-port fallback only (no baseline/_ref): 1/8 of the nodes/edges
 REF_EPOCHS = 2                 # timed halobit.train epochs per reference measurement (after 1 warm-up)
@@ -153,7 +154,14 @@ def _to_halobit_partition(p, hb_graph, hb_linalg):
         id=p.id, num_partitions=p.num_partitions, local_nodes=p.local_nodes, halo_nodes=p.halo_nodes,
         send_sets=list(p.send_sets), recv_sets=list(p.recv_sets), adj_block=csr(p.adj_block),
         mean_block=csr(p.mean_block), features=np.asarray(p.features, dtype=np.float64),
-        labels=p.labels, train_mask=p.train_mask, val_mask=p.val_mask, test_mask=p.test_mask)
+        labels=_single_label(p.labels), train_mask=p.train_mask, val_mask=p.val_mask, test_mask=p.test_mask)
+
+
+def _single_label(labels):
+    """The reference trains only a softmax CE: a multi-label
+    matrix becomes its first positive class for the CPU arm."""
+    lab = np.asarray(labels)
+    return lab.argmax(1).astype(np.int64) if lab.ndim == 2 else lab
 
 
 def reference_epochs(name: str, parts: dict, train_mask, bits: int, mode: str, staleness: int,
@@ -187,6 +195,8 @@ def cpu_epoch_sample(name: str, threads: int, epochs: int = 1, warmup: int = 0):
     sample, sample description, times, scale)."""
     from oracle.epoch import OracleTrainer
     g, parts = build_graph(name, CPU_SAMPLE_SCALE)
+    for p in parts.values():
+        p.labels = _single_label(p.labels)
     o = OracleTrainer([parts[k] for k in sorted(parts)], WIDTHS[name], MODEL[name], "sync", 0, 1, 0,
                       threads=threads)
     for e in range(1, warmup + 1):
@@ -270,7 +280,7 @@ def workload_config(args) -> dict:
                         f"Sylvie-{'S' if args.mode == 'sync' else 'A'}",
             "nodes": spec.num_nodes, "edges": spec.num_edges, "partitions": PARTITIONS,
             "bits": args.bits, "mode": args.mode, "staleness": args.staleness,
-            "model": MODEL[args.config], "widths": list(WIDTHS[args.config]),
+            "model": MODEL[args.config], "widths": list(WIDTHS[args.config]), "loss": LOSS[args.config],
             "scale": getattr(args, "scale", 1.0),
             "l2": "inputs larger than L2 (features 561 MB, aggregation CSR 0.9 GB)" if getattr(args, "scale", 1.0) == 1.0
                   else "reduced-scale diagnostic run"}
@@ -306,7 +316,7 @@ def run_b200(args):
     gnorm = int(g.train_mask.sum())
     train_mask = g.train_mask
     layout = RankLayout(parts, owner, rank)
-    eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config]),
+    eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config], loss=LOSS[args.config]),
                      TrainMode(args.mode, args.staleness), QuantConfig(args.bits), args.seed, 0.01, gnorm,
                      device=torch.device("cuda", local))
     # the step's input features, pinned and laid out like the device buffer

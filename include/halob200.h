@@ -200,6 +200,21 @@ int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const
                     const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
                     double* loss_out, int32_t keep_unmasked, double* partials, void* stream);
 
+/* Multi-label extension (not in the reference, whose only loss is the
+ * softmax CE; used for the Yelp-shaped "multilabel 100" config):
+ * masked sigmoid binary cross-entropy over C labels, labels[i*ldl + c] in
+ * {0, 1}: row_loss[i] = sum_c [max(z,0) - z y + log1p(exp(-|z|))] / (norm C),
+ * grad = (sigmoid(z) - y) / (norm C) (0 outside the mask), f64 math;
+ * *loss_out, keep_unmasked and partials as hb_softmax_xent. */
+int hb_sigmoid_bce(const float* logits, int64_t ld, int32_t n, int32_t C, const uint8_t* labels, int64_t ldl,
+                   const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
+                   double* loss_out, int32_t keep_unmasked, double* partials, void* stream);
+
+/* Multi-label evaluation counts (prediction z > 0) per mask value k = 1..3:
+ * counts[3(k-1)] true positives, +1 false positives, +2 false negatives. */
+int hb_multilabel_counts(const float* logits, int64_t ld, int32_t n, int32_t C, const uint8_t* labels,
+                         int64_t ldl, const uint8_t* mask, int64_t* counts, void* stream);
+
 /* ReLU epilogue (linalg.py:78-80): y = max(z, 0), in place allowed. */
 int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream);
 

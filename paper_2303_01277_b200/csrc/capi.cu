@@ -24,6 +24,10 @@ cudaError_t launch_argmax_accuracy(const float*, int64_t, int, int, const int32_
                                    int64_t*, cudaStream_t);
 cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, uint64_t, float, float*,
                            int64_t, cudaStream_t);
+cudaError_t launch_bce(const float*, int64_t, int, int, const uint8_t*, int64_t, const uint8_t*, double, float*,
+                       int64_t, double*, double*, int, double*, cudaStream_t);
+cudaError_t launch_multilabel_counts(const float*, int64_t, int, int, const uint8_t*, int64_t, const uint8_t*,
+                                     int64_t*, cudaStream_t);
 
 cudaError_t launch_gemm_tf32x3(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
                                float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
@@ -192,6 +196,25 @@ int hb_softmax_xent(const float* logits, int64_t ld, int32_t n, int32_t C, const
   return check(hb::launch_xent(logits, ld, n, C, labels, mask, norm, grad, ldg, row_loss, loss_out, keep_unmasked,
                                partials, S(stream)),
                "hb_softmax_xent");
+}
+
+int hb_sigmoid_bce(const float* logits, int64_t ld, int32_t n, int32_t C, const uint8_t* labels, int64_t ldl,
+                   const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss, double* loss_out,
+                   int32_t keep_unmasked, double* partials, void* stream) {
+  if (n < 0 || C <= 0 || norm <= 0 || !loss_out || ldl < C ||
+      (n > 0 && (!logits || !labels || !mask || !grad || !row_loss)) || (n > 16 * 1024 && !partials))
+    return fail(HB_EINVAL, "hb_sigmoid_bce: bad arguments");
+  return check(hb::launch_bce(logits, ld, n, C, labels, ldl, mask, norm, grad, ldg, row_loss, loss_out,
+                              keep_unmasked, partials, S(stream)),
+               "hb_sigmoid_bce");
+}
+
+int hb_multilabel_counts(const float* logits, int64_t ld, int32_t n, int32_t C, const uint8_t* labels, int64_t ldl,
+                         const uint8_t* mask, int64_t* counts, void* stream) {
+  if (n < 0 || C <= 0 || ldl < C || !counts || (n > 0 && (!logits || !labels || !mask)))
+    return fail(HB_EINVAL, "hb_multilabel_counts: bad arguments");
+  return check(hb::launch_multilabel_counts(logits, ld, n, C, labels, ldl, mask, counts, S(stream)),
+               "hb_multilabel_counts");
 }
 
 int hb_relu(const float* z, int64_t ldz, int32_t n, int32_t d, float* y, int64_t ldy, void* stream) {

@@ -1,7 +1,8 @@
 // Small fused elementwise/row kernels around the halo path (K8):
 // masked softmax-CE + grad (linalg.py:87-112), ReLU / relu' product
 // (linalg.py:78-84, trainer.py:295,312), Adam (linalg.py:115-140),
-// argmax accuracy (trainer.py:129-144) and keyed dropout (trainer.py:285-289).
+// argmax accuracy (trainer.py:129-144), keyed dropout (trainer.py:285-289) and
+// the multi-label sigmoid BCE extension.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "common.cuh"
@@ -212,6 +213,72 @@ __global__ void argmax_acc_kernel(const float* __restrict__ logits, int64_t ld, 
       if (local[k]) atomicAdd(counts + k, local[k]);
 }
 
+// ---- masked multi-label sigmoid BCE (extension: the reference has only the
+// softmax CE; used for the Yelp-shaped multi-label config) ------
+// row loss = sum_c [max(z,0) - z y + log1p(exp(-|z|))] / (norm C); grad =
+// (sigmoid(z) - y) / (norm C); f64 math, one fp32 rounding of the gradient.
+__global__ void bce_rows_kernel(const float* __restrict__ logits, int64_t ld, int n, int C,
+                                const uint8_t* __restrict__ Y, int64_t ldy, const uint8_t* __restrict__ mask,
+                                double norm, float* __restrict__ grad, int64_t ldg, double* __restrict__ row_loss,
+                                int keep_unmasked) {
+  const int lane = threadIdx.x & 31;
+  const double scale = 1.0 / (norm * (double)C);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    float* g = grad + (int64_t)row * ldg;
+    if (!mask[row]) {
+      if (keep_unmasked) continue;
+      for (int c = lane; c < C; c += 32) g[c] = 0.f;
+      if (lane == 0) row_loss[row] = 0.0;
+      continue;
+    }
+    const float* z = logits + (int64_t)row * ld;
+    const uint8_t* y = Y + (int64_t)row * ldy;
+    double s = 0.0;
+    for (int c = lane; c < C; c += 32) {
+      const double zc = (double)z[c], yc = y[c] ? 1.0 : 0.0;
+      s += fmax(zc, 0.0) - zc * yc + log1p(exp(-fabs(zc)));
+      g[c] = (float)((1.0 / (1.0 + exp(-zc)) - yc) * scale);
+    }
+    s = warp_sum_d(s);
+    if (lane == 0) row_loss[row] = s * scale;
+  }
+}
+
+// Multi-label counts per mask value k = 1..3 (train / val / test):
+// counts[3(k-1)] = true positives, +1 false positives, +2 false negatives of
+// the prediction z > 0 (micro-F1 = 2TP / (2TP + FP + FN)).
+__global__ void multilabel_counts_kernel(const float* __restrict__ logits, int64_t ld, int n, int C,
+                                         const uint8_t* __restrict__ Y, int64_t ldy,
+                                         const uint8_t* __restrict__ mask, unsigned long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long local[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    const int mk = mask[row];
+    if (mk < 1 || mk > 3) continue;
+    const float* z = logits + (int64_t)row * ld;
+    const uint8_t* y = Y + (int64_t)row * ldy;
+    unsigned tp = 0, fp = 0, fn = 0;
+    for (int c = lane; c < C; c += 32) {
+      const bool p = z[c] > 0.f, t = y[c] != 0;
+      tp += p && t;
+      fp += p && !t;
+      fn += !p && t;
+    }
+    local[3 * (mk - 1)] += tp;
+    local[3 * (mk - 1) + 1] += fp;
+    local[3 * (mk - 1) + 2] += fn;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    unsigned long long v = local[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(counts + k, v);
+  }
+}
+
 // ---- keyed dropout -----------------------------------------------------------------
 __global__ void dropout_kernel(const float* __restrict__ x, int64_t ldx, int nrows, int64_t row0, int d,
                                uint64_t k0, uint64_t k1, double p, float scale, float* __restrict__ out,
@@ -284,6 +351,32 @@ cudaError_t launch_argmax_accuracy(const float* logits, int64_t ld, int n, int C
   if (n > 0)
     argmax_acc_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, labels, mask,
                                                        reinterpret_cast<unsigned long long*>(counts));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bce(const float* logits, int64_t ld, int n, int C, const uint8_t* Y, int64_t ldy,
+                       const uint8_t* mask, double norm, float* grad, int64_t ldg, double* row_loss,
+                       double* loss_out, int keep_unmasked, double* partials, cudaStream_t st) {
+  if (n > 0)
+    bce_rows_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, Y, ldy, mask, norm, grad, ldg, row_loss,
+                                                    keep_unmasked);
+  if (n <= 16 * 1024) {
+    sum_f64_kernel<<<1, 256, 0, st>>>(row_loss, n, loss_out);
+  } else {
+    if (!partials) return cudaErrorInvalidValue;
+    const int chunk = (n + kSumBlocks - 1) / kSumBlocks;
+    sum_f64_part_kernel<<<kSumBlocks, 256, 0, st>>>(row_loss, n, chunk, partials);
+    sum_f64_kernel<<<1, 256, 0, st>>>(partials, kSumBlocks, loss_out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_multilabel_counts(const float* logits, int64_t ld, int n, int C, const uint8_t* Y, int64_t ldy,
+                                     const uint8_t* mask, int64_t* counts, cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, 9 * sizeof(int64_t), st);
+  if (n > 0)
+    multilabel_counts_kernel<<<grid_for(n, 8), 256, 0, st>>>(logits, ld, n, C, Y, ldy, mask,
+                                                             reinterpret_cast<unsigned long long*>(counts));
   return cudaGetLastError();
 }
 

@@ -90,6 +90,7 @@ class PlantedSpec:
     train_frac: float = 0.6
     val_frac: float = 0.2
     seed: int = 0
+    multilabel: bool = False       # labels: (nodes x classes) 0/1 matrix (Yelp-shaped config)
 
     def __post_init__(self):
         if self.num_nodes < 2 or self.num_edges < 0 or not (0.0 <= self.cut <= 1.0):
@@ -163,8 +164,27 @@ def generate_planted(spec: PlantedSpec) -> Graph:
         feats[blk] += labels[blk, None] == cls_of_col[None, :]
     perm = keyed_generator(spec.seed, "planted-masks").permutation(n)
     tr, va, te = _split_masks(n, perm, (spec.train_frac, spec.val_frac))
-    return Graph(num_nodes=n, edges=edges, features=feats, labels=labels.astype(np.int64),
+    out_labels = _multilabels(spec, comm, labels) if spec.multilabel else labels.astype(np.int64)
+    return Graph(num_nodes=n, edges=edges, features=feats, labels=out_labels,
                  train_mask=tr, val_mask=va, test_mask=te, num_classes=spec.num_classes)
+
+
+def _multilabels(spec: PlantedSpec, comm: np.ndarray, primary: np.ndarray) -> np.ndarray:
+    """(nodes x classes) 0/1 labels: each community owns a label set (its
+    primary class — the one the features carry — plus ~5 % of the others);
+    every node takes its community's set with 1 % of the entries flipped."""
+    K = spec.num_classes
+    rng = keyed_generator(spec.seed, "planted-multilabels")
+    ncomm = int(comm.max()) + 1 if len(comm) else 0
+    sets = rng.random((ncomm, K)) < 0.05
+    sets[np.arange(ncomm), np.arange(ncomm) % K] = True
+    out = np.empty((len(comm), K), dtype=np.uint8)
+    for start in range(0, len(comm), 1 << 16):
+        blk = slice(start, min(len(comm), start + (1 << 16)))
+        flip = rng.random((blk.stop - blk.start, K)) < 0.01
+        out[blk] = sets[comm[blk]] ^ flip
+    out[np.arange(len(comm)), primary] = 1
+    return out
 
 
 # BASELINE.json configs (shapes from PAPER.md Table "dataset info" and the
@@ -176,7 +196,7 @@ REDDIT = PlantedSpec(num_nodes=232_965, num_edges=114_615_892, feature_dim=602,
 OGBN_PRODUCTS = PlantedSpec(num_nodes=2_449_029, num_edges=61_859_140, feature_dim=100,
                             num_classes=47, cut=0.03, train_frac=0.08, val_frac=0.02, seed=2303)
 YELP = PlantedSpec(num_nodes=716_847, num_edges=13_954_820, feature_dim=300,
-                   num_classes=100, cut=0.05, train_frac=0.75, val_frac=0.10, seed=2303)
+                   num_classes=100, cut=0.05, train_frac=0.75, val_frac=0.10, seed=2303, multilabel=True)
 
 
 def scaled(spec: PlantedSpec, factor: float) -> PlantedSpec:

@@ -292,6 +292,25 @@ def softmax_xent(logits, C: int, labels, mask, norm: float, grad, row_loss, loss
               ptr(partials), stream_handle(stream))
 
 
+def sigmoid_bce(logits, C: int, labels, mask, norm: float, grad, row_loss, loss_out, stream=None,
+                keep_unmasked: bool = False, partials=None):
+    """Multi-label sigmoid BCE (extension; include/halob200.h hb_sigmoid_bce).
+    labels: uint8 (n x C) 0/1 matrix."""
+    import torch
+    n = labels.shape[0]
+    if partials is None and n > 16 * 1024:
+        partials = torch.empty(XENT_PARTIALS, dtype=torch.float64, device=logits.device)
+    _lib.call("hb_sigmoid_bce", ptr(logits), logits.stride(0), n, C, ptr(labels), labels.stride(0), ptr(mask),
+              float(norm), ptr(grad), grad.stride(0), ptr(row_loss), ptr(loss_out), int(bool(keep_unmasked)),
+              ptr(partials), stream_handle(stream))
+
+
+def multilabel_counts(logits, C: int, labels, mask, counts, stream=None):
+    """TP / FP / FN per mask value (hb_multilabel_counts), counts: int64[9]."""
+    _lib.call("hb_multilabel_counts", ptr(logits), logits.stride(0), labels.shape[0], C, ptr(labels),
+              labels.stride(0), ptr(mask), ptr(counts), stream_handle(stream))
+
+
 def relu(z, y, n: int, d: int, stream=None):
     """``linalg.relu`` (linalg.py:78-80)."""
     _lib.call("hb_relu", ptr(z), z.stride(0), n, d, ptr(y), y.stride(0), stream_handle(stream))

@@ -42,11 +42,20 @@ class TrainingError(RuntimeError):
     pass
 
 
+LOSSES = ("softmax", "multilabel")
+
+
 @dataclass(frozen=True)
 class ModelConfig:
+    """``trainer.py:32-45``.  ``loss`` is an extension (default = the
+    reference's masked softmax CE): "multilabel" trains a sigmoid BCE over a
+    (nodes x classes) 0/1 label matrix and evaluates micro-F1 (the Yelp-shaped
+    "multilabel 100" config; not in the reference)."""
+
     widths: tuple
     model: str = "gcn"
     dropout: float = 0.0
+    loss: str = "softmax"
 
     def __post_init__(self):
         if len(self.widths) < 2 or any(w <= 0 for w in self.widths):
@@ -55,6 +64,8 @@ class ModelConfig:
             raise TrainingError(f"unknown model {self.model!r}")
         if not (0.0 <= self.dropout < 1.0):
             raise TrainingError("dropout must be in [0, 1)")
+        if self.loss not in LOSSES:
+            raise TrainingError(f"unknown loss {self.loss!r}")
 
     @property
     def num_layers(self) -> int:
@@ -235,9 +246,16 @@ class DeviceRank:
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
         self.xent_partials = torch.zeros(ops.XENT_PARTIALS, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(6, dtype=torch.int64, device=dev)
-        labels = np.concatenate([np.asarray(p.labels) for p in layout.parts]).astype(np.int32)
-        self.labels = torch.from_numpy(labels).to(dev)
+        self.counts = torch.zeros(9, dtype=torch.int64, device=dev)
+        self.multilabel = cfg.loss == "multilabel"
+        if self.multilabel:
+            labels = np.concatenate([np.asarray(p.labels).reshape(p.num_local, -1) for p in layout.parts])
+            if labels.shape[1] != W[L]:
+                raise TrainingError(f"multilabel labels have {labels.shape[1]} columns, output width {W[L]}")
+            self.labels = torch.from_numpy(np.ascontiguousarray(labels, dtype=np.uint8)).to(dev)
+        else:
+            labels = np.concatenate([np.asarray(p.labels) for p in layout.parts]).astype(np.int32)
+            self.labels = torch.from_numpy(labels).to(dev)
         tm = np.concatenate([np.asarray(p.train_mask, dtype=bool) for p in layout.parts])
         self.train_mask = torch.from_numpy(tm.astype(np.uint8)).to(dev)
         em = np.zeros(NL, dtype=np.uint8)
@@ -585,8 +603,9 @@ class DeviceRank:
         C = W[L]
         # JL / row_loss rows outside the train mask are zero from allocation and
         # never written: the CE kernel skips them
-        ops.softmax_xent(logits, C, self.labels, self.train_mask, self.norm, self.JL,
-                         self.row_loss, self.loss_dev, keep_unmasked=True, partials=self.xent_partials)
+        loss_fn = ops.sigmoid_bce if self.multilabel else ops.softmax_xent
+        loss_fn(logits, C, self.labels, self.train_mask, self.norm, self.JL,
+                self.row_loss, self.loss_dev, keep_unmasked=True, partials=self.xent_partials)
         self.launches += 2
         J = self.JL
         for l in range(L, 0, -1):
@@ -679,7 +698,10 @@ class DeviceRank:
             self.xeval = {l: ExchangeBuffers(self.layout, self.layout.fwd, self.cfg.widths[l - 1], 32,
                                              self.dev, 1) for l in range(1, self.L + 1)}
         logits = self.forward(0, "sync", training=False)
-        ops.argmax_accuracy(logits, self.cfg.widths[-1], self.labels, self.eval_mask, self.counts)
+        if self.multilabel:
+            ops.multilabel_counts(logits, self.cfg.widths[-1], self.labels, self.eval_mask, self.counts)
+        else:
+            ops.argmax_accuracy(logits, self.cfg.widths[-1], self.labels, self.eval_mask, self.counts)
         if self.world > 1:
             import torch.distributed as dist
             from .transport import host_staged
@@ -689,10 +711,7 @@ class DeviceRank:
                 self.counts.copy_(c)
             else:
                 dist.all_reduce(self.counts, group=self.group)
-        c = self.counts.cpu().numpy()
-        names = ("train_acc", "val_acc", "test_acc")
-        return {n: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0)
-                for k, n in enumerate(names)}
+        return _accuracies(self.counts.cpu().numpy(), self.multilabel)
 
     def weights_host(self) -> list:
         return [w.double().cpu().numpy() for w in self.W]
@@ -706,6 +725,18 @@ class DeviceRank:
             t.messages_sent += s.messages_sent
             t.allreduce_bytes += s.allreduce_bytes
         return t.snapshot()
+
+
+def _accuracies(c, multilabel: bool) -> dict:
+    """train/val/test accuracy from argmax counts; micro-F1 for multi-label."""
+    names = ("train_acc", "val_acc", "test_acc")
+    if multilabel:
+        out = {}
+        for k, n in enumerate(names):
+            tp, fp, fn = (float(x) for x in c[3 * k:3 * k + 3])
+            out[n] = 2 * tp / (2 * tp + fp + fn) if (2 * tp + fp + fn) else 0.0
+        return out
+    return {n: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0) for k, n in enumerate(names)}
 
 
 def reduce_gradients(gflat, loss, group=None):
@@ -813,12 +844,15 @@ def evaluate(weights: list, graph: Graph, cfg: ModelConfig, a_hat=None, mean_hat
     em[np.asarray(graph.train_mask, bool)] = 1
     em[np.asarray(graph.val_mask, bool)] = 2
     em[np.asarray(graph.test_mask, bool)] = 3
-    counts = torch.zeros(6, dtype=torch.int64, device=dev)
-    labels = torch.from_numpy(np.asarray(graph.labels).astype(np.int32)).to(dev)
-    ops.argmax_accuracy(logits, C, labels, torch.from_numpy(em).to(dev), counts)
-    c = counts.cpu().numpy()
-    names = ("train_acc", "val_acc", "test_acc")
-    return {nm: (float(c[2 * k + 1]) / float(c[2 * k]) if c[2 * k] else 0.0) for k, nm in enumerate(names)}
+    counts = torch.zeros(9, dtype=torch.int64, device=dev)
+    mask = torch.from_numpy(em).to(dev)
+    if cfg.loss == "multilabel":
+        labels = torch.from_numpy(np.ascontiguousarray(graph.labels, dtype=np.uint8)).to(dev)
+        ops.multilabel_counts(logits, C, labels, mask, counts)
+    else:
+        labels = torch.from_numpy(np.asarray(graph.labels).astype(np.int32)).to(dev)
+        ops.argmax_accuracy(logits, C, labels, mask, counts)
+    return _accuracies(counts.cpu().numpy(), cfg.loss == "multilabel")
 
 
 def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMode,

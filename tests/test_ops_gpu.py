@@ -80,3 +80,37 @@ def test_adam_matches_oracle():
         w_ref = opt.step(w_ref, gr.astype(np.float64))
         ops.adam_step(w, torch.from_numpy(gr).cuda(), m, v, 0.01, t)
     np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-6, atol=1e-6)   # fp32 storage of w, m, v
+
+
+@pytest.mark.parametrize("n,C", [(1000, 100), (20000, 7)])
+def test_sigmoid_bce_multilabel_vs_torch_f64(n, C):
+    """Multi-label extension (not in the reference): masked sigmoid BCE loss
+    and gradient vs a torch float64 restatement (mean over labels, global
+    normaliser); rel 1e-6 on the loss, 1e-7 absolute on the gradient."""
+    from paper_2303_01277_b200 import ops
+    rng = np.random.default_rng(n + C)
+    z = torch.from_numpy((rng.standard_normal((n, C)) * 4).astype(np.float32)).cuda()
+    y = torch.from_numpy((rng.random((n, C)) < 0.1).astype(np.uint8)).cuda()
+    mask = torch.from_numpy((rng.random(n) < 0.7).astype(np.uint8)).cuda()
+    norm = float(mask.sum()) + 5.0
+    zd, yd, md = z.double(), y.double(), mask.bool()
+    per = torch.nn.functional.binary_cross_entropy_with_logits(zd, yd, reduction="none")
+    loss_ref = float(per[md].sum() / (norm * C))
+    grad_ref = torch.where(md[:, None], (torch.sigmoid(zd) - yd) / (norm * C), torch.zeros_like(zd))
+    ld = (C + 3) // 4 * 4
+    L = torch.zeros(n, ld, device="cuda")
+    L[:, :C] = z
+    grad = torch.full((n, ld), 5.0, device="cuda")
+    row_loss = torch.zeros(n, dtype=torch.float64, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.sigmoid_bce(L, C, y, mask, norm, grad, row_loss, loss)
+    assert float(loss) == pytest.approx(loss_ref, rel=1e-6)
+    assert float((grad[:, :C].double() - grad_ref).abs().max()) <= 1e-7
+    counts = torch.zeros(9, dtype=torch.int64, device="cuda")
+    em = torch.from_numpy(rng.integers(0, 4, n).astype(np.uint8)).cuda()
+    ops.multilabel_counts(L, C, y, em, counts)
+    pred, tgt = z > 0, y.bool()
+    for k in range(3):
+        sel = em == k + 1
+        want = [int((pred & tgt)[sel].sum()), int((pred & ~tgt)[sel].sum()), int((~pred & tgt)[sel].sum())]
+        assert counts[3 * k:3 * k + 3].tolist() == want

@@ -309,3 +309,30 @@ def test_wide_hidden_small_graph_pre_order(model):
     for m, lo in zip(res.metrics, losses):
         assert m.train_loss == pytest.approx(lo, rel=5e-5)
     assert _wdiff(res.final_weights, o.weights) < 1e-4
+
+
+def test_multilabel_training_serial_equivalence():
+    """Multi-label extension (Yelp-shaped config, BCE + micro-F1; not in the
+    reference): passthrough halos make a 3-partition run equal the
+    1-partition run (the reference's serial-equivalence property,
+    tests/test_acceptance.py:154-164), the loss falls, and the trainer's
+    micro-F1 equals the module-level evaluate on the final weights."""
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.datasets import PlantedSpec, generate_planted
+    from paper_2303_01277_b200.graph import build_partitions
+    from paper_2303_01277_b200.trainer import ModelConfig, TrainMode, evaluate, train
+    g = generate_planted(PlantedSpec(num_nodes=3000, num_edges=60000, feature_dim=40, num_classes=12,
+                                     communities=12, cut=0.05, seed=3, multilabel=True))
+    cfg = ModelConfig((40, 32, 12), "gcn", loss="multilabel")
+    runs = []
+    for n in (1, 3):
+        parts = build_partitions(g, n, "contiguous", 0, "gcn")[2]
+        runs.append(train(g, parts, cfg, TrainMode(), QuantConfig(32), 12, 4, lr=0.02))
+    a, b = runs
+    for ma, mb in zip(a.metrics, b.metrics):
+        assert ma.train_loss == pytest.approx(mb.train_loss, rel=5e-5)
+    assert _wdiff(b.final_weights, a.final_weights) < 1e-4
+    assert a.metrics[-1].train_loss < 0.8 * a.metrics[0].train_loss
+    acc = evaluate(a.final_weights, g, cfg)
+    assert acc["test_acc"] == pytest.approx(a.metrics[-1].test_acc, abs=2e-3)
+    assert 0.0 < acc["test_acc"] <= 1.0

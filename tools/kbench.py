@@ -97,18 +97,21 @@ def spmm(args):
         X = torch.randn(M.cols, ld, device="cuda")
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
-        variants = [("rows", 0)] + ([("tiled", 0)] if args.config == "reddit" else []) + \
+        variants = [("rows", 0)] + ([("tiled", 0), ("tiled_bin", 0)] if args.config == "reddit" else []) + \
             ([("rows", 4), ("rows", 16)] if d <= 64 else []) + ([("rows", 1), ("rows", 4)] if d > 256 else [])
+        if args.tiled_only:
+            variants = [v for v in variants if v[0].startswith("tiled")]
         for algo, win in variants:
-            if algo == "tiled":
-                if name not in tiled:
+            if algo.startswith("tiled"):
+                key = (name, algo)
+                if key not in tiled:
                     t0 = time.time()
-                    tiled[name] = ops.TiledCsr(M)
+                    tiled[key] = ops.TiledCsr(M, factored=algo == "tiled_bin")
                     torch.cuda.synchronize()
-                    print(json.dumps({"tiled": name, "build_s": round(time.time() - t0, 2),
-                                      "tiles": tiled[name].ntiles,
-                                      "tiled_fraction": round(tiled[name].tiled_fraction, 4)}), flush=True)
-                T = tiled[name]
+                    print(json.dumps({"tiled": name, "algo": algo, "build_s": round(time.time() - t0, 2),
+                                      "tiles": tiled[key].ntiles,
+                                      "tiled_fraction": round(tiled[key].tiled_fraction, 4)}), flush=True)
+                T = tiled[key]
                 ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
             else:
                 sc = lay.NL if name == "A" else None
@@ -192,5 +195,6 @@ if __name__ == "__main__":
     ap.add_argument("--segs", type=int, default=56)
     ap.add_argument("--config", default="reddit")
     ap.add_argument("--d-list", type=int, nargs="*", default=None)
+    ap.add_argument("--tiled-only", action="store_true")
     a = ap.parse_args()
     {"codec": codec, "spmm": spmm, "gemm": gemm}[a.what](a)
