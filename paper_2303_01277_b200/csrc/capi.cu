@@ -42,7 +42,8 @@ cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, con
                               float*, int64_t, int*, cudaStream_t);
 cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                                   const uint8_t*, const int64_t*, const int32_t*, const float*, const float*,
-                                  const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, cudaStream_t);
+                                  const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, int,
+                                  cudaStream_t);
 
 int num_sms() {
   static int cached = 0;
@@ -143,13 +144,15 @@ int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32
                       const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
                       const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                       const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
-                      float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, void* stream) {
-  if (nrows < 0 || d < 0 || ldx < d || ldy < d || nblocks != (nrows + 127) / 128 ||
+                      float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, int32_t block_rows,
+                      void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (block_rows != 64 && block_rows != 128) ||
+      nblocks != (nrows + block_rows - 1) / block_rows ||
       (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y || !work)) || (col_scale && (!xs || ldxs < d)))
     return fail(HB_EINVAL, "hb_spmm_tiled_bin: bad arguments");
   const cudaError_t e = hb::launch_spmm_tiled_bin(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_rowoff,
                                                   tile_rec, res_ptr, res_col, row_scale, col_scale, X, ldx, d, Y,
-                                                  ldy, xs, ldxs, work, S(stream));
+                                                  ldy, xs, ldxs, work, block_rows, S(stream));
   if (e == cudaErrorNotSupported)
     return fail(HB_EINVAL, "hb_spmm_tiled_bin: X/Y need 16-byte aligned rows (ld % 4 == 0)");
   return check(e, "hb_spmm_tiled_bin");

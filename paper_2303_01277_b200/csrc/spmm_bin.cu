@@ -13,9 +13,8 @@
 // read 16 at a time with one broadcast LDS.128 and unpacked in registers, so
 // the shared-memory datapath — the binding resource of a SIMT SpMM — carries
 // only the gathered X rows: 8 wavefronts per nonzero at d = 256 instead of 9.
-// Row blocks are 128 rows tall (16 consumer warps x 8 rows): the TMA-staged
-// 64-row X window is reused by twice as many rows as in the general kernel,
-// halving the staging traffic per nonzero.  c is applied by a pre-pass into a
+// Row blocks are 64 or 128 rows tall (16 consumer warps x 4 or 8 rows); taller
+// blocks reuse each TMA-staged 64-row X window across more rows.  c is applied by a pre-pass into a
 // caller-provided scratch copy of X (one HBM read + write of X), r to the
 // accumulators before the store.
 //
@@ -33,13 +32,12 @@
 namespace hb {
 namespace sb {
 
-constexpr int kRB = 128;          // rows per block
 constexpr int kW = 64;            // columns per window (a record is col - c0 < 64)
-constexpr int kRowOff = 136;      // u16 row offsets per tile (129 used; 272 bytes)
-constexpr int kRPW = 8;           // rows per consumer warp
 constexpr int kMaxRec = 2048;     // record bytes per tile (ops.TiledCsr splits denser tiles)
-constexpr int kConsumers = kRB / kRPW;
+constexpr int kConsumers = 16;    // consumer warps; a warp owns RB / 16 rows of the block
 constexpr int kThreads = 32 * (kConsumers + 1);
+// u16 row offsets per tile: RB + 1 used, padded to a 16-byte multiple
+constexpr int row_off_count(int rb) { return rb == 128 ? 136 : 72; }
 constexpr int kQ = 4;
 
 struct Args {
@@ -48,7 +46,7 @@ struct Args {
   const int32_t* tile_ptr;
   const int32_t* tile_win;
   const int64_t* tile_off;        // byte offsets of each tile's records (multiples of 16)
-  const uint16_t* tile_rowoff;    // [ntiles][kRowOff]
+  const uint16_t* tile_rowoff;    // [ntiles][row_off_count(RB)]
   const uint8_t* tile_rec;
   const int64_t* res_ptr;         // residual pattern (CSR without values)
   const int32_t* res_col;
@@ -59,11 +57,11 @@ struct Args {
   int64_t ldy;
 };
 
-template <int NV, int G, int S>
+template <int RB, int NV, int G, int S>
 struct Smem {
   static constexpr int P = 4 * G * NV;
   static constexpr int X_BYTES = kW * P * 4;
-  static constexpr int RO_BYTES = kRowOff * 2;
+  static constexpr int RO_BYTES = row_off_count(RB) * 2;
   static constexpr int STAGE = X_BYTES + kMaxRec + RO_BYTES + 112;   // 16-byte multiple
   static constexpr int TOTAL = S * STAGE + 128;
   static_assert(STAGE % 16 == 0, "stage alignment");
@@ -99,13 +97,19 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 
 // 1 CTA/SM: 17 warps are allocated registers as 20 (4-warp granularity), so
 // 96 per thread is the most that launches; 2 CTAs/SM: 56
-template <int NV, int G, int S, int MINB>
+// RB rows per block (kRPW = RB / 16 per warp), NV float4 per lane, G lanes
+// per row group, S ring stages, MINB CTAs per SM, U records in flight per
+// warp (G == 32)
+template <int RB, int NV, int G, int S, int MINB, int U>
 __global__ void __maxnreg__(MINB == 1 ? 96 : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
-  using S_ = Smem<NV, G, S>;
+  using S_ = Smem<RB, NV, G, S>;
   constexpr int P = S_::P;
+  constexpr int kRPW = RB / kConsumers;
+  constexpr int kRowOff = row_off_count(RB);
   constexpr int NG = 32 / G;             // lane groups per warp (each owns whole rows)
   constexpr int RPG = kRPW / NG;         // rows per lane group
+  static_assert(RPG >= 1 && kRPW % NG == 0, "row split");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   __shared__ __align__(8) uint64_t full[S], empty[S], ifull[kQ], iempty[kQ];
@@ -177,7 +181,7 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
     if (lane == 0) mbar_arrive_cta(&iempty[q]);
     if (item >= items) break;
     const int b = item / a.npanels, pn = item % a.npanels;
-    const int r0 = b * kRB + warp * kRPW;
+    const int r0 = b * RB + warp * kRPW;
     const int col0 = pn * P;
     float4 acc[RPG][NV];
 #pragma unroll
@@ -199,10 +203,29 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
           const uint4 c = *reinterpret_cast<const uint4*>(rec + kb);       // 16 records, one broadcast
           int p = k > kb ? k - kb : 0;
           const int pe = k1 - kb < 16 ? k1 - kb : 16;
-          if constexpr (NV >= 2 && G == 32) {
-            // wide rows: one X row (NV float4 per lane) in flight per record
+          if constexpr (G == 32) {
+            // U records (U X rows of NV float4 per lane) in flight per warp
+            for (; p + U <= pe; p += U) {
+              float4 x[U][NV];
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int j = rec_byte(c, p + u);
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  if (v < NV - 1 || nlast) x[u][v] = xs[j * pw4 + v * G];
+              }
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  if (v < NV - 1 || nlast) {
+                    acc[i][v].x += x[u][v].x; acc[i][v].y += x[u][v].y;
+                    acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
+                  }
+            }
             for (; p < pe; ++p) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
           } else {
+            // narrow rows: each lane group walks its own row, two records at a time
             for (; p + 1 < pe; p += 2) {
               const int j0 = rec_byte(c, p), j1 = rec_byte(c, p + 1);
               float4 x0[NV], x1[NV];
@@ -221,8 +244,8 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
                 }
               }
             }
+            if (p < pe) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
           }
-          if (p < pe) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
         }
       }
       __syncwarp();
@@ -289,9 +312,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int NV, int G, int S, int MINB = 1>
+template <int RB, int NV, int G, int S, int MINB, int U>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
-  using S_ = Smem<NV, G, S>;
+  using S_ = Smem<RB, NV, G, S>;
   static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
   Args a = a0;
   a.npanels = (a.d + S_::P - 1) / S_::P;
@@ -309,14 +332,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<NV, G, S, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, U>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
-  if (grid > 0) spmm_bin_kernel<NV, G, S, MINB><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, U><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -327,7 +350,7 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
                                   const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                                   const float* row_scale, const float* col_scale, const float* X, int64_t ldx,
                                   int d, float* Y, int64_t ldy, float* xs, int64_t ldxs, int* work,
-                                  cudaStream_t stream) {
+                                  int block_rows, cudaStream_t stream) {
   if (nrows <= 0 || d <= 0) return cudaSuccess;
   if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
   if (col_scale) {
@@ -347,9 +370,18 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-  if (d <= 64) return sb::launch_nv<2, 8, 4, 2>(a, xrows, stream);      // 4 rows of a warp in parallel
-  if (d <= 128) return sb::launch_nv<1, 32, 5>(a, xrows, stream);
-  return sb::launch_nv<2, 32, 3>(a, xrows, stream);                        // 256-column panels
+  // HB_BIN_VARIANT (tuning): 1 = one X row in flight per warp at 256-column
+  // panels (128-row blocks only)
+  static const int variant = getenv("HB_BIN_VARIANT") ? atoi(getenv("HB_BIN_VARIANT")) : 0;
+  if (block_rows == 64) {
+    if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2, 1>(a, xrows, stream);   // 4 rows of a warp in parallel
+    if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1, 4>(a, xrows, stream);
+    return sb::launch_nv<64, 2, 32, 3, 1, 4>(a, xrows, stream);              // 256-column panels
+  }
+  if (block_rows != 128) return cudaErrorInvalidValue;
+  if (d <= 64) return sb::launch_nv<128, 2, 8, 4, 2, 1>(a, xrows, stream);
+  if (d <= 128 || variant != 1) return sb::launch_nv<128, 1, 32, 5, 1, 4>(a, xrows, stream);
+  return sb::launch_nv<128, 2, 32, 3, 1, 1>(a, xrows, stream);
 }
 
 }  // namespace hb

@@ -103,12 +103,13 @@ class TiledCsr:
     * general (``hb_spmm_tiled``): 64-row blocks, 8-byte {col, val} records;
     * factored (``hb_spmm_tiled_bin``, when ``factor_scales`` finds the values
       to be r[i] c[j] over a 0/1 pattern — the trainer's aggregation
-      operators): 128-row blocks, one-byte column records, r / c applied as
-      diagonal scalings."""
+      operators): 64- or 128-row blocks, one-byte column records, r / c
+      applied as diagonal scalings."""
 
     W = 64
 
-    def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None):
+    def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None,
+                 block_rows: int | None = None):
         import torch
         dev = a.row_ptr.device
         scales = factor_scales(a) if factored in (None, True) else None
@@ -116,7 +117,14 @@ class TiledCsr:
             raise ValueError("matrix values do not factor into diagonal scalings of a 0/1 pattern")
         self.binary = scales is not None
         self.row_scale, self.col_scale = scales if self.binary else (None, None)
-        self.RB, self.ROWOFF, self.MAXREC = (128, 136, 2048) if self.binary else (64, 72, 1024)
+        if self.binary:
+            import os
+            rb = block_rows or int(os.environ.get("HB_BIN_RB", "64"))
+            if rb not in (64, 128):
+                raise ValueError(f"factored tiles are 64 or 128 rows, not {rb}")
+            self.RB, self.ROWOFF, self.MAXREC = rb, (136 if rb == 128 else 72), 2048
+        else:
+            self.RB, self.ROWOFF, self.MAXREC = 64, 72, 1024
         self.rows, self.cols, self.nnz = a.rows, a.cols, a.nnz
         self.work = torch.zeros(2, dtype=torch.int32, device=dev)
         self._xs = {}
@@ -209,7 +217,7 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
         _lib.call("hb_spmm_tiled_bin", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),
                   ptr(t.tile_off), ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col),
                   ptr(t.row_scale), ptr(t.col_scale), ptr(x), x.stride(0), d, ptr(out), out.stride(0),
-                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), stream_handle(stream))
+                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), t.RB, stream_handle(stream))
         return out
     _lib.call("hb_spmm_tiled", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win), ptr(t.tile_off),
               ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col), ptr(t.res_val), ptr(x),

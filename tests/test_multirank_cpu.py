@@ -1,4 +1,5 @@
-"""Multi-rank halo exchange over torch.distributed (gloo, world size 2, CPU).
+"""Multi-rank halo exchange over torch.distributed (gloo, world sizes 2, 4 and
+8, CPU).
 
 The N>1 device path (one rank per GPU, NCCL) runs the same host code as here:
 ``RankLayout`` splits the partitions over ranks, ``ExchangeBuffers`` lays the
@@ -37,11 +38,16 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _parts():
+# world size -> partition owners (non-contiguous: every rank's partitions are
+# interleaved with other ranks')
+OWNERS = {2: [0, 1, 0, 1], 4: [1, 0, 3, 2, 1, 0, 3, 2], 8: [3, 0, 6, 1, 7, 2, 5, 4]}
+
+
+def _parts(n):
     from paper_2303_01277_b200.datasets import SbmSpec, generate_sbm
     from paper_2303_01277_b200.graph import build_partitions
-    g = generate_sbm(SbmSpec(nodes_per_community=25, communities=4, feature_dim=D, seed=3))
-    return build_partitions(g, 4, "hash", 0, "gcn")[2]
+    g = generate_sbm(SbmSpec(nodes_per_community=25 if n == 4 else 15, communities=n, feature_dim=D, seed=3))
+    return build_partitions(g, n, "hash", 0, "gcn")[2]
 
 
 def _rows(p, peer, phase):
@@ -85,10 +91,23 @@ def _check(rank, world):
     from oracle.codec import dequantize, parse_wire_block
     from paper_2303_01277_b200.rngstream import BACKWARD, FORWARD
     from paper_2303_01277_b200.transport import ExchangeBuffers, RankLayout, nccl_exchange
-    parts = _parts()
-    owner = [0, 1, 0, 1]                      # non-contiguous ownership
+    owner = OWNERS[world]
+    parts = _parts(len(owner))
     lay = RankLayout({p.id: p for p in parts if owner[p.id] == rank}, owner, rank)
     checked = 0
+    # every rank plans the same P2P traffic: what rank a sends to rank b is
+    # what b expects from a, for every (layer width, bits, phase)
+    for plan in (lay.fwd, lay.bwd):
+        for bits in (1, 32):
+            bufs = ExchangeBuffers(lay, plan, D, bits, "cpu", parities=1)
+            mine = {"send": {r: n for r, (o, n) in bufs.send_group.items()},
+                    "recv": {r: n for r, (o, n) in bufs.recv_group.items() if r != rank}}
+            allp = [None] * world
+            dist.all_gather_object(allp, mine)
+            for a in range(world):
+                for b in range(world):
+                    if a != b:
+                        assert allp[a]["send"].get(b, 0) == allp[b]["recv"].get(a, 0), (a, b, bits)
     for phase, plan in ((FORWARD, lay.fwd), (BACKWARD, lay.bwd)):
         for bits in (1, 4, 32):
             want = _expected_blocks(parts, phase, bits)
@@ -141,7 +160,8 @@ def _check(rank, world):
     g = torch.full((7,), float(rank + 1))
     loss = torch.tensor([0.25 * (rank + 1)], dtype=torch.float64)
     reduce_gradients(g, loss)
-    assert torch.all(g == 3.0) and float(loss) == 0.75
+    tot = world * (world + 1) / 2
+    assert torch.all(g == tot) and float(loss) == 0.25 * tot
     return checked
 
 
@@ -158,11 +178,12 @@ def _worker(rank, world, port, q):
             dist.destroy_process_group()
 
 
-def test_two_rank_halo_exchange_matches_reference_semantics():
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multi_rank_halo_exchange_matches_reference_semantics(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]

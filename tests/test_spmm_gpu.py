@@ -76,11 +76,11 @@ def test_spmm_random_power_law_rows(d):
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None):
+def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None, block_rows=None):
     from paper_2303_01277_b200 import ops
     rows, d = len(rp) - 1, x.shape[1]
     A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
-    T = ops.TiledCsr(A, threshold=threshold, factored=factored)
+    T = ops.TiledCsr(A, threshold=threshold, factored=factored, block_rows=block_rows)
     X = torch.zeros(ncols, d + ld_pad, device="cuda")
     X[:, :d] = torch.from_numpy(x)
     Y = torch.full((rows, d + ld_pad), 7.0, device="cuda")
@@ -121,10 +121,11 @@ def _community_pattern(rng, rows, comm, halo_cols, lo=20, hi=120):
     return np.asarray(rp, dtype=np.int64), np.concatenate(ci).astype(np.int64)
 
 
+@pytest.mark.parametrize("rb", [64, 128])
 @pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn", "gcn_T"])
 @pytest.mark.parametrize("d", [41, 100, 128, 256, 602])
 @pytest.mark.parametrize("threshold", [1, 64])
-def test_spmm_tiled_factored_operators(kind, d, threshold):
+def test_spmm_tiled_factored_operators(kind, d, threshold, rb):
     """The trainer's aggregation operators on community blocks (the Reddit
     shape in miniature): SAGE mean D^-1 A (row scale), its transpose (column
     scale, applied through the scratch copy of X), GCN Â = D^-1/2 (A+I)
@@ -153,15 +154,16 @@ def test_spmm_tiled_factored_operators(kind, d, threshold):
     rp2, ci2 = a.indptr.astype(np.int64), a.indices.astype(np.int64)
     x = rng.standard_normal((a.shape[1], d)).astype(np.float32)
     ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
-    got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True)
-    assert T.binary
+    got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=rb)
+    assert T.binary and T.RB == rb
     assert (T.row_scale is None) == (kind == "mean_T") and (T.col_scale is None) == (kind == "mean")
     tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
+@pytest.mark.parametrize("rb", [64, 128])
 @pytest.mark.parametrize("d", [41, 256])
-def test_spmm_tiled_factored_splits_dense_tiles(d):
+def test_spmm_tiled_factored_splits_dense_tiles(d, rb):
     """A fully dense 128x64 block (8192 one-byte records) exceeds a factored
     tile's 2048-record slot and becomes several tiles of the same window;
     the second launch reuses the self-resetting work counter."""
@@ -176,7 +178,7 @@ def test_spmm_tiled_factored_splits_dense_tiles(d):
     x = rng.standard_normal((cols, d)).astype(np.float32)
     ref = sp.csr_matrix((v.astype(np.float64), ci, rp), shape=a.shape) @ x.astype(np.float64)
     for _ in range(2):
-        got, T = _tiled_run(rp, ci, v, x, cols, 64, ld_pad=(-d) % 4, factored=True)
+        got, T = _tiled_run(rp, ci, v, x, cols, 64, ld_pad=(-d) % 4, factored=True, block_rows=rb)
         assert T.ntiles > int((T.tile_ptr[1:] - T.tile_ptr[:-1]).gt(0).sum())
         tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
         assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()

@@ -97,7 +97,7 @@ def spmm(args):
         X = torch.randn(M.cols, ld, device="cuda")
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
-        variants = [("rows", 0)] + ([("tiled", 0), ("tiled_bin", 0)] if args.config == "reddit" else []) + \
+        variants = [("rows", 0)] + ([("tiled", 0), ("tiled_bin64", 0), ("tiled_bin128", 0)] if args.config == "reddit" else []) + \
             ([("rows", 4), ("rows", 16)] if d <= 64 else []) + ([("rows", 1), ("rows", 4)] if d > 256 else [])
         if args.tiled_only:
             variants = [v for v in variants if v[0].startswith("tiled")]
@@ -106,7 +106,8 @@ def spmm(args):
                 key = (name, algo)
                 if key not in tiled:
                     t0 = time.time()
-                    tiled[key] = ops.TiledCsr(M, factored=algo == "tiled_bin")
+                    rb = int(algo[len("tiled_bin"):]) if algo.startswith("tiled_bin") else None
+                    tiled[key] = ops.TiledCsr(M, factored=rb is not None, block_rows=rb)
                     torch.cuda.synchronize()
                     print(json.dumps({"tiled": name, "algo": algo, "build_s": round(time.time() - t0, 2),
                                       "tiles": tiled[key].ntiles,
