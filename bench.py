@@ -341,6 +341,8 @@ def run_b200(args):
     # ---- device-timed region: K epochs, no host syncs inside ------------------
     timer = KernelTimer()
     eng.timer = timer
+    if world > 1:
+        eng.comm_events = []
     launches0 = eng.launches
     with ClockSampler(local) as clk:
         barrier()
@@ -356,6 +358,8 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier()
     launches = eng.launches - launches0
+    halo_net = _halo_net(eng, world, args.steps)
+    eng.comm_events = None
     eng.timer = KernelTimer()
     eng.timer.enabled = False
     eng.check_epoch(epoch)
@@ -377,6 +381,39 @@ def run_b200(args):
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     e2e = _max_over_ranks(statistics.mean(e2e_times), world)
+
+    # ---- Sylvie-A sub-line (async, staleness 0) on the same graph -------------
+    async_line = None
+    if args.mode == "sync" and not args.no_async_line:
+        import gc
+        sync_recv = sum(b.recv[0].numel() for b in list(eng.xf.values()) + list(eng.xb.values()))
+        del eng
+        gc.collect()
+        torch.cuda.empty_cache()
+        eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config], loss=LOSS[args.config]),
+                         TrainMode("async", 0), QuantConfig(args.bits), args.seed, 0.01, gnorm,
+                         device=torch.device("cuda", local))
+        for _ in range(args.warmup):
+            epoch += 1
+            eng.run_epoch(epoch)
+        barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            epoch += 1
+            eng.run_epoch(epoch, check=False)
+        a1.record()
+        torch.cuda.synchronize()
+        barrier()
+        eng.check_epoch(epoch)
+        ams = _max_over_ranks(a0.elapsed_time(a1) / args.steps, world)
+        async_recv = sum(sum(r.numel() for r in b.recv) for b in list(eng.xf.values()) + list(eng.xb.values()))
+        async_line = {"mode": "async", "staleness": 0, "ms_per_step": ams, "vs_sync": ams / ms,
+                      "recv_buffer_bytes": {"sync": int(sync_recv), "async_two_parities": int(async_recv)},
+                      "note": ("Sylvie-A: each exchange ships epoch t's halos into parity t%2 while epoch t "
+                               "consumes parity (t-1)%2; at N=1 the wire blocks move HBM->HBM, so the deferred "
+                               "exchange overlaps nothing and the two modes cost the same device work")}
 
     if rank == 0:
         peaks = load_peaks()
@@ -470,6 +507,8 @@ def run_b200(args):
                               ("gloo with host staging (--share-gpu: all ranks on one GPU)" if args.share_gpu
                                else "NCCL send/recv on the comm stream"))},
             "gpu_launches": launches,
+            "halo_network": halo_net,
+            "async": async_line,
             "host_issue_ms_per_step": round(host_issue_ms, 3),
             "host_issue_note": "wall time to issue an epoch; includes the waits on each exchange's two pinned "
                                "descriptor slots that keep the host at most two epochs ahead of the GPU "
@@ -486,6 +525,20 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _halo_net(eng, world: int, steps: int):
+    """Halo GB/s over the network leg (N>1): remote wire bytes / NCCL span,
+    both from the comm-stream events of the timed epochs."""
+    if world == 1 or not eng.comm_events:
+        return None
+    ms = sum(a.elapsed_time(b) for a, b, _ in eng.comm_events)
+    nbytes = sum(n for _, _, n in eng.comm_events)
+    ms = _max_over_ranks(ms, world)
+    return {"wire_bytes_per_epoch": nbytes / steps, "nccl_ms_per_epoch": ms / steps,
+            "halo_gbps": nbytes / ms / 1e6 if ms > 0 else None, "nvlink_peak_gbps": 900.0,
+            "frac": (nbytes / ms / 1e6) / 900.0 if ms > 0 else None,
+            "note": "this rank's sends to other ranks over NCCL; comm-stream events, max span over ranks"}
 
 
 def _max_over_ranks(x: float, world: int) -> float:
@@ -533,6 +586,10 @@ def main():
     ap.add_argument("--staleness", type=int, default=0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-async-line", action="store_true", help="skip the Sylvie-A sub-line")
+    ap.add_argument("--partitions", type=int, default=8,
+                    help="graph partitions (8 = BASELINE config 2; --partitions N with --gpus N = one "
+                         "subgraph per GPU)")
     ap.add_argument("--scale", type=float, default=1.0,
                     help="graph size factor (1.0 = the BASELINE shape; smaller only for diagnostics)")
     ap.add_argument("--share-gpu", action="store_true",
@@ -540,6 +597,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    global PARTITIONS
+    PARTITIONS = args.partitions
+    if PARTITIONS < max(1, args.gpus):
+        raise SystemExit("--partitions must be >= --gpus (every GPU hosts at least one partition)")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -183,12 +183,13 @@ class DeviceRank:
 
     def __init__(self, layout: RankLayout, cfg: ModelConfig, mode: TrainMode, quant: QuantConfig,
                  seed: int, lr: float, global_norm: int, device=None, group=None, probe=None,
-                 features=None, agg_order=None):
+                 features=None, agg_order=None, timeout: float = 60.0):
         import torch
         self.torch = torch
         self.dev = torch.device(device or "cuda")
         self.layout, self.cfg, self.mode, self.quant = layout, cfg, mode, quant
         self.seed, self.lr, self.norm = seed, lr, float(global_norm)
+        self.timeout = float(timeout)
         self.group, self.probe = group, probe
         self.world = 1
         if group is not None or _dist_initialized():
@@ -246,6 +247,7 @@ class DeviceRank:
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
         self.xent_partials = torch.zeros(ops.XENT_PARTIALS, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.proto_flags = torch.zeros(1, dtype=torch.int32, device=dev)   # written on the comm stream only
         self.counts = torch.zeros(9, dtype=torch.int64, device=dev)
         self.multilabel = cfg.loss == "multilabel"
         if self.multilabel:
@@ -302,6 +304,7 @@ class DeviceRank:
         self.stats = {p: TransportStats() for p in layout.ids}
         self.epoch_loss = 0.0
         self.comm_stream = torch.cuda.Stream(device=dev) if self.world > 1 else None
+        self.comm_events = None      # list -> (start, end, remote wire bytes) per NCCL exchange
         self.launches = 0
         self.timer = null_timer
 
@@ -336,8 +339,16 @@ class DeviceRank:
             ev = torch.cuda.current_stream().record_event()
             with torch.cuda.stream(self.comm_stream):
                 self.comm_stream.wait_event(ev)
-                nccl_exchange(bufs, parity, self.group)
+                if self.comm_events is not None:     # halo GB/s: the NCCL span on the comm stream
+                    t0 = torch.cuda.Event(enable_timing=True)
+                    t0.record(self.comm_stream)
+                nccl_exchange(bufs, parity, self.group, tag=(epoch, layer, bufs.plan.phase),
+                              flags=self.proto_flags)
                 done = self.comm_stream.record_event()
+                if self.comm_events is not None:
+                    t1 = torch.cuda.Event(enable_timing=True)
+                    t1.record(self.comm_stream)
+                    self.comm_events.append((t0, t1, sum(n for _, n in bufs.send_group.values())))
             if defer:
                 # Sylvie-A: the exchange overlaps the rest of this epoch and the
                 # next one up to the consuming K2 (_recv waits on `done`)
@@ -680,7 +691,15 @@ class DeviceRank:
         return epoch_mode
 
     def check_epoch(self, epoch: int):
-        """Host checks of the reference (codec.py:167-168, trainer.py:361-363)."""
+        """Host checks of the reference (codec.py:167-168, trainer.py:361-363),
+        after waiting at most ``timeout`` seconds for the epoch to finish on
+        the device (the reference's recv timeout, transport.py:115-124: with
+        NCCL a stalled or diverged peer leaves the comm stream waiting)."""
+        wait_device(self.torch.cuda.current_stream().record_event(), self.timeout,
+                    f"epoch {epoch} did not complete within {self.timeout:g} s (a peer rank stalled "
+                    "or the ranks diverged)")
+        if int(self.proto_flags.item()):
+            raise ProtocolError(f"tag mismatch in an exchange of epoch {epoch}: the ranks diverged")
         flags = int(self.flags.item())
         if flags & 1:
             raise TrainingError(f"worker {self.layout.ids[0]} aborted: "
@@ -725,6 +744,21 @@ class DeviceRank:
             t.messages_sent += s.messages_sent
             t.allreduce_bytes += s.allreduce_bytes
         return t.snapshot()
+
+
+def wait_device(event, timeout: float, what: str, poll=None):
+    """Block until `event` completes, raising ProtocolError after `timeout`
+    seconds (a spin for the first ~50 us, then 50-us sleeps)."""
+    import time
+    done = poll or event.query
+    t0 = time.monotonic()
+    spins = 0
+    while not done():
+        if time.monotonic() - t0 > timeout:
+            raise ProtocolError(f"timed out: {what}")
+        spins += 1
+        if spins > 64:
+            time.sleep(5e-5)
 
 
 def _accuracies(c, multilabel: bool) -> dict:
@@ -867,7 +901,7 @@ def train(graph: Graph, partitions: list, model_cfg: ModelConfig, mode: TrainMod
     global_norm = max(1, int(np.asarray(graph.train_mask).sum()))
     layout = RankLayout({p.id: p for p in partitions}, [0] * n, 0)
     eng = DeviceRank(layout, model_cfg, mode, quant_cfg, seed, lr, global_norm, device=device,
-                     probe=probe, agg_order=agg_order)
+                     probe=probe, agg_order=agg_order, timeout=timeout)
     if epochs == 0:
         return TrainResult([], init_weights(model_cfg, seed))
     ar_per_epoch = (4 * sum(int(w.numel()) for w in eng.W)) if n > 1 else 0

@@ -326,25 +326,63 @@ def host_staged(group=None) -> bool:
     return dist.get_backend(group) != "nccl"
 
 
-def nccl_exchange(bufs: ExchangeBuffers, parity: int, group=None):
+ENVELOPE_MAGIC = int.from_bytes(b"HBM1", "little")
+_PHASE_CODE = {FORWARD: 0, BACKWARD: 1}
+FLAG_PROTOCOL = 2          # device flag bit: an envelope did not match its exchange's tag
+
+
+def envelope(src_rank: int, dst_rank: int, tag) -> list:
+    """The ``Message`` envelope of one rank-to-rank group (transport.py:23-59:
+    magic "HBM1", src, dst and the tag (epoch, layer, phase)) as 6 int64."""
+    epoch, layer, phase = tag
+    return [ENVELOPE_MAGIC, src_rank, dst_rank, int(epoch), int(layer), _PHASE_CODE[phase]]
+
+
+def nccl_exchange(bufs: ExchangeBuffers, parity: int, group=None, tag=None, flags=None):
     """Move the remote groups with NCCL send/recv (one pair per peer rank).
-    Called on the comm stream; a no-op on a single rank."""
+    Called on the comm stream; a no-op on a single rank.
+
+    tag = (epoch, layer, phase): every group travels with its 48-byte envelope
+    (not byte-metered, like the reference's ``Message`` header) and the
+    receiver checks it against its own tag — the reference's tag check in
+    ``Fabric.recv`` (transport.py:115-124).  A mismatch raises ProtocolError
+    at once when the exchange is host-staged (gloo), and sets FLAG_PROTOCOL in
+    the device word ``flags`` on the NCCL path (read at the epoch check)."""
+    import torch
     import torch.distributed as dist
     stage = bufs.send.is_cuda and host_staged(group)
-    ops, landing = [], []
+    me = bufs.layout.rank
+    ops, landing, envs = [], [], []
+    env_dev = bufs.send.device if not stage else torch.device("cpu")
     for r, (o, n) in bufs.send_group.items():
         t = bufs.send[o:o + n]
         ops.append(dist.P2POp(dist.isend, t.cpu() if stage else t, r, group=group))
+        if tag is not None:
+            e = torch.tensor(envelope(me, r, tag), dtype=torch.int64, device=env_dev)
+            ops.append(dist.P2POp(dist.isend, e, r, group=group))
     for r, (o, n) in bufs.recv_group.items():
-        if r == bufs.layout.rank:
+        if r == me:
             continue
         t = bufs.recv[parity][o:o + n]
         h = t.cpu() if stage else t
         if stage:
             landing.append((t, h))
         ops.append(dist.P2POp(dist.irecv, h, r, group=group))
+        if tag is not None:
+            e = torch.empty(6, dtype=torch.int64, device=env_dev)
+            envs.append((r, e))
+            ops.append(dist.P2POp(dist.irecv, e, r, group=group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
     for t, h in landing:
         t.copy_(h, non_blocking=False)
+    for r, e in envs:
+        want = torch.tensor(envelope(r, me, tag), dtype=torch.int64, device=e.device)
+        if e.device.type == "cpu":
+            if not torch.equal(e, want):
+                got = e.tolist()
+                raise ProtocolError(f"tag mismatch from rank {r}: got (epoch {got[3]}, layer {got[4]}, "
+                                    f"phase {got[5]}), expected {tuple(tag)}")
+        elif flags is not None:
+            flags.bitwise_or_(torch.ne(e, want).any().to(flags.dtype) * FLAG_PROTOCOL)

@@ -192,3 +192,59 @@ def test_multi_rank_halo_exchange_matches_reference_semantics(world):
     for rank, status, info in results:
         assert status == "ok", f"rank {rank}:\n{info}"
         assert info > 0
+
+
+def _tag_worker(rank, world, port, q):
+    """Both ranks run one exchange; rank 1 is one epoch ahead (a diverged
+    rank).  Each receiver's envelope check must raise ProtocolError
+    (transport.py:115-124), and a matching exchange must pass."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        from paper_2303_01277_b200.rngstream import FORWARD
+        from paper_2303_01277_b200.transport import ExchangeBuffers, ProtocolError, RankLayout, nccl_exchange
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        owner = OWNERS[2]
+        parts = _parts(4)
+        lay = RankLayout({p.id: p for p in parts if owner[p.id] == rank}, owner, rank)
+        bufs = ExchangeBuffers(lay, lay.fwd, D, 1, "cpu")
+        nccl_exchange(bufs, 0, tag=(3, 1, FORWARD))            # agreeing tags: no error
+        try:
+            nccl_exchange(bufs, 0, tag=(3 + rank, 1, FORWARD))
+            q.put((rank, "fail", "no ProtocolError on a diverged tag"))
+        except ProtocolError as e:
+            q.put((rank, "ok", str(e)))
+    except Exception:
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_envelope_tag_mismatch_raises_protocol_error():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tag_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, info in results:
+        assert status == "ok", f"rank {rank}:\n{info}"
+        assert "tag mismatch" in info
+
+
+def test_wait_device_times_out():
+    """train(timeout=) / DeviceRank(timeout=): a device epoch that never
+    completes (a stalled peer on the NCCL path) raises ProtocolError, which
+    train() reports as TrainingError (trainer.py:386-388, 457-464)."""
+    import time
+    from paper_2303_01277_b200.trainer import wait_device
+    from paper_2303_01277_b200.transport import ProtocolError
+    t0 = time.monotonic()
+    with pytest.raises(ProtocolError, match="timed out"):
+        wait_device(None, 0.05, "stalled", poll=lambda: False)
+    assert time.monotonic() - t0 < 2.0
+    wait_device(None, 0.05, "done", poll=lambda: True)
