@@ -1379,6 +1379,110 @@ __global__ void philox_uniforms_kernel(uint64_t k0, uint64_t k1, uint64_t start,
   }
 }
 
+// ---- passthrough (bits = 32): K1 / K2 as pure gather / scatter copies ------
+// codec.py:186-187 (quantize_rows returns the rows) and :202-203 (dequantize
+// returns them): no metadata, no RNG.  A warp per row, lane-contiguous 4-byte
+// accesses (a wire row starts 12 bytes past a 16-byte boundary, so wider
+// accesses would be misaligned; lane-contiguous words still give 128-byte
+// warp transactions), four words in flight per lane.  Segments are looked up
+// from a per-warp cache (rows are visited in ascending order).
+__device__ __forceinline__ int seg_lookup(const int32_t* seg_begin, int nseg, int row, int& cs) {
+  if (!(row >= seg_begin[cs] && row < seg_begin[cs + 1])) cs = find_segment_smem(seg_begin, nseg, row);
+  return cs;
+}
+
+__global__ void __launch_bounds__(kQWarps * 32)
+quantize_pass_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
+                     int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
+                     uint32_t* __restrict__ flags) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  int cs = 0;
+  for (int row = blockIdx.x * kQWarps + warp; row < total_rows; row += gridDim.x * kQWarps) {
+    const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, row, cs)];
+    const int r = row - sg.row_begin;
+    const float* __restrict__ x = src + (int64_t)row_idx[row] * ld;
+    uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
+    float* prow = reinterpret_cast<float*>(out + HB_HEADER_BYTES) + (int64_t)r * d;
+    bool bad = false;
+    for (int c = lane; c < d; c += 128) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? __ldg(x + c + 32 * u) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c + 32 * u < d) {
+          bad |= !isfinite(v[u]);
+          prow[c + 32 * u] = v[u];
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, HB_FLAG_NONFINITE);
+    if (r == 0 && lane == 0) write_header(out, 32, sg.num_rows, d);
+  }
+}
+
+__global__ void __launch_bounds__(kQWarps * 32)
+dequant_pass_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_dst,
+                    const int32_t* __restrict__ dst_rows, const int32_t* __restrict__ src_ptr,
+                    const int32_t* __restrict__ src_rows, int d, float* __restrict__ dst, int64_t ld,
+                    int accumulate) {
+  __shared__ hb_segment_t segs_s[kMaxSmemSegs];
+  __shared__ int32_t seg_begin[kMaxSmemSegs + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    segs_s[i] = segs_g[i];
+    seg_begin[i] = segs_g[i].row_begin;
+  }
+  if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
+  __syncthreads();
+  int cs = 0;
+  for (int i = blockIdx.x * kQWarps + warp; i < num_dst; i += gridDim.x * kQWarps) {
+    float* out = dst + (int64_t)dst_rows[i] * ld;
+    const int k0 = src_ptr[i], k1 = src_ptr[i + 1];
+    if (!accumulate && k1 - k0 == 1) {          // forward halo row: a straight copy
+      const int q = src_rows[k0];
+      const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, q, cs)];
+      const float* prow = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) + HB_HEADER_BYTES) +
+                          (int64_t)(q - sg.row_begin) * d;
+      for (int c = lane; c < d; c += 128) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? prow[c + 32 * u] : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c + 32 * u < d) out[c + 32 * u] = v[u];
+      }
+      continue;
+    }
+    // f64 sum (destination first when accumulating, then the sources in
+    // ascending peer order), one fp32 rounding — as dequant_rows_kernel
+    for (int c = lane; c < d; c += 128) {
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = (accumulate && c + 32 * u < d) ? (double)out[c + 32 * u] : 0.0;
+      for (int k = k0; k < k1; ++k) {
+        const int q = src_rows[k];
+        const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, q, cs)];
+        const float* prow = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) +
+                                                           HB_HEADER_BYTES) + (int64_t)(q - sg.row_begin) * d;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c + 32 * u < d) a[u] = __dadd_rn(a[u], (double)prow[c + 32 * u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c + 32 * u < d) out[c + 32 * u] = __double2float_rn(a[u]);
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------
 cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* row_idx,
                                    int total_rows, const hb_segment_t* segs, int nseg, int d,
@@ -1390,6 +1494,11 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
   const int want = (total_rows + kQWarps - 1) / kQWarps;
   const int grid = want < num_sms() * 16 ? want : num_sms() * 16;
   const dim3 blk(kQWarps * 32);
+  static const bool legacy_pass = getenv("HB_PASS_LEGACY") != nullptr;
+  if (bits == 32 && nseg <= kMaxSmemSegs && !legacy_pass) {
+    quantize_pass_kernel<<<grid, blk, 0, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags);
+    return cudaGetLastError();
+  }
 #define ARGS src, ld, row_idx, total_rows, segs, nseg, d, bits, flags
   static const bool no_tma = getenv("HB_K1_NO_TMA") != nullptr;
   static const bool no_hw = getenv("HB_K1_NO_HW") != nullptr;
@@ -1455,6 +1564,13 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
   static const bool legacy = getenv("HB_K2_LEGACY") != nullptr;
   static const bool no_acc = getenv("HB_K2_NO_B1ACC") != nullptr;
   const bool vec_dst = !no_acc && ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
+  static const bool legacy_pass = getenv("HB_PASS_LEGACY") != nullptr;
+  if (bits == 32 && nseg <= kMaxSmemSegs && !legacy_pass) {
+    const int g = want < num_sms() * 16 ? want : num_sms() * 16;
+    dequant_pass_kernel<<<g, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, src_rows, d, dst, ld,
+                                                   accumulate);
+    return cudaGetLastError();
+  }
   if (!legacy && nseg <= kMaxSmemSegs && nch <= 8) {
 #define HB_K2(N, F) dequant_rows_kernel<N, F><<<grid, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, \
                                                                        src_ptr, src_rows, d, bits, dst, ld, accumulate)

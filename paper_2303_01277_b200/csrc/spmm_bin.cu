@@ -9,10 +9,13 @@
 //   * GCN              Â  = D^-1/2 (A+I) D^-1/2 -> r = c = dinv.
 // With the values factored out a tile record is the nonzero's column inside
 // its 64-column window: ONE BYTE (the general kernel, spmm_tiled.cu, moves an
-// 8-byte (col, val) record per nonzero through shared memory).  Records are
-// read 16 at a time with one broadcast LDS.128 and unpacked in registers, so
-// the shared-memory datapath — the binding resource of a SIMT SpMM — carries
-// only the gathered X rows: 8 wavefronts per nonzero at d = 256 instead of 9.
+// 8-byte (col, val) record per nonzero through shared memory).  Each row's
+// run of records is padded to whole 32-bit words (0xFF = padding) and read a
+// word — 4 records — per broadcast load, unpacked with byte permutes, so the
+// shared-memory datapath (the binding resource of a SIMT SpMM) carries the
+// gathered X rows plus a quarter wavefront per nonzero: 8.25 wavefronts per
+// nonzero at d = 256 instead of 9, with no per-record issue overhead beyond
+// the general kernel's.
 // Row blocks are 64 or 128 rows tall (16 consumer warps x 4 or 8 rows); taller
 // blocks reuse each TMA-staged 64-row X window across more rows.  c is applied by a pre-pass into a
 // caller-provided scratch copy of X (one HBM read + write of X), r to the
@@ -78,12 +81,6 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
-// byte p (0..15) of a 16-byte record chunk
-__device__ __forceinline__ int rec_byte(const uint4& c, int p) {
-  const uint32_t w = (p & 8) ? ((p & 4) ? c.w : c.z) : ((p & 4) ? c.y : c.x);
-  return (int)__byte_perm(w, 0u, 0x4440u | (uint32_t)(p & 3));
-}
-
 template <int NV, int G>
 __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restrict__ x, int nlast) {
 #pragma unroll
@@ -98,9 +95,8 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 // 1 CTA/SM: 17 warps are allocated registers as 20 (4-warp granularity), so
 // 96 per thread is the most that launches; 2 CTAs/SM: 56
 // RB rows per block (kRPW = RB / 16 per warp), NV float4 per lane, G lanes
-// per row group, S ring stages, MINB CTAs per SM, U records in flight per
-// warp (G == 32)
-template <int RB, int NV, int G, int S, int MINB, int U>
+// per row group, S ring stages, MINB CTAs per SM
+template <int RB, int NV, int G, int S, int MINB>
 __global__ void __maxnreg__(MINB == 1 ? 96 : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   using S_ = Smem<RB, NV, G, S>;
@@ -193,58 +189,65 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       mbar_wait(&full[s], (it / S) & 1);
       const uint8_t* st = smem + s * S_::STAGE;
       const float4* xs = reinterpret_cast<const float4*>(st) + gl;
-      const uint8_t* rec = st + S_::X_BYTES;
+      const uint32_t* rec32 = reinterpret_cast<const uint32_t*>(st + S_::X_BYTES);
       const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + kMaxRec) + warp * kRPW;
 #pragma unroll
       for (int i = 0; i < RPG; ++i) {
         const int rr = hg + i * NG;
-        const int k = ro[rr], k1 = ro[rr + 1];
-        for (int kb = k & ~15; kb < k1; kb += 16) {
-          const uint4 c = *reinterpret_cast<const uint4*>(rec + kb);       // 16 records, one broadcast
-          int p = k > kb ? k - kb : 0;
-          const int pe = k1 - kb < 16 ? k1 - kb : 16;
-          if constexpr (G == 32) {
-            // U records (U X rows of NV float4 per lane) in flight per warp
-            for (; p + U <= pe; p += U) {
-              float4 x[U][NV];
+        // the row's run of one-byte records, padded to whole words with 0xFF:
+        // every word but the last holds 4 records
+        const int w1 = ro[rr + 1] >> 2;
+        int w = ro[rr] >> 2;
+        if constexpr (G == 32) {
+          for (; w + 1 < w1; ++w) {
+            const uint32_t q = rec32[w];                           // 4 records, one broadcast
+            float4 x[4][NV];
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                const int j = rec_byte(c, p + u);
+            for (int u = 0; u < 4; ++u) {
+              const int j = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)u);
 #pragma unroll
-                for (int v = 0; v < NV; ++v)
-                  if (v < NV - 1 || nlast) x[u][v] = xs[j * pw4 + v * G];
-              }
-#pragma unroll
-              for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-                  if (v < NV - 1 || nlast) {
-                    acc[i][v].x += x[u][v].x; acc[i][v].y += x[u][v].y;
-                    acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
-                  }
+              for (int v = 0; v < NV; ++v)
+                if (v < NV - 1 || nlast) x[u][v] = xs[j * pw4 + v * G];
             }
-            for (; p < pe; ++p) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
-          } else {
-            // narrow rows: each lane group walks its own row, two records at a time
-            for (; p + 1 < pe; p += 2) {
-              const int j0 = rec_byte(c, p), j1 = rec_byte(c, p + 1);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                if (v < NV - 1 || nlast) {
+                  acc[i][v].x += x[u][v].x; acc[i][v].y += x[u][v].y;
+                  acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
+                }
+          }
+        } else {
+          // narrow rows: each lane group walks its own row, two records at a time
+          for (; w + 1 < w1; ++w) {
+            const uint32_t q = rec32[w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j0 = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)(2 * h));
+              const int j1 = (int)__byte_perm(q, 0u, 0x4441u | (uint32_t)(2 * h));
               float4 x0[NV], x1[NV];
 #pragma unroll
-              for (int v = 0; v < NV; ++v) {
+              for (int v = 0; v < NV; ++v)
                 if (v < NV - 1 || nlast) {
                   x0[v] = xs[j0 * pw4 + v * G];
                   x1[v] = xs[j1 * pw4 + v * G];
                 }
-              }
 #pragma unroll
-              for (int v = 0; v < NV; ++v) {
+              for (int v = 0; v < NV; ++v)
                 if (v < NV - 1 || nlast) {
                   acc[i][v].x += x0[v].x; acc[i][v].y += x0[v].y; acc[i][v].z += x0[v].z; acc[i][v].w += x0[v].w;
                   acc[i][v].x += x1[v].x; acc[i][v].y += x1[v].y; acc[i][v].z += x1[v].z; acc[i][v].w += x1[v].w;
                 }
-              }
             }
-            if (p < pe) add_row<NV, G>(acc[i], xs + rec_byte(c, p) * pw4, nlast);
+          }
+        }
+        if (w < w1) {                    // the run's last word: 0xFF bytes are padding
+          const uint32_t q = rec32[w];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)u);
+            if (j != 0xFF) add_row<NV, G>(acc[i], xs + j * pw4, nlast);
           }
         }
       }
@@ -312,7 +315,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int RB, int NV, int G, int S, int MINB, int U>
+template <int RB, int NV, int G, int S, int MINB>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   using S_ = Smem<RB, NV, G, S>;
   static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
@@ -332,14 +335,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, U>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
-  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, U><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -370,18 +373,15 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-  // HB_BIN_VARIANT (tuning): 1 = one X row in flight per warp at 256-column
-  // panels (128-row blocks only)
-  static const int variant = getenv("HB_BIN_VARIANT") ? atoi(getenv("HB_BIN_VARIANT")) : 0;
   if (block_rows == 64) {
-    if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2, 1>(a, xrows, stream);   // 4 rows of a warp in parallel
-    if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1, 4>(a, xrows, stream);
-    return sb::launch_nv<64, 2, 32, 3, 1, 4>(a, xrows, stream);              // 256-column panels
+    if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2>(a, xrows, stream);   // 4 rows of a warp in parallel
+    if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1>(a, xrows, stream);
+    return sb::launch_nv<64, 2, 32, 3, 1>(a, xrows, stream);              // 256-column panels
   }
   if (block_rows != 128) return cudaErrorInvalidValue;
-  if (d <= 64) return sb::launch_nv<128, 2, 8, 4, 2, 1>(a, xrows, stream);
-  if (d <= 128 || variant != 1) return sb::launch_nv<128, 1, 32, 5, 1, 4>(a, xrows, stream);
-  return sb::launch_nv<128, 2, 32, 3, 1, 1>(a, xrows, stream);
+  // 128-row blocks: 8 rows per warp, so 128-column panels (register budget)
+  if (d <= 64) return sb::launch_nv<128, 2, 8, 4, 2>(a, xrows, stream);
+  return sb::launch_nv<128, 1, 32, 5, 1>(a, xrows, stream);
 }
 
 }  // namespace hb

@@ -143,49 +143,61 @@ class TiledCsr:
         gid = torch.repeat_interleave(torch.arange(len(uniq), device=dev), cnt)
         dense_nz = dense_g[gid]
         grp_key, grp_cnt = uniq[dense_g], cnt[dense_g]
-        # a tile holds at most MAXREC records (the kernel's smem record slot);
-        # denser (block, window) groups become several tiles of the same window
-        nsplit = (grp_cnt + self.MAXREC - 1) // self.MAXREC
+        # a tile holds at most `cap` records (the kernel's smem record slot;
+        # factored tiles pad each row's run to whole 4-byte words, up to 3
+        # bytes per row); denser (block, window) groups become several tiles
+        # of the same window
+        cap = self.MAXREC - 3 * RB if self.binary else self.MAXREC
+        nsplit = (grp_cnt + cap - 1) // cap
         sub_of_grp = torch.repeat_interleave(torch.arange(grp_key.numel(), device=dev), nsplit)
         first_sub = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
         first_sub[1:] = torch.cumsum(nsplit, 0)
         j = torch.arange(sub_of_grp.numel(), device=dev) - first_sub[sub_of_grp]
         tile_key = grp_key[sub_of_grp]
-        tile_cnt = torch.clamp(grp_cnt[sub_of_grp] - j * self.MAXREC, max=self.MAXREC)
+        tile_cnt = torch.clamp(grp_cnt[sub_of_grp] - j * cap, max=cap)
         self.ntiles = int(tile_key.numel())
         tile_blk = tile_key // nwin
         self.tile_win = (tile_key % nwin).to(torch.int32).contiguous()
         tp = torch.zeros(self.nblocks + 1, dtype=torch.int64, device=dev)
         tp[1:] = torch.cumsum(torch.bincount(tile_blk, minlength=self.nblocks), 0)
         self.tile_ptr = tp.to(torch.int32)
-        align = 16 if self.binary else 2                      # record runs start 16-byte aligned
-        padded = (tile_cnt + align - 1) // align * align
-        off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
-        off[1:] = torch.cumsum(padded, 0)
         didx = order[dense_nz]                                # original nonzero ids, tile order
         grp_of = (torch.cumsum(dense_g.long(), 0) - 1)[gid[dense_nz]]
         gstart = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
         gstart[1:] = torch.cumsum(grp_cnt, 0)
         grank = torch.arange(didx.numel(), device=dev) - gstart[grp_of]
-        tile_of = first_sub[grp_of] + grank // self.MAXREC
-        rank = grank % self.MAXREC
-        pos = off[tile_of] + rank
+        tile_of = first_sub[grp_of] + grank // cap
+        rank = grank % cap                                    # position in the tile (rows ascending)
         rel = col[didx] - self.tile_win.long()[tile_of] * W
+        lr = rows[didx] % RB
+        per = torch.bincount(tile_of * RB + lr, minlength=self.ntiles * RB).view(self.ntiles, RB)
+        ro = torch.zeros((self.ntiles, self.ROWOFF), dtype=torch.int64, device=dev)
         if self.binary:
-            rec = torch.zeros(max(16, int(off[-1].item())), dtype=torch.uint8, device=dev)
+            # row runs padded to 4-byte words (0xFF fills the padding): the
+            # kernel reads a row's records one word at a time
+            pc = (per + 3) // 4 * 4
+            ro[:, 1:RB + 1] = torch.cumsum(pc, 1)
+            start = torch.zeros((self.ntiles, RB), dtype=torch.int64, device=dev)
+            start[:, 1:] = torch.cumsum(per, 1)[:, :-1]       # unpadded start of each row in the tile
+            padded = (ro[:, RB] + 15) // 16 * 16
+            off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
+            off[1:] = torch.cumsum(padded, 0)
+            pos = off[tile_of] + ro[tile_of, lr] + (rank - start[tile_of, lr])
+            rec = torch.full((max(16, int(off[-1].item())),), 0xFF, dtype=torch.uint8, device=dev)
             rec[pos] = rel.to(torch.uint8)
             self.tile_nz = rec
             self.tile_off = off                               # byte offsets
         else:
+            ro[:, 1:RB + 1] = torch.cumsum(per, 1)
+            padded = (tile_cnt + 1) // 2 * 2                  # 16-byte aligned record runs
+            off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
+            off[1:] = torch.cumsum(padded, 0)
+            pos = off[tile_of] + rank
             nz = torch.zeros((int(off[-1].item()), 2), dtype=torch.int32, device=dev)
             nz[pos, 0] = rel.to(torch.int32)
             nz[pos, 1] = a.values[didx].view(torch.int32)
             self.tile_nz = nz
             self.tile_off = off                               # record (8-byte) offsets
-        lr = rows[didx] % RB
-        per = torch.bincount(tile_of * RB + lr, minlength=self.ntiles * RB).view(self.ntiles, RB)
-        ro = torch.zeros((self.ntiles, self.ROWOFF), dtype=torch.int32, device=dev)
-        ro[:, 1:RB + 1] = torch.cumsum(per, 1)
         self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= MAXREC, read as uint16
         keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
         keep[didx] = False

@@ -136,7 +136,12 @@ def _tile_dense(T):
                 r = b * T.RB + lr
                 for k in range(ro[t, lr], ro[t, lr + 1]):
                     if T.binary:
-                        c = win[t] * T.W + int(T.tile_nz[off[t] + k])
+                        assert ro[t, lr] % 4 == 0                 # row runs start on whole words
+                        j = int(T.tile_nz[off[t] + k])
+                        if j == 0xFF:                             # word padding: only at a run's end
+                            assert all(int(T.tile_nz[off[t] + kk]) == 0xFF for kk in range(k, ro[t, lr + 1]))
+                            break
+                        c = win[t] * T.W + j
                         out[r, c] += rs[r] * cs[c]
                     else:
                         c = win[t] * T.W + int(T.tile_nz[off[t] + k, 0])
