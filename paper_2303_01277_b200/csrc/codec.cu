@@ -538,8 +538,8 @@ quantize_gather_tma_kernel(const float* __restrict__ src, int64_t ld, const int3
 // each lane runs two interleaved Philox4x64-10 blocks (64-column chunks in
 // pairs) for twice the multiply-chain ILP.  Each half streams its rows through
 // two TMA-filled smem row buffers, one row ahead, like the 32-lane kernel.
-template <int MINB>
-__global__ void __launch_bounds__(kQWarps * 32, MINB)
+template <int MAXT, int MINB, int NBUF>
+__global__ void __launch_bounds__(MAXT, MINB)
 quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
                       int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
                       uint32_t* __restrict__ flags, int ldr, int imgw) {
@@ -554,9 +554,9 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
     seg_begin[i] = segs_g[i].row_begin;
   }
   if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
-  const size_t per_half = (size_t)2 * ldr * 4 + (size_t)imgw * 4;
+  const size_t per_half = (size_t)NBUF * ldr * 4 + (size_t)imgw * 4;
   float* rows_s = reinterpret_cast<float*>(dsm + (size_t)(2 * warp + hw) * per_half);
-  uint32_t* buf = reinterpret_cast<uint32_t*>(rows_s + 2 * ldr);
+  uint32_t* buf = reinterpret_cast<uint32_t*>(rows_s + NBUF * ldr);
   if (hl == 0) {
     mbar_init(&bars[warp][hw][0], 1);
     mbar_init(&bars[warp][hw][1], 1);
@@ -584,13 +584,20 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
   for (int k = 0;; row += stride, ++k) {
     const bool active = row < row_end;
     if (!__any_sync(0xffffffffu, active)) break;
-    const int cur = k & 1;
+    const int cur = NBUF == 2 ? (k & 1) : 0;
     const int nxt = row + stride;
-    if (nxt < row_end && hl == 0) {
+    if (NBUF == 2 && nxt < row_end && hl == 0) {
       fence_proxy_async_smem();
       mbar_expect_tx(&bars[warp][hw][cur ^ 1], bytes);
       tma_load_1d(rows_s + (cur ^ 1) * ldr, src + (int64_t)__ldg(row_idx + nxt) * ld, bytes,
                   &bars[warp][hw][cur ^ 1]);
+    }
+    if (NBUF == 1 && k > 0 && active && hl == 0) {
+      // single buffer: this row's load is issued once the previous row's
+      // passes are done with the buffer (other warps cover its latency)
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bars[warp][hw][0], bytes);
+      tma_load_1d(rows_s, src + (int64_t)__ldg(row_idx + row) * ld, bytes, &bars[warp][hw][0]);
     }
     if (active && !(row >= seg_begin[cseg] && row < seg_begin[cseg + 1]))
       cseg = find_segment_smem(seg_begin, nseg, row);
@@ -1405,26 +1412,40 @@ quantize_pass_kernel(const float* __restrict__ src, int64_t ld, const int32_t* _
   if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
   __syncthreads();
   int cs = 0;
-  for (int row = blockIdx.x * kQWarps + warp; row < total_rows; row += gridDim.x * kQWarps) {
-    const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, row, cs)];
-    const int r = row - sg.row_begin;
-    const float* __restrict__ x = src + (int64_t)row_idx[row] * ld;
-    uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
-    float* prow = reinterpret_cast<float*>(out + HB_HEADER_BYTES) + (int64_t)r * d;
+  // 32 rows per warp at a time: lane l resolves row l's source and wire
+  // pointers (and writes its block header), then the rows are copied one
+  // after another from register broadcasts
+  const int nwarps = gridDim.x * kQWarps;
+  for (int r0 = (blockIdx.x * kQWarps + warp) * 32; r0 < total_rows; r0 += nwarps * 32) {
+    const int row = r0 + lane;
+    const float* x_l = nullptr;
+    float* p_l = nullptr;
+    if (row < total_rows) {
+      const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, row, cs)];
+      const int r = row - sg.row_begin;
+      uint8_t* out = reinterpret_cast<uint8_t*>(sg.out);
+      x_l = src + (int64_t)row_idx[row] * ld;
+      p_l = reinterpret_cast<float*>(out + HB_HEADER_BYTES) + (int64_t)r * d;
+      if (r == 0) write_header(out, 32, sg.num_rows, d);
+    }
+    const int n = min(32, total_rows - r0);
     bool bad = false;
-    for (int c = lane; c < d; c += 128) {
-      float v[4];
+    for (int t = 0; t < n; ++t) {
+      const float* x = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(x_l), t));
+      float* prow = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(p_l), t));
+      for (int c = lane; c < d; c += 128) {
+        float v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? __ldg(x + c + 32 * u) : 0.f;
+        for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? __ldg(x + c + 32 * u) : 0.f;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + 32 * u < d) {
-          bad |= !isfinite(v[u]);
-          prow[c + 32 * u] = v[u];
-        }
+        for (int u = 0; u < 4; ++u)
+          if (c + 32 * u < d) {
+            bad |= !isfinite(v[u]);
+            prow[c + 32 * u] = v[u];
+          }
+      }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, HB_FLAG_NONFINITE);
-    if (r == 0 && lane == 0) write_header(out, 32, sg.num_rows, d);
   }
 }
 
@@ -1443,42 +1464,63 @@ dequant_pass_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_d
   if (threadIdx.x == 0) seg_begin[nseg] = 0x7fffffff;
   __syncthreads();
   int cs = 0;
-  for (int i = blockIdx.x * kQWarps + warp; i < num_dst; i += gridDim.x * kQWarps) {
-    float* out = dst + (int64_t)dst_rows[i] * ld;
-    const int k0 = src_ptr[i], k1 = src_ptr[i + 1];
-    if (!accumulate && k1 - k0 == 1) {          // forward halo row: a straight copy
-      const int q = src_rows[k0];
-      const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, q, cs)];
-      const float* prow = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) + HB_HEADER_BYTES) +
-                          (int64_t)(q - sg.row_begin) * d;
-      for (int c = lane; c < d; c += 128) {
-        float v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? prow[c + 32 * u] : 0.f;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c + 32 * u < d) out[c + 32 * u] = v[u];
-      }
-      continue;
-    }
-    // f64 sum (destination first when accumulating, then the sources in
-    // ascending peer order), one fp32 rounding — as dequant_rows_kernel
-    for (int c = lane; c < d; c += 128) {
-      double a[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = (accumulate && c + 32 * u < d) ? (double)out[c + 32 * u] : 0.0;
-      for (int k = k0; k < k1; ++k) {
-        const int q = src_rows[k];
+  // a warp takes 32 destinations at a time: lane l resolves destination l's
+  // indices, segment and source row pointer with independent loads, then the
+  // rows are copied one after another from register broadcasts (the index
+  // chain is paid once per 32 rows, not once per row)
+  const int nwarps = gridDim.x * kQWarps;
+  for (int i0 = (blockIdx.x * kQWarps + warp) * 32; i0 < num_dst; i0 += nwarps * 32) {
+    const int i = i0 + lane;
+    int k0 = 0, k1 = 0;
+    float* out_l = nullptr;
+    const float* src_l = nullptr;
+    if (i < num_dst) {
+      out_l = dst + (int64_t)dst_rows[i] * ld;
+      k0 = src_ptr[i];
+      k1 = src_ptr[i + 1];
+      if (k1 - k0 == 1) {
+        const int q = src_rows[k0];
         const hb_segment_t& sg = segs_s[seg_lookup(seg_begin, nseg, q, cs)];
-        const float* prow = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) +
+        src_l = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) + HB_HEADER_BYTES) +
+                (int64_t)(q - sg.row_begin) * d;
+      }
+    }
+    const int n = min(32, num_dst - i0);
+    for (int t = 0; t < n; ++t) {
+      float* out = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(out_l), t));
+      const float* prow =
+          reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src_l), t));
+      const int tk0 = __shfl_sync(0xffffffffu, k0, t), tk1 = __shfl_sync(0xffffffffu, k1, t);
+      if (!accumulate && tk1 - tk0 == 1) {        // forward halo row: a straight copy
+        for (int c = lane; c < d; c += 128) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = c + 32 * u < d ? prow[c + 32 * u] : 0.f;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c + 32 * u < d) out[c + 32 * u] = v[u];
+        }
+        continue;
+      }
+      // f64 sum (destination first when accumulating, then the sources in
+      // ascending peer order), one fp32 rounding — as dequant_rows_kernel
+      for (int c = lane; c < d; c += 128) {
+        double acc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = (accumulate && c + 32 * u < d) ? (double)out[c + 32 * u] : 0.0;
+        for (int k = tk0; k < tk1; ++k) {
+          const int q = src_rows[k];
+          const hb_segment_t& sg = segs_s[find_segment_smem(seg_begin, nseg, q)];
+          const float* pr = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sg.out) +
                                                            HB_HEADER_BYTES) + (int64_t)(q - sg.row_begin) * d;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c + 32 * u < d) a[u] = __dadd_rn(a[u], (double)prow[c + 32 * u]);
-      }
+          for (int u = 0; u < 4; ++u)
+            if (c + 32 * u < d) acc[u] = __dadd_rn(acc[u], (double)pr[c + 32 * u]);
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c + 32 * u < d) out[c + 32 * u] = __double2float_rn(a[u]);
+        for (int u = 0; u < 4; ++u)
+          if (c + 32 * u < d) out[c + 32 * u] = __double2float_rn(acc[u]);
+      }
     }
   }
 }
@@ -1496,7 +1538,9 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
   const dim3 blk(kQWarps * 32);
   static const bool legacy_pass = getenv("HB_PASS_LEGACY") != nullptr;
   if (bits == 32 && nseg <= kMaxSmemSegs && !legacy_pass) {
-    quantize_pass_kernel<<<grid, blk, 0, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags);
+    const int want32 = (total_rows + 32 * kQWarps - 1) / (32 * kQWarps);
+    const int g = want32 < num_sms() * 16 ? want32 : num_sms() * 16;
+    quantize_pass_kernel<<<g, blk, 0, st>>>(src, ld, row_idx, total_rows, segs, nseg, d, flags);
     return cudaGetLastError();
   }
 #define ARGS src, ld, row_idx, total_rows, segs, nseg, d, bits, flags
@@ -1507,14 +1551,19 @@ cudaError_t launch_quantize_gather(const float* src, int64_t ld, const int32_t* 
     const int ldr = (d + 3) & ~3;
     const int nch64 = (d + 3 + 63) >> 6;
     const int imgw = (2 * nch64 + 2 + 3) & ~3;
+    // HB_K1_NBUF (tuning): row buffers per half-warp (2 = next row prefetched)
+    static const int nbuf = getenv("HB_K1_NBUF") ? atoi(getenv("HB_K1_NBUF")) : 2;
     // wide rows: smaller CTAs so the per-warp row buffers do not cap the warps per SM
-    const size_t per_warp = (size_t)2 * (2 * ldr * 4 + imgw * 4);
+    const size_t per_warp = (size_t)2 * (nbuf * ldr * 4 + imgw * 4);
     const int wpc = per_warp > 6 * 1024 ? 4 : kQWarps;
     const size_t dyn = (size_t)wpc * per_warp;
     if (dyn <= 200 * 1024) {
       static const int minb = getenv("HB_K1_MINB") ? atoi(getenv("HB_K1_MINB")) : 3;
-      auto kern = minb == 2 ? quantize_b1_hw_kernel<2> : (minb == 4 ? quantize_b1_hw_kernel<4>
-                                                                     : quantize_b1_hw_kernel<3>);
+      // occupancy variants (128-thread CTAs for wide rows): <threads, CTAs/SM, buffers>
+      auto kern = wpc == 4 ? (nbuf == 1 ? (minb >= 8 ? quantize_b1_hw_kernel<128, 8, 1>
+                                                     : quantize_b1_hw_kernel<128, 6, 1>)
+                                        : quantize_b1_hw_kernel<128, 5, 2>)
+                           : (nbuf == 1 ? quantize_b1_hw_kernel<256, 4, 1> : quantize_b1_hw_kernel<256, 3, 2>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
       const int want2 = (total_rows + 2 * wpc - 1) / (2 * wpc);
       const int cap = num_sms() * 16 * (kQWarps / wpc);
@@ -1566,7 +1615,8 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
   const bool vec_dst = !no_acc && ((ld & 3) == 0) && ((((uintptr_t)dst) & 15) == 0);
   static const bool legacy_pass = getenv("HB_PASS_LEGACY") != nullptr;
   if (bits == 32 && nseg <= kMaxSmemSegs && !legacy_pass) {
-    const int g = want < num_sms() * 16 ? want : num_sms() * 16;
+    const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
+    const int g = want32 < num_sms() * 16 ? want32 : num_sms() * 16;
     dequant_pass_kernel<<<g, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, src_rows, d, dst, ld,
                                                    accumulate);
     return cudaGetLastError();
