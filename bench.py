@@ -34,9 +34,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (300, 512, 512, 512, 100)}
-MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn"}
-LOSS = {"reddit": "softmax", "ogbn": "softmax", "yelp": "multilabel"}   # BASELINE configs[3]: multilabel 100
+WIDTHS = {"reddit": (602, 256, 256, 41), "ogbn": (100, 128, 128, 47), "yelp": (300, 512, 512, 512, 100),
+          "config1": (64, 32, 4)}
+MODEL = {"reddit": "sage", "ogbn": "sage", "yelp": "gcn", "config1": "gcn"}
+LOSS = {"reddit": "softmax", "ogbn": "softmax", "yelp": "multilabel",   # BASELINE configs[3]: multilabel 100
+        "config1": "softmax"}
+# BASELINE configs[0] (the reference's CPU-runnable case) is 2 partitions
+DEFAULT_PARTS = {"config1": 2}
 PARTITIONS = 8
 CPU_SAMPLE_SCALE = 0.125       # oracle-port fallback only (no baseline/_ref): 1/8 of the nodes/edges
 REF_EPOCHS = 2                 # timed halobit.train epochs per reference measurement (after 1 warm-up)
@@ -47,15 +51,28 @@ PHILOX_CEILING_GELEM_S = 414.0
 
 def _spec(name: str, scale: float = 1.0):
     from paper_2303_01277_b200 import datasets as ds
+    if name == "config1":
+        if scale != 1.0:
+            raise SystemExit("config1 is the reference's own SBM graph: --scale 1 only")
+        return ds.CONFIG1
     spec = {"reddit": ds.REDDIT, "ogbn": ds.OGBN_PRODUCTS, "yelp": ds.YELP}[name]
     return spec if scale == 1.0 else ds.scaled(spec, scale)
+
+
+def _spec_size(spec):
+    """(nodes, directed edges) of a spec (the SBM's edge count is known after drawing)."""
+    if hasattr(spec, "num_nodes"):
+        return spec.num_nodes, spec.num_edges
+    return spec.nodes_per_community * spec.communities, 195_652     # CONFIG1: measured (SURVEY 8d)
 
 
 def build_graph(name: str, scale: float = 1.0, parts_needed=None):
     from paper_2303_01277_b200.datasets import generate_planted
     from paper_2303_01277_b200.graph import build_partition, mean_adjacency, normalize_adjacency, \
         partition_nodes
-    g = generate_planted(_spec(name, scale))
+    from paper_2303_01277_b200.datasets import generate_sbm
+    spec = _spec(name, scale)
+    g = generate_planted(spec) if hasattr(spec, "num_nodes") else generate_sbm(spec)
     a = normalize_adjacency(g)
     m = mean_adjacency(g) if MODEL[name] == "sage" else None
     plan = partition_nodes(g, PARTITIONS)
@@ -278,12 +295,11 @@ def workload_config(args) -> dict:
                         f"{MODEL[args.config].upper()} {'-'.join(map(str, WIDTHS[args.config]))}, "
                         f"{PARTITIONS} partitions over {args.gpus} GPU(s), {args.bits}-bit halos, "
                         f"Sylvie-{'S' if args.mode == 'sync' else 'A'}",
-            "nodes": spec.num_nodes, "edges": spec.num_edges, "partitions": PARTITIONS,
+            "nodes": _spec_size(spec)[0], "edges": _spec_size(spec)[1], "partitions": PARTITIONS,
             "bits": args.bits, "mode": args.mode, "staleness": args.staleness,
             "model": MODEL[args.config], "widths": list(WIDTHS[args.config]), "loss": LOSS[args.config],
             "scale": getattr(args, "scale", 1.0),
-            "l2": "inputs larger than L2 (features 561 MB, aggregation CSR 0.9 GB)" if getattr(args, "scale", 1.0) == 1.0
-                  else "reduced-scale diagnostic run"}
+            "l2": "n/a (CPU)" if args.impl == "reference" else None}
 
 
 def run_b200(args):
@@ -344,15 +360,28 @@ def run_b200(args):
     if world > 1:
         eng.comm_events = []
     launches0 = eng.launches
+    # a working set below L2 (config 1): every timed epoch starts from a
+    # flushed L2 (a 512 MB write between epochs, outside the event pairs)
+    small = _working_set_bytes(eng) < 126e6
+    flush = torch.empty(128 << 20, dtype=torch.float32, device=torch.device("cuda", local)) if small else None
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        spans = []
         ev0.record()
         h0 = time.perf_counter()
         for _ in range(args.steps):
             epoch += 1
-            eng.run_epoch(epoch, check=False)
+            if small:
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                eng.run_epoch(epoch, check=False)
+                e1.record()
+                spans.append((e0, e1))
+            else:
+                eng.run_epoch(epoch, check=False)
         host_issue_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         ev1.record()
         torch.cuda.synchronize()
@@ -363,8 +392,10 @@ def run_b200(args):
     eng.timer = KernelTimer()
     eng.timer.enabled = False
     eng.check_epoch(epoch)
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = (sum(a.elapsed_time(b) for a, b in spans) if small else ev0.elapsed_time(ev1)) / args.steps
     ms = _max_over_ranks(ms, world)
+    l2_note = ("working set below L2: L2 flushed (512 MB write) before every timed epoch, outside its event pair"
+               if small else f"inputs larger than L2 (working set {_working_set_bytes(eng) / 1e9:.2f} GB)")
     ksum = timer.summary()
     clocks = clk.result()
 
@@ -491,7 +522,7 @@ def run_b200(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (planted-partition reddit-shaped graph, random-init Glorot weights)",
-            "config": workload_config(args),
+            "config": dict(workload_config(args), l2=l2_note),
             "roofline": roof,
             "kernel_rooflines": kroof,
             "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
@@ -525,6 +556,14 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _working_set_bytes(eng) -> float:
+    """Bytes an epoch touches at least once: features / activations and the
+    aggregation operator (CSR + its transpose)."""
+    act = sum(t.numel() * 4 for t in eng.Ht.values())
+    csr = sum(m.nnz * 8 + (m.rows + 1) * 8 for m in (eng.A, eng.At))
+    return float(act + csr)
 
 
 def _halo_net(eng, world: int, steps: int):
@@ -587,7 +626,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-async-line", action="store_true", help="skip the Sylvie-A sub-line")
-    ap.add_argument("--partitions", type=int, default=8,
+    ap.add_argument("--partitions", type=int, default=None,
                     help="graph partitions (8 = BASELINE config 2; --partitions N with --gpus N = one "
                          "subgraph per GPU)")
     ap.add_argument("--scale", type=float, default=1.0,
@@ -598,7 +637,7 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     global PARTITIONS
-    PARTITIONS = args.partitions
+    PARTITIONS = args.partitions or DEFAULT_PARTS.get(args.config, 8)
     if PARTITIONS < max(1, args.gpus):
         raise SystemExit("--partitions must be >= --gpus (every GPU hosts at least one partition)")
     if args.impl == "reference":

@@ -191,13 +191,28 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       const float4* xs = reinterpret_cast<const float4*>(st) + gl;
       const uint32_t* rec32 = reinterpret_cast<const uint32_t*>(st + S_::X_BYTES);
       const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + kMaxRec) + warp * kRPW;
+      // the warp's kRPW + 1 row offsets in two broadcast loads (not 2 per row)
+      uint64_t ro_lo, ro_hi = 0;
+      if constexpr (kRPW == 4) {
+        ro_lo = *reinterpret_cast<const uint64_t*>(ro);
+      } else {
+        const uint4 v = *reinterpret_cast<const uint4*>(ro);
+        ro_lo = ((uint64_t)v.y << 32) | v.x;
+        ro_hi = ((uint64_t)v.w << 32) | v.z;
+      }
+      const int ro_end = ro[kRPW];
+      auto row_off = [&](int q) -> int {
+        if (q >= kRPW) return ro_end;
+        const uint64_t v = q < 4 ? ro_lo : ro_hi;
+        return (int)((v >> (16 * (q & 3))) & 0xffffu);
+      };
 #pragma unroll
       for (int i = 0; i < RPG; ++i) {
         const int rr = hg + i * NG;
         // the row's run of one-byte records, padded to whole words with 0xFF:
         // every word but the last holds 4 records
-        const int w1 = ro[rr + 1] >> 2;
-        int w = ro[rr] >> 2;
+        const int w1 = row_off(rr + 1) >> 2;
+        int w = row_off(rr) >> 2;
         if constexpr (G == 32) {
           for (; w + 1 < w1; ++w) {
             const uint32_t q = rec32[w];                           // 4 records, one broadcast
