@@ -424,20 +424,21 @@ def run_b200(args):
         eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config], loss=LOSS[args.config]),
                          TrainMode("async", 0), QuantConfig(args.bits), args.seed, 0.01, gnorm,
                          device=torch.device("cuda", local))
+        aepoch = 0                       # a fresh run: epoch 1 has no stale buffers yet
         for _ in range(args.warmup):
-            epoch += 1
-            eng.run_epoch(epoch)
+            aepoch += 1
+            eng.run_epoch(aepoch)
         barrier()
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
         for _ in range(args.steps):
-            epoch += 1
-            eng.run_epoch(epoch, check=False)
+            aepoch += 1
+            eng.run_epoch(aepoch, check=False)
         a1.record()
         torch.cuda.synchronize()
         barrier()
-        eng.check_epoch(epoch)
+        eng.check_epoch(aepoch)
         ams = _max_over_ranks(a0.elapsed_time(a1) / args.steps, world)
         async_recv = sum(sum(r.numel() for r in b.recv) for b in list(eng.xf.values()) + list(eng.xb.values()))
         async_line = {"mode": "async", "staleness": 0, "ms_per_step": ams, "vs_sync": ams / ms,

@@ -86,10 +86,13 @@ __device__ __forceinline__ int quant_fast(float x, const QuantRowCtx& q, uint64_
 // (hbar ~ 1: ut <= 1 - 2^-23, so ut < h unless they are within Eu) and near
 // the minimum — so that single test routes every undecidable element to the
 // f64 path.
+// 1 bit: code = (u < h), exact unless |h - ut| <= Eu.  x == row_min gives
+// h == 0 exactly and code 0 on both paths, so it needs no exclusion here
+// (it only reaches the exact path when ut <= Eu, probability ~1e-6).
 __device__ __forceinline__ uint32_t quant_fast_b1(float x, const QuantRowCtx& q, uint64_t w, bool& amb) {
   const float h = __fmul_rn(__fsub_rn(x, q.mn), q.inv_s);
   const float ut = __fsub_rn(__uint_as_float(((uint32_t)(w >> 32) >> 9) | 0x3f800000u), 1.0f);
-  amb = (x != q.mn) & (fabsf(__fsub_rn(h, ut)) <= q.Eu);
+  amb = fabsf(__fsub_rn(h, ut)) <= q.Eu;
   return ut < h ? 1u : 0u;
 }
 
@@ -660,9 +663,13 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
     }
 
     // ---- pass 2: chunk pairs, two interleaved Philox blocks per lane ------------
+    // Branches are warp-uniform (ballots): divergent ones cost reconvergence
+    // bookkeeping on every chunk, and the rare cases (edge chunks, ambiguous
+    // elements, constant rows) do not need their own paths per lane.
+    const bool any_live = __any_sync(0xffffffffu, q.live);
     for (int t = 0; t < nch2; t += 2) {
       uint32_t f2[2] = {0u, 0u};
-      if (q.live) {
+      if (any_live) {
         U64x4 ua, ub;
         philox4x64_10_x2(blk0 + (uint64_t)(16 * t + hl) + 1ull, blk0 + (uint64_t)(16 * (t + 1) + hl) + 1ull,
                          sg.key0, sg.key1, ua, ub);
@@ -675,27 +682,27 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
           const bool full = q.fast && (64 * tt - delta >= 0) && (64 * tt - delta + 64 <= d);
           uint32_t code[4];
           bool amb[4];
-          if (full) {
+          if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) code[i] = quant_fast_b1(xs[c0 + i], q, ws[i], amb[i]);
           } else {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int c = c0 + i;
-              amb[i] = false;
-              code[i] = 0;
-              if (c >= 0 && c < d) {
-                if (q.fast) code[i] = quant_fast_b1(xs[c], q, ws[i], amb[i]);
-                else amb[i] = true;
-              }
+              const bool in = q.live && c >= 0 && c < d;
+              const float xv = xs[min(max(c, 0), d - 1)];
+              code[i] = quant_fast_b1(xv, q, ws[i], amb[i]);
+              amb[i] = in && (amb[i] || !q.fast);
+              if (!in) code[i] = 0u;
             }
           }
-          if (amb[0] | amb[1] | amb[2] | amb[3]) {
+          const bool a4 = amb[0] | amb[1] | amb[2] | amb[3];
+          if (__any_sync(0xffffffffu, a4)) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               if (amb[i]) code[i] = (uint32_t)quant_exact(xs[c0 + i], q.mn, q.s, 1, ws[i]);
           }
-          f2[j] = code[0] | (code[1] << 1) | (code[2] << 2) | (code[3] << 3);
+          f2[j] = q.live ? (code[0] | (code[1] << 1) | (code[2] << 2) | (code[3] << 3)) : 0u;
         }
       }
       // 64-bit chunk image = 16 lanes x 4 bits: word (hl >> 3) from lanes 8w .. 8w+7
