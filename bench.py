@@ -462,7 +462,10 @@ def run_b200(args):
             # staged smem tiles (tiled kernel); gathered bytes = 4 * nnz * d
             dp_peak = 148 * 128 * clocks_mhz * 1e6 / 1e9
             gather_gbps = 2.0 * s["flops"] / sec / 1e9 if sec > 0 else 0.0
-            roof = {"kernel": {"spmm_tiled": "hb_spmm_tiled (K3/K4, TMA-staged tiles)",
+            binary = any(t is not None and t.binary for t in eng._tiles.values())
+            roof = {"kernel": {"spmm_tiled": "hb_spmm_tiled_bin (K3/K4, TMA-staged tiles, one-byte records, "
+                                             "diagonal scalings)" if binary else
+                                             "hb_spmm_tiled (K3/K4, TMA-staged tiles)",
                                "spmm_rows": "hb_spmm_csr_ex (K3/K4, row gather)"}[skey], "bound": "hbm",
                     "achieved": s["gbps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": s["gbps"] / peaks["hbm_gbs"], "traffic": _ncu_traffic(skey, args),

@@ -663,13 +663,9 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
     }
 
     // ---- pass 2: chunk pairs, two interleaved Philox blocks per lane ------------
-    // Branches are warp-uniform (ballots): divergent ones cost reconvergence
-    // bookkeeping on every chunk, and the rare cases (edge chunks, ambiguous
-    // elements, constant rows) do not need their own paths per lane.
-    const bool any_live = __any_sync(0xffffffffu, q.live);
     for (int t = 0; t < nch2; t += 2) {
       uint32_t f2[2] = {0u, 0u};
-      if (any_live) {
+      if (q.live) {
         U64x4 ua, ub;
         philox4x64_10_x2(blk0 + (uint64_t)(16 * t + hl) + 1ull, blk0 + (uint64_t)(16 * (t + 1) + hl) + 1ull,
                          sg.key0, sg.key1, ua, ub);
@@ -682,27 +678,27 @@ quantize_b1_hw_kernel(const float* __restrict__ src, int64_t ld, const int32_t* 
           const bool full = q.fast && (64 * tt - delta >= 0) && (64 * tt - delta + 64 <= d);
           uint32_t code[4];
           bool amb[4];
-          if (__all_sync(0xffffffffu, full)) {
+          if (full) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) code[i] = quant_fast_b1(xs[c0 + i], q, ws[i], amb[i]);
           } else {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int c = c0 + i;
-              const bool in = q.live && c >= 0 && c < d;
-              const float xv = xs[min(max(c, 0), d - 1)];
-              code[i] = quant_fast_b1(xv, q, ws[i], amb[i]);
-              amb[i] = in && (amb[i] || !q.fast);
-              if (!in) code[i] = 0u;
+              amb[i] = false;
+              code[i] = 0;
+              if (c >= 0 && c < d) {
+                if (q.fast) code[i] = quant_fast_b1(xs[c], q, ws[i], amb[i]);
+                else amb[i] = true;
+              }
             }
           }
-          const bool a4 = amb[0] | amb[1] | amb[2] | amb[3];
-          if (__any_sync(0xffffffffu, a4)) {
+          if (amb[0] | amb[1] | amb[2] | amb[3]) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               if (amb[i]) code[i] = (uint32_t)quant_exact(xs[c0 + i], q.mn, q.s, 1, ws[i]);
           }
-          f2[j] = q.live ? (code[0] | (code[1] << 1) | (code[2] << 2) | (code[3] << 3)) : 0u;
+          f2[j] = code[0] | (code[1] << 1) | (code[2] << 2) | (code[3] << 3);
         }
       }
       // 64-bit chunk image = 16 lanes x 4 bits: word (hl >> 3) from lanes 8w .. 8w+7

@@ -37,8 +37,7 @@ namespace sb {
 
 constexpr int kW = 64;            // columns per window (a record is col - c0 < 64)
 constexpr int kMaxRec = 2048;     // record bytes per tile (ops.TiledCsr splits denser tiles)
-constexpr int kConsumers = 16;    // consumer warps; a warp owns RB / 16 rows of the block
-constexpr int kThreads = 32 * (kConsumers + 1);
+// consumer warps per CTA (CW; a warp owns RB / CW rows of the block) + 1 producer
 // u16 row offsets per tile: RB + 1 used, padded to a 16-byte multiple
 constexpr int row_off_count(int rb) { return rb == 128 ? 136 : 72; }
 constexpr int kQ = 4;
@@ -94,13 +93,14 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 
 // 1 CTA/SM: 17 warps are allocated registers as 20 (4-warp granularity), so
 // 96 per thread is the most that launches; 2 CTAs/SM: 56
-// RB rows per block (kRPW = RB / 16 per warp), NV float4 per lane, G lanes
-// per row group, S ring stages, MINB CTAs per SM
-template <int RB, int NV, int G, int S, int MINB>
+// RB rows per block (kRPW = RB / CW per warp), NV float4 per lane, G lanes
+// per row group, S ring stages, MINB CTAs per SM, CW consumer warps
+template <int RB, int NV, int G, int S, int MINB, int CW>
 __global__ void __maxnreg__(MINB == 1 ? 96 : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   using S_ = Smem<RB, NV, G, S>;
   constexpr int P = S_::P;
+  constexpr int kConsumers = CW;
   constexpr int kRPW = RB / kConsumers;
   constexpr int kRowOff = row_off_count(RB);
   constexpr int NG = 32 / G;             // lane groups per warp (each owns whole rows)
@@ -330,7 +330,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int RB, int NV, int G, int S, int MINB>
+template <int RB, int NV, int G, int S, int MINB, int CW = 16>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   using S_ = Smem<RB, NV, G, S>;
   static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
@@ -350,14 +350,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, CW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
-  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB><<<grid, kThreads, S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, CW><<<grid, 32 * (CW + 1), S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -388,7 +388,11 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
+  static const int narrow = getenv("HB_BIN_NARROW") ? atoi(getenv("HB_BIN_NARROW")) : 1;
   if (block_rows == 64) {
+    // d <= 48: 4-lane groups x 3 float4, 8 consumer warps x 8 rows, the warp's
+    // 8 rows in parallel (one per group), 3 CTAs per SM
+    if (d <= 48 && narrow == 1) return sb::launch_nv<64, 3, 4, 4, 3, 8>(a, xrows, stream);
     if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2>(a, xrows, stream);   // 4 rows of a warp in parallel
     if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1>(a, xrows, stream);
     return sb::launch_nv<64, 2, 32, 3, 1>(a, xrows, stream);              // 256-column panels
