@@ -248,7 +248,7 @@ def spmm(a: DeviceCsr, x, out, d: int | None = None, stream=None, algo: str = "a
     sc = 2**31 - 1 if stream_col is None else int(stream_col)
     _lib.call("hb_spmm_csr_ex", a.rows, ptr(a.row_ptr), ptr(a.col_idx), ptr(a.values), ptr(x),
               x.stride(0), d, ptr(out), out.stride(0), a.nnz, SPMM_ALGOS[algo], int(window), sc,
-              ptr(getattr(a, "work", None)), stream_handle(stream))
+              ptr(a.work), stream_handle(stream))
     return out
 
 

@@ -175,6 +175,7 @@ def _transpose_device(a: "ops.DeviceCsr") -> "ops.DeviceCsr":
     rp = torch.zeros(a.cols + 1, dtype=torch.int64, device=dev)
     rp[1:] = torch.cumsum(torch.bincount(a.col_idx.long(), minlength=a.cols), 0)
     t.row_ptr = rp
+    t.work = torch.zeros(2, dtype=torch.int32, device=dev)    # the dynamic row schedule's counter pair
     return t
 
 

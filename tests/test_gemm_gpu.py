@@ -235,10 +235,17 @@ def test_relu_only_store_small_m_long_k(M, K, N):
     ws = torch.empty(64 * K * Np, device="cuda")
     R = torch.full((M, Np), 3.0, device="cuda")
     ops.gemm(A, W, None, relu_out=R[:, :N], ws=ws)
+    # the same single-split path with C stored (a workspace that holds the
+    # pre-split weight but not M x N partials: split-K off), so the ReLU copy
+    # must be the bit-identical clamp of it
     Z = torch.empty(M, N, device="cuda")
-    ops.gemm(A, W, Z, ws=ws)
+    ops.gemm(A, W, Z, ws=torch.empty(2 * N * Kp, device="cuda"))
     _check(A, W, Z)
     assert torch.equal(R[:, :N], torch.clamp(Z, min=0))
+    # and the split-K path (C only) agrees within the 3xTF32 tolerance
+    Zs = torch.empty(M, N, device="cuda")
+    ops.gemm(A, W, Zs, ws=ws)
+    _check(A, W, Zs)
 
 
 def test_simt_split_k_relu_out(gemm_path):
