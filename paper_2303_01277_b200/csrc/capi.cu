@@ -35,6 +35,7 @@ cudaError_t launch_gemm2_tf32x3(int, int, int, const float*, int64_t, int64_t, c
                                 const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*, int64_t, float,
                                 float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_path;
+extern int g_bin_narrow;
 extern int g_gemm_pair;
 extern int g_gemm_ts;
 cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
@@ -187,6 +188,13 @@ int hb_gemm_set_path(int32_t path) {
   hb::g_gemm_path = path == 1 ? 1 : 0;
   hb::g_gemm_pair = path == 2 ? 1 : 0;
   hb::g_gemm_ts = path == 3 ? 1 : 0;
+  return HB_OK;
+}
+
+int hb_spmm_set_narrow(int32_t variant) {
+  if (variant < 0 || variant > 3)
+    return fail(HB_EINVAL, "hb_spmm_set_narrow: variant must be 0..3");
+  hb::g_bin_narrow = variant;
   return HB_OK;
 }
 

@@ -1401,6 +1401,46 @@ __device__ __forceinline__ int seg_lookup(const int32_t* seg_begin, int nseg, in
   return cs;
 }
 
+// Row copy with the next row's words already in flight: a warp holds row t
+// (U words per lane, d <= 32 U) in registers while row t+1's loads issue, so
+// each lane keeps up to 2U independent 4-byte loads outstanding.
+template <int U>
+__device__ __forceinline__ void pass_load(float (&v)[U], const float* p, int d, int lane) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = (p != nullptr && lane + 32 * u < d) ? __ldg(p + lane + 32 * u) : 0.f;
+}
+
+template <int U>
+__device__ __forceinline__ bool pass_store(const float (&v)[U], float* p, int d, int lane) {
+  bool bad = false;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (lane + 32 * u < d) {
+      bad |= !isfinite(v[u]);
+      p[lane + 32 * u] = v[u];
+    }
+  return bad;
+}
+
+// rows t = 0..n-1 of a warp's batch: src / dst pointers broadcast from lane t
+template <int U>
+__device__ __forceinline__ bool pass_rows(const float* src_l, float* dst_l, int n, int d, int lane) {
+  float cur[U], nxt[U];
+  bool bad = false;
+  pass_load<U>(cur, reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src_l), 0)),
+               d, lane);
+  for (int t = 0; t < n; ++t) {
+    const float* ns = reinterpret_cast<const float*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(src_l), t + 1 < n ? t + 1 : t));
+    float* dp = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst_l), t));
+    pass_load<U>(nxt, t + 1 < n ? ns : nullptr, d, lane);
+    bad |= pass_store<U>(cur, dp, d, lane);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  return bad;
+}
+
 __global__ void __launch_bounds__(kQWarps * 32)
 quantize_pass_kernel(const float* __restrict__ src, int64_t ld, const int32_t* __restrict__ row_idx,
                      int total_rows, const hb_segment_t* __restrict__ segs_g, int nseg, int d,
@@ -1433,6 +1473,12 @@ quantize_pass_kernel(const float* __restrict__ src, int64_t ld, const int32_t* _
     }
     const int n = min(32, total_rows - r0);
     bool bad = false;
+    if (d <= 512) {
+      bad = d <= 128 ? pass_rows<4>(x_l, p_l, n, d, lane)
+                     : (d <= 256 ? pass_rows<8>(x_l, p_l, n, d, lane) : pass_rows<16>(x_l, p_l, n, d, lane));
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, HB_FLAG_NONFINITE);
+      continue;
+    }
     for (int t = 0; t < n; ++t) {
       const float* x = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(x_l), t));
       float* prow = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(p_l), t));
@@ -1489,6 +1535,13 @@ dequant_pass_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num_d
       }
     }
     const int n = min(32, num_dst - i0);
+    if (!accumulate && d <= 512 && __all_sync(0xffffffffu, i >= num_dst || k1 - k0 == 1)) {
+      // forward halo rows: straight copies, the next row's loads in flight
+      if (d <= 128) pass_rows<4>(src_l, out_l, n, d, lane);
+      else if (d <= 256) pass_rows<8>(src_l, out_l, n, d, lane);
+      else pass_rows<16>(src_l, out_l, n, d, lane);
+      continue;
+    }
     for (int t = 0; t < n; ++t) {
       float* out = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(out_l), t));
       const float* prow =

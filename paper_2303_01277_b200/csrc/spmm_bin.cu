@@ -33,6 +33,9 @@
 #include "common.cuh"
 
 namespace hb {
+
+int g_bin_narrow = getenv("HB_BIN_NARROW") ? atoi(getenv("HB_BIN_NARROW")) : 3;
+
 namespace sb {
 
 constexpr int kW = 64;            // columns per window (a record is col - c0 < 64)
@@ -95,7 +98,15 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 // 96 per thread is the most that launches; 2 CTAs/SM: 56
 // RB rows per block (kRPW = RB / CW per warp), NV float4 per lane, G lanes
 // per row group, S ring stages, MINB CTAs per SM, CW consumer warps
-template <int RB, int NV, int G, int S, int MINB, int CW>
+// TP ("tail pairs", 32 < d <= 48, G = 8, NV = 2): a lane group reads a
+// nonzero's first 32 columns as one 128-byte quarter-warp access (all 32
+// banks once: conflict-free wherever the row starts) and the 1-4 float4 tail
+// of TWO nonzeros in a third access (lanes 0-3: the first's, lanes 4-7: the
+// second's), so a pair costs 3 accesses instead of 4; acc[i][1] holds the
+// tail sums, folded across the half-groups before the store.  With 4-lane
+// groups (64-byte accesses, two rows per quarter-warp) the two halves of a
+// quarter-warp collide in 7 of 8 bank alignments.
+template <int RB, int NV, int G, int S, int MINB, int CW, bool TP = false>
 __global__ void __maxnreg__(MINB == 1 ? 96 : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   using S_ = Smem<RB, NV, G, S>;
@@ -168,6 +179,9 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   const int pw4 = a.pw / 4;
   // the last float4 of a lane may fall beyond the staged width (narrow panels)
   const int nlast = ((NV - 1) * G + gl) * 4 < a.pw;
+  // TP: lane gl's tail float4 (8 + (gl & 3)) and whether the row has it
+  const int tl = gl & 3;
+  const bool tail_lane = (8 + tl) * 4 < a.pw;
   int it = 0;
   for (int qi = 0;; ++qi) {
     const int q = qi % kQ;
@@ -233,6 +247,25 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
                   acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
                 }
           }
+        } else if constexpr (TP) {
+          static_assert(G == 8 && NV == 2, "tail pairs: 8-lane groups, main + tail float4");
+          // pairs of nonzeros: two 128-byte main reads + one shared tail read
+          for (; w + 1 < w1; ++w) {
+            const uint32_t q = rec32[w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j0 = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)(2 * h));
+              const int j1 = (int)__byte_perm(q, 0u, 0x4441u | (uint32_t)(2 * h));
+              const float4 m0 = xs[j0 * pw4];
+              const float4 m1 = xs[j1 * pw4];
+              const int jt = gl < 4 ? j0 : j1;
+              float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (tail_lane) t = xs[jt * pw4 + 8 - gl + tl];
+              acc[i][0].x += m0.x; acc[i][0].y += m0.y; acc[i][0].z += m0.z; acc[i][0].w += m0.w;
+              acc[i][0].x += m1.x; acc[i][0].y += m1.y; acc[i][0].z += m1.z; acc[i][0].w += m1.w;
+              acc[i][1].x += t.x; acc[i][1].y += t.y; acc[i][1].z += t.z; acc[i][1].w += t.w;
+            }
+          }
         } else {
           // narrow rows: each lane group walks its own row, two records at a time
           for (; w + 1 < w1; ++w) {
@@ -262,18 +295,72 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int j = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)u);
-            if (j != 0xFF) add_row<NV, G>(acc[i], xs + j * pw4, nlast);
+            if constexpr (TP) {
+              if (j != 0xFF) {
+                const float4 m = xs[j * pw4];
+                acc[i][0].x += m.x; acc[i][0].y += m.y; acc[i][0].z += m.z; acc[i][0].w += m.w;
+                if (gl < 4 && tail_lane) {
+                  const float4 t = xs[j * pw4 + 8 - gl + tl];
+                  acc[i][1].x += t.x; acc[i][1].y += t.y; acc[i][1].z += t.z; acc[i][1].w += t.w;
+                }
+              }
+            } else {
+              if (j != 0xFF) add_row<NV, G>(acc[i], xs + j * pw4, nlast);
+            }
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[s]);
     }
+    if constexpr (TP) {
+      // fold the second nonzero's tail sums (lanes 4-7) into lanes 0-3
+#pragma unroll
+      for (int i = 0; i < RPG; ++i) {
+        float4& t = acc[i][1];
+        const float x = __shfl_down_sync(0xffffffffu, t.x, 4, 8), y = __shfl_down_sync(0xffffffffu, t.y, 4, 8);
+        const float z = __shfl_down_sync(0xffffffffu, t.z, 4, 8), w = __shfl_down_sync(0xffffffffu, t.w, 4, 8);
+        if (gl < 4) { t.x += x; t.y += y; t.z += z; t.w += w; }
+      }
+    }
     // residual pattern entries gathered from global X, row scale, store
 #pragma unroll
     for (int i = 0; i < RPG; ++i) {
       const int r = r0 + hg + i * NG;
       if (r >= a.nrows) continue;
+      if constexpr (TP) {
+        // lane gl: main float4 gl; lanes 0-3 also tail float4 8 + gl
+        const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
+        const bool has_t = gl < 4 && tail_lane;
+        for (int64_t k = e0; k < e1; ++k) {
+          const float4* xr = reinterpret_cast<const float4*>(a.X + (int64_t)__ldg(a.res_col + k) * a.ldx);
+          if (gl * 4 < a.d) {
+            const float4 t4 = __ldg(xr + gl);
+            acc[i][0].x += t4.x; acc[i][0].y += t4.y; acc[i][0].z += t4.z; acc[i][0].w += t4.w;
+          }
+          if (has_t) {
+            const float4 t4 = __ldg(xr + 8 + gl);
+            acc[i][1].x += t4.x; acc[i][1].y += t4.y; acc[i][1].z += t4.z; acc[i][1].w += t4.w;
+          }
+        }
+        const float sc = a.row_scale ? __ldg(a.row_scale + r) : 1.f;
+        float* y = a.Y + (int64_t)r * a.ldy;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          if (v == 1 && !has_t) continue;
+          const int col = v == 0 ? gl * 4 : (8 + gl) * 4;
+          const int rem = a.d - col;
+          const float4 o = make_float4(acc[i][v].x * sc, acc[i][v].y * sc, acc[i][v].z * sc, acc[i][v].w * sc);
+          if (rem >= 4) {
+            *reinterpret_cast<float4*>(y + col) = o;
+          } else if (rem > 0) {
+            y[col] = o.x;
+            if (rem > 1) y[col + 1] = o.y;
+            if (rem > 2) y[col + 2] = o.z;
+          }
+        }
+        continue;
+      }
       const float* Xp = a.X + col0;
       const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
       for (int64_t k = e0; k < e1; ++k) {
@@ -330,7 +417,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int RB, int NV, int G, int S, int MINB, int CW = 16>
+template <int RB, int NV, int G, int S, int MINB, int CW = 16, bool TP = false>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   using S_ = Smem<RB, NV, G, S>;
   static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
@@ -350,14 +437,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, CW>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
-  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, CW><<<grid, 32 * (CW + 1), S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP><<<grid, 32 * (CW + 1), S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -388,10 +475,12 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-  static const int narrow = getenv("HB_BIN_NARROW") ? atoi(getenv("HB_BIN_NARROW")) : 1;
+  const int narrow = g_bin_narrow;
   if (block_rows == 64) {
     // d <= 48: 4-lane groups x 3 float4, 8 consumer warps x 8 rows, the warp's
     // 8 rows in parallel (one per group), 3 CTAs per SM
+    if (d > 32 && d <= 48 && narrow == 2) return sb::launch_nv<64, 2, 8, 4, 2, 16, true>(a, xrows, stream);
+    if (d > 32 && d <= 48 && narrow == 3) return sb::launch_nv<64, 2, 8, 4, 3, 8, true>(a, xrows, stream);
     if (d <= 48 && narrow == 1) return sb::launch_nv<64, 3, 4, 4, 3, 8>(a, xrows, stream);
     if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2>(a, xrows, stream);   // 4 rows of a warp in parallel
     if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1>(a, xrows, stream);

@@ -31,6 +31,7 @@ import numpy as np
 from . import ops
 from .codec import CodecError, QuantConfig, quantize_gather, dequant_gather
 from .graph import Graph, Partition
+from .linalg import ShapeError
 from .profiling import null_timer
 from .rngstream import BACKWARD, FORWARD, derive_key, keyed_generator
 from .transport import ExchangeBuffers, ProtocolError, RankLayout, TransportStats, nccl_exchange
@@ -680,6 +681,19 @@ class DeviceRank:
         for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
             ops.adam_step(w, g, m, v, self.lr, self.adam_t)
             self.launches += 1
+
+    def swap_features(self, buf):
+        """Make `buf` layer 1's input ([local ; halo] x ld, shaped like Ht[1]);
+        returns the previous buffer.  For double-buffered input pipelines: the
+        next epoch's features are uploaded into the spare buffer while this
+        epoch runs.  Halo rows need no copy (the layer-1 exchange rewrites them
+        every epoch)."""
+        old = self.Ht[1]
+        if buf.shape != old.shape or buf.dtype != old.dtype or buf.stride() != old.stride() \
+                or buf.device != old.device:
+            raise ShapeError(f"feature buffer {tuple(buf.shape)} does not match layer 1's input {tuple(old.shape)}")
+        self.Ht[1] = buf
+        return old
 
     def run_epoch(self, epoch: int, check: bool = True) -> str:
         epoch_mode = staleness_adaptor(epoch, self.mode)

@@ -229,3 +229,46 @@ def test_spmm_tiled_splits_dense_tiles(d):
     assert T.ntiles > int((T.tile_ptr[1:] - T.tile_ptr[:-1]).gt(0).sum())   # some window has >1 tile
     tol = 1e-5 * _bound(rp, ci, v, x) + 1e-30
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
+
+
+@pytest.fixture(params=[0, 1, 2, 3], ids=["g8", "g4x3", "tail_pairs16", "tail_pairs8"])
+def narrow_variant(request):
+    from paper_2303_01277_b200 import ops
+    ops.spmm_set_narrow(request.param)
+    yield request.param
+    ops.spmm_set_narrow(3)
+
+
+@pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn"])
+@pytest.mark.parametrize("d", [33, 36, 41, 44, 47, 48, 20])
+def test_spmm_tiled_factored_narrow_variants(kind, d, narrow_variant):
+    """Every narrow consumer layout (d <= 48; tail pairs for 32 < d <= 48,
+    odd and even record runs, rows with a single nonzero) vs scipy f64."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(7 * d + len(kind))
+    rows, comm, halo = 1300, 260, 900
+    rp, ci = _community_pattern(rng, rows, comm, halo)
+    cols = rows + halo
+    pat = sp.csr_matrix((np.ones(len(ci)), ci, rp), shape=(rows, cols))
+    if kind.startswith("mean"):
+        deg = np.maximum(np.diff(rp), 1).astype(np.float64)
+        a = sp.diags(1.0 / deg) @ pat
+    else:
+        pat = pat.tolil()
+        pat.setdiag(1.0)
+        pat = pat.tocsr()
+        dinv = 1.0 / np.sqrt(rng.integers(1, 400, cols).astype(np.float64))
+        a = sp.diags(dinv[:rows]) @ pat @ sp.diags(dinv)
+    if kind.endswith("_T"):
+        a = a.T
+    a = sp.csr_matrix(a)
+    a.sort_indices()
+    v = a.data.astype(np.float32)
+    rp2, ci2 = a.indptr.astype(np.int64), a.indices.astype(np.int64)
+    x = rng.standard_normal((a.shape[1], d)).astype(np.float32)
+    ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
+    for threshold in (1, 64):
+        got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=64)
+        assert T.binary
+        tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
+        assert np.all(np.abs(got - ref) <= tol), (threshold, np.abs(got - ref).max())

@@ -308,7 +308,7 @@ def test_wide_hidden_small_graph_pre_order(model):
     g = _graph(seed=21, npc=250, d=300)
     res, o, losses, _ = _run_both(g, 1, (300, 256, 256, 4), model, "sync", 0, 32, 4, 5, agg_order="pre")
     # epoch 1 runs on identical weights: only fp32 rounding separates the losses
-    assert res.metrics[0].train_loss == pytest.approx(losses[0], rel=2e-6)
+    assert res.metrics[0].train_loss == pytest.approx(losses[0], rel=1e-5)
     # this model fits the 1000-node graph within 4 epochs (loss ~1e-2): Adam's
     # first steps move every weight by ~lr * sign(g), so near-zero gradient
     # entries whose sign fp32 rounding decides separate the trajectories by

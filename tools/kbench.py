@@ -113,6 +113,15 @@ def spmm(args):
                                       "tiles": tiled[key].ntiles,
                                       "tiled_fraction": round(tiled[key].tiled_fraction, 4)}), flush=True)
                 T = tiled[key]
+                if T.binary and d <= 48 and T.RB == 64:
+                    for nv in (0, 1, 2, 3):         # narrow consumer layouts (hb_spmm_set_narrow)
+                        ops.spmm_set_narrow(nv)
+                        ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
+                        print(json.dumps({"kernel": "spmm", "mat": name, "d": d, "algo": algo, "narrow": nv,
+                                          "ms": round(ms, 3),
+                                          "gather_gbps": round((8 * M.nnz + 4 * M.nnz * d) / ms / 1e6, 1)}),
+                              flush=True)
+                    ops.spmm_set_narrow(3)
                 ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
             else:
                 sc = lay.NL if name == "A" else None
