@@ -192,11 +192,12 @@ int hb_gemm_set_path(int32_t path);
 
 /* Tuning / test hook: the consumer layout of hb_spmm_tiled_bin for narrow
  * rows (d <= 48, 64-row blocks).  0 = 8-lane groups x 2 float4 (2 CTAs/SM);
- * 1 = 4-lane groups x 3 float4, 8 consumer warps x 8 rows (3 CTAs/SM);
+ * 1 = 4-lane groups x 3 float4, 8 consumer warps x 8 rows (3 CTAs/SM) —
+ * the default;
  * 2 = "tail pairs" (32 < d <= 48): 8-lane groups read a nonzero's first 32
  * columns as one 128-byte access and the tails of two nonzeros in a third,
  * 16 consumer warps (2 CTAs/SM); 3 = tail pairs with 8 consumer warps x 8
- * rows (3 CTAs/SM) — the default. */
+ * rows (3 CTAs/SM). */
 int hb_spmm_set_narrow(int32_t variant);
 
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:

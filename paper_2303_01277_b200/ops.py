@@ -291,8 +291,8 @@ def gemm2(A1, B1, A2, B2, C, beta: float = 0.0, relu_out=None, ws=None, stream=N
 
 def spmm_set_narrow(variant: int):
     """Consumer layout of the factored tiled SpMM for d <= 48 (tuning / tests):
-    0 8-lane groups, 1 4-lane groups, 2 / 3 tail pairs (16 / 8 consumer warps;
-    3 is the default).  See hb_spmm_set_narrow."""
+    0 8-lane groups, 1 4-lane groups (the default), 2 / 3 tail pairs (16 / 8
+    consumer warps).  See hb_spmm_set_narrow."""
     _lib.call("hb_spmm_set_narrow", int(variant))
 
 

@@ -236,7 +236,7 @@ def narrow_variant(request):
     from paper_2303_01277_b200 import ops
     ops.spmm_set_narrow(request.param)
     yield request.param
-    ops.spmm_set_narrow(3)
+    ops.spmm_set_narrow(1)
 
 
 @pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn"])

@@ -121,7 +121,7 @@ def spmm(args):
                                           "ms": round(ms, 3),
                                           "gather_gbps": round((8 * M.nnz + 4 * M.nnz * d) / ms / 1e6, 1)}),
                               flush=True)
-                    ops.spmm_set_narrow(3)
+                    ops.spmm_set_narrow(1)
                 ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
             else:
                 sc = lay.NL if name == "A" else None
