@@ -137,8 +137,10 @@ int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* 
  * D^-1 A, its transpose A^T D^-1, GCN D^-1/2 (A+I) D^-1/2):
  *   Y[i, 0:d) = r[i] * sum_{(i,j) in pattern} c[j] * X[j, 0:d)
  * row_scale r / col_scale c may each be NULL (= 1).  Tiles are block_rows
- * (64 or 128) rows x 64 columns (nblocks = ceil(nrows / block_rows)); a
- * record is one byte, the column inside the tile's window;
+ * (64 or 128) rows x window_cols columns: 64; for d <= 48 also 128 (64-row
+ * blocks) or 255 (64-row blocks, or 128-row blocks with 32 < d <= 48;
+ * records up to 4096 bytes per tile then) (nblocks = ceil(nrows / block_rows)); a record is one byte, the
+ * column inside the tile's window;
  * tile_rec[tile_off[t] .. tile_off[t+1]) (byte offsets, multiples of 16) are
  * tile t's row-sorted records and tile_rowoff[t*R .. +block_rows+1) their
  * row offsets (R = 72 for 64-row blocks, 136 for 128); res_ptr / res_col the
@@ -150,7 +152,7 @@ int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32
                       const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                       const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
                       float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, int32_t block_rows,
-                      void* stream);
+                      int32_t window_cols, void* stream);
 
 /* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
  * tensor cores with the 3xTF32 split (fp32 accuracy):
@@ -191,13 +193,13 @@ int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1
 int hb_gemm_set_path(int32_t path);
 
 /* Tuning / test hook: the consumer layout of hb_spmm_tiled_bin for narrow
- * rows (d <= 48, 64-row blocks).  0 = 8-lane groups x 2 float4 (2 CTAs/SM);
- * 1 = 4-lane groups x 3 float4, 8 consumer warps x 8 rows (3 CTAs/SM) —
- * the default;
- * 2 = "tail pairs" (32 < d <= 48): 8-lane groups read a nonzero's first 32
- * columns as one 128-byte access and the tails of two nonzeros in a third,
- * 16 consumer warps (2 CTAs/SM); 3 = tail pairs with 8 consumer warps x 8
- * rows (3 CTAs/SM). */
+ * rows (d <= 48, 64-row blocks).  64- and 128-column windows: 0 = 8-lane
+ * groups x 2 float4 (2 CTAs/SM); 1 = 4-lane groups x 3 float4, 8 consumer
+ * warps x 8 rows (3 CTAs/SM) — the default; 2 / 3 = "tail pairs" (32 < d <=
+ * 48): 8-lane groups read a nonzero's first 32 columns as one 128-byte
+ * access and the tails of two nonzeros in a third (16 / 8 consumer warps).
+ * 255-column windows: 1 or 3 (default) = tail pairs, 2 CTAs/SM; 2 = tail
+ * pairs, 1 CTA/SM; 0 = 4-lane groups. */
 int hb_spmm_set_narrow(int32_t variant);
 
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:

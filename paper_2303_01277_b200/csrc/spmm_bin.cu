@@ -37,11 +37,15 @@ namespace hb {
 // narrow-row consumer layout (hb_spmm_set_narrow); 1 measured fastest at
 // d = 41 on Reddit (1.41 ms vs 1.54 / 1.56 / 1.61 ms for 0 / 2 / 3)
 int g_bin_narrow = getenv("HB_BIN_NARROW") ? atoi(getenv("HB_BIN_NARROW")) : 1;
+// 128-row blocks, d > 128: 1 = 256-column panels (two records in flight), 0 = 128-column panels
+int g_bin_wide128 = getenv("HB_BIN_WIDE128") ? atoi(getenv("HB_BIN_WIDE128")) : 1;
 
 namespace sb {
 
-constexpr int kW = 64;            // columns per window (a record is col - c0 < 64)
-constexpr int kMaxRec = 2048;     // record bytes per tile (ops.TiledCsr splits denser tiles)
+// columns per window KW (64, or 128 for narrow rows): a record is col - c0 < KW
+// record bytes per tile (ops.TiledCsr splits denser tiles): 2048, 4096 for
+// 128-row x 255-column narrow tiles
+constexpr int max_rec(int rb, int kw) { return rb == 128 && kw == 255 ? 4096 : 2048; }
 // consumer warps per CTA (CW; a warp owns RB / CW rows of the block) + 1 producer
 // u16 row offsets per tile: RB + 1 used, padded to a 16-byte multiple
 constexpr int row_off_count(int rb) { return rb == 128 ? 136 : 72; }
@@ -64,12 +68,14 @@ struct Args {
   int64_t ldy;
 };
 
-template <int RB, int NV, int G, int S>
+template <int RB, int NV, int G, int S, int KW = 64, bool TP = false>
 struct Smem {
-  static constexpr int P = 4 * G * NV;
-  static constexpr int X_BYTES = kW * P * 4;
+  // panel width in floats (TP: at most 48 columns, one panel)
+  static constexpr int P = TP ? 48 : 4 * G * NV;
+  static constexpr int X_BYTES = (KW * P * 4 + 127) / 128 * 128;   // TMA destinations: 128-byte aligned
   static constexpr int RO_BYTES = row_off_count(RB) * 2;
-  static constexpr int STAGE = X_BYTES + kMaxRec + RO_BYTES + 112;   // 16-byte multiple
+  static constexpr int MAXREC = max_rec(RB, KW);
+  static constexpr int STAGE = X_BYTES + MAXREC + RO_BYTES + 112;   // 16-byte multiple
   static constexpr int TOTAL = S * STAGE + 128;
   static_assert(STAGE % 16 == 0, "stage alignment");
 };
@@ -108,10 +114,10 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 // tail sums, folded across the half-groups before the store.  With 4-lane
 // groups (64-byte accesses, two rows per quarter-warp) the two halves of a
 // quarter-warp collide in 7 of 8 bank alignments.
-template <int RB, int NV, int G, int S, int MINB, int CW, bool TP = false>
+template <int RB, int NV, int G, int S, int MINB, int CW, bool TP = false, int KW = 64>
 __global__ void __maxnreg__(MINB == 1 ? 96 : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
-  using S_ = Smem<RB, NV, G, S>;
+  using S_ = Smem<RB, NV, G, S, KW, TP>;
   constexpr int P = S_::P;
   constexpr int kConsumers = CW;
   constexpr int kRPW = RB / kConsumers;
@@ -166,10 +172,10 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         uint8_t* st = smem + s * S_::STAGE;
         const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
         const uint32_t rb = (uint32_t)(o1 - o0);
-        mbar_expect_tx(&full[s], (uint32_t)(kW * a.pw * 4) + rb + S_::RO_BYTES);
-        tma_2d(st, &tmX, pn * P, a.tile_win[t] * kW, &full[s]);
+        mbar_expect_tx(&full[s], (uint32_t)(KW * a.pw * 4) + rb + S_::RO_BYTES);
+        tma_2d(st, &tmX, pn * P, a.tile_win[t] * KW, &full[s]);
         if (rb) tma_load_1d(st + S_::X_BYTES, a.tile_rec + o0, rb, &full[s]);
-        tma_load_1d(st + S_::X_BYTES + kMaxRec, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES, &full[s]);
+        tma_load_1d(st + S_::X_BYTES + S_::MAXREC, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES, &full[s]);
       }
     }
     __syncwarp();
@@ -206,7 +212,7 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       const uint8_t* st = smem + s * S_::STAGE;
       const float4* xs = reinterpret_cast<const float4*>(st) + gl;
       const uint32_t* rec32 = reinterpret_cast<const uint32_t*>(st + S_::X_BYTES);
-      const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + kMaxRec) + warp * kRPW;
+      const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + S_::MAXREC) + warp * kRPW;
       // the warp's kRPW + 1 row offsets in two broadcast loads (not 2 per row)
       uint64_t ro_lo, ro_hi = 0;
       if constexpr (kRPW == 4) {
@@ -230,30 +236,39 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         const int w1 = row_off(rr + 1) >> 2;
         int w = row_off(rr) >> 2;
         if constexpr (G == 32) {
+          // records in flight per warp: 4, or 2 when the accumulators of a
+          // 128-row block (8 rows x NV float4) leave no registers for more
+          constexpr int kU = RPG * NV > 8 ? 2 : 4;
           for (; w + 1 < w1; ++w) {
             const uint32_t q = rec32[w];                           // 4 records, one broadcast
-            float4 x[4][NV];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)u);
+            for (int u0 = 0; u0 < 4; u0 += kU) {
+              float4 x[kU][NV];
 #pragma unroll
-              for (int v = 0; v < NV; ++v)
-                if (v < NV - 1 || nlast) x[u][v] = xs[j * pw4 + v * G];
+              for (int u = 0; u < kU; ++u) {
+                const int j = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)(u0 + u));
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  if (v < NV - 1 || nlast) x[u][v] = xs[j * pw4 + v * G];
+              }
+#pragma unroll
+              for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  if (v < NV - 1 || nlast) {
+                    acc[i][v].x += x[u][v].x; acc[i][v].y += x[u][v].y;
+                    acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
+                  }
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int v = 0; v < NV; ++v)
-                if (v < NV - 1 || nlast) {
-                  acc[i][v].x += x[u][v].x; acc[i][v].y += x[u][v].y;
-                  acc[i][v].z += x[u][v].z; acc[i][v].w += x[u][v].w;
-                }
           }
         } else if constexpr (TP) {
           static_assert(G == 8 && NV == 2, "tail pairs: 8-lane groups, main + tail float4");
-          // pairs of nonzeros: two 128-byte main reads + one shared tail read
+          // pairs of nonzeros: two 128-byte main reads + one shared tail read;
+          // the next record word is loaded before this word's X rows
+          uint32_t qn = w + 1 < w1 ? rec32[w] : 0u;
           for (; w + 1 < w1; ++w) {
-            const uint32_t q = rec32[w];
+            const uint32_t q = qn;
+            qn = rec32[w + 1];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int j0 = (int)__byte_perm(q, 0u, 0x4440u | (uint32_t)(2 * h));
@@ -419,9 +434,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int RB, int NV, int G, int S, int MINB, int CW = 16, bool TP = false>
+template <int RB, int NV, int G, int S, int MINB, int CW = 16, bool TP = false, int KW = 64>
 static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
-  using S_ = Smem<RB, NV, G, S>;
+  using S_ = Smem<RB, NV, G, S, KW, TP>;
   static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
   Args a = a0;
   a.npanels = (a.d + S_::P - 1) / S_::P;
@@ -431,7 +446,7 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)xrows};
   cuuint64_t strides[1] = {(cuuint64_t)(a.ldx * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)a.pw, (cuuint32_t)kW};
+  cuuint32_t box[2] = {(cuuint32_t)a.pw, (cuuint32_t)KW};
   cuuint32_t es[2] = {1u, 1u};
   if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.X), dims, strides, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -439,14 +454,14 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
     return cudaErrorNotSupported;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP>,
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP, KW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items = a.nblocks * a.npanels;
   const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
-  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP><<<grid, 32 * (CW + 1), S_::TOTAL, stream>>>(map, a);
+  if (grid > 0) spmm_bin_kernel<RB, NV, G, S, MINB, CW, TP, KW><<<grid, 32 * (CW + 1), S_::TOTAL, stream>>>(map, a);
   return cudaGetLastError();
 }
 
@@ -457,7 +472,7 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
                                   const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                                   const float* row_scale, const float* col_scale, const float* X, int64_t ldx,
                                   int d, float* Y, int64_t ldy, float* xs, int64_t ldxs, int* work,
-                                  int block_rows, cudaStream_t stream) {
+                                  int block_rows, int window_cols, cudaStream_t stream) {
   if (nrows <= 0 || d <= 0) return cudaSuccess;
   if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
   if (col_scale) {
@@ -478,6 +493,32 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
   a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
   const int narrow = g_bin_narrow;
+  if (window_cols == 255) {
+    // 255-column windows (one-byte records 0..254, 0xFF = padding)
+    if (d > 48) return cudaErrorInvalidValue;
+    if (block_rows == 128) {
+      // 128-row blocks: each staged window serves twice the rows; 16 consumer
+      // warps x 8 rows (tail pairs, two rows per lane group), 2 CTAs per SM
+      if (d <= 32) return cudaErrorInvalidValue;
+      return sb::launch_nv<128, 2, 8, 2, 2, 16, true, 255>(a, xrows, stream);
+    }
+    if (block_rows != 64) return cudaErrorInvalidValue;
+    // default (1, 3): tail pairs, 2 CTAs per SM (1.03 ms at d = 41 on Reddit);
+    // 2: tail pairs, 1 CTA per SM; 0 (or d <= 32): 4-lane groups
+    if (d > 32 && narrow == 2) return sb::launch_nv<64, 2, 8, 2, 1, 16, true, 255>(a, xrows, stream);
+    if (d > 32 && narrow != 0) return sb::launch_nv<64, 2, 8, 2, 2, 16, true, 255>(a, xrows, stream);
+    return sb::launch_nv<64, 3, 4, 2, 2, 8, false, 255>(a, xrows, stream);
+  }
+  if (window_cols == 128) {
+    // 128-column windows (narrow rows): twice the nonzeros per (row, tile)
+    // for the per-row record-run overhead
+    if (block_rows != 64 || d > 48) return cudaErrorInvalidValue;
+    if (d > 32 && narrow == 2) return sb::launch_nv<64, 2, 8, 2, 3, 8, true, 128>(a, xrows, stream);
+    if (d > 32 && narrow == 3) return sb::launch_nv<64, 2, 8, 3, 2, 16, true, 128>(a, xrows, stream);
+    if (narrow == 0) return sb::launch_nv<64, 3, 4, 4, 2, 8, false, 128>(a, xrows, stream);
+    return sb::launch_nv<64, 3, 4, 2, 3, 8, false, 128>(a, xrows, stream);
+  }
+  if (window_cols != 64) return cudaErrorInvalidValue;
   if (block_rows == 64) {
     // d <= 48: 4-lane groups x 3 float4, 8 consumer warps x 8 rows, the warp's
     // 8 rows in parallel (one per group), 3 CTAs per SM
@@ -489,9 +530,13 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
     return sb::launch_nv<64, 2, 32, 3, 1>(a, xrows, stream);              // 256-column panels
   }
   if (block_rows != 128) return cudaErrorInvalidValue;
-  // 128-row blocks: 8 rows per warp, so 128-column panels (register budget)
+  // 128-row blocks: 8 rows per warp; a TMA-staged X window serves twice the
+  // rows (half the window writes into shared memory per nonzero).  256-column
+  // panels with two records in flight per warp (register budget), 128-column
+  // panels for d <= 128
   if (d <= 64) return sb::launch_nv<128, 2, 8, 4, 2>(a, xrows, stream);
-  return sb::launch_nv<128, 1, 32, 5, 1>(a, xrows, stream);
+  if (d <= 128 || g_bin_wide128 == 0) return sb::launch_nv<128, 1, 32, 5, 1>(a, xrows, stream);
+  return sb::launch_nv<128, 2, 32, 3, 1>(a, xrows, stream);
 }
 
 }  // namespace hb

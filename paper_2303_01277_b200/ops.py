@@ -104,12 +104,11 @@ class TiledCsr:
     * factored (``hb_spmm_tiled_bin``, when ``factor_scales`` finds the values
       to be r[i] c[j] over a 0/1 pattern — the trainer's aggregation
       operators): 64- or 128-row blocks, one-byte column records, r / c
-      applied as diagonal scalings."""
-
-    W = 64
+      applied as diagonal scalings; ``window=128`` (64-row blocks, rows of
+      at most 48 columns) doubles the nonzeros per (row, tile)."""
 
     def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None,
-                 block_rows: int | None = None):
+                 block_rows: int | None = None, window: int = 64):
         import torch
         dev = a.row_ptr.device
         scales = factor_scales(a) if factored in (None, True) else None
@@ -125,6 +124,12 @@ class TiledCsr:
             self.RB, self.ROWOFF, self.MAXREC = rb, (136 if rb == 128 else 72), 2048
         else:
             self.RB, self.ROWOFF, self.MAXREC = 64, 72, 1024
+        if window not in (64, 128, 255) or (window != 64 and not self.binary) or \
+                (window == 128 and self.RB != 64):
+            raise ValueError("128-column windows need factored 64-row tiles, 255-column ones factored tiles")
+        if window == 255 and self.RB == 128:
+            self.MAXREC = 4096
+        self.W = window
         self.rows, self.cols, self.nnz = a.rows, a.cols, a.nnz
         self.work = torch.zeros(2, dtype=torch.int32, device=dev)
         self._xs = {}
@@ -229,7 +234,7 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
         _lib.call("hb_spmm_tiled_bin", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),
                   ptr(t.tile_off), ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col),
                   ptr(t.row_scale), ptr(t.col_scale), ptr(x), x.stride(0), d, ptr(out), out.stride(0),
-                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), t.RB, stream_handle(stream))
+                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), t.RB, t.W, stream_handle(stream))
         return out
     _lib.call("hb_spmm_tiled", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win), ptr(t.tile_off),
               ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col), ptr(t.res_val), ptr(x),
@@ -290,9 +295,9 @@ def gemm2(A1, B1, A2, B2, C, beta: float = 0.0, relu_out=None, ws=None, stream=N
 
 
 def spmm_set_narrow(variant: int):
-    """Consumer layout of the factored tiled SpMM for d <= 48 (tuning / tests):
-    0 8-lane groups, 1 4-lane groups (the default), 2 / 3 tail pairs (16 / 8
-    consumer warps).  See hb_spmm_set_narrow."""
+    """Consumer layout of the factored tiled SpMM for d <= 48 (tuning / tests);
+    the meaning depends on the tile window, see hb_spmm_set_narrow (1 is the
+    default)."""
     _lib.call("hb_spmm_set_narrow", int(variant))
 
 

@@ -221,6 +221,9 @@ class DeviceRank:
         if self.spmm_impl not in ("auto", "rows", "tiled"):
             raise TrainingError(f"unknown SpMM implementation {self.spmm_impl!r}")
         self._tiles = {}
+        # factored SpMM rows of <= 48 columns: 255-column windows (1.03-1.07 ms
+        # vs 1.41-1.43 with 64 at d = 41 on Reddit, profiles/r2_kbench_spmm_narrow_windows.jsonl)
+        self.narrow_window = int(os.environ.get("HB_NARROW_WINDOW", "255"))
         self.gemm_impl = os.environ.get("HB_GEMM", "tcgen05")
         if self.gemm_impl not in GEMM_FLOPS:
             raise TrainingError(f"unknown GEMM implementation {self.gemm_impl!r}")
@@ -488,21 +491,29 @@ class DeviceRank:
                 ops.gemm2(a1, b1, a2, b2, out, relu_out=relu_out, ws=self.gemm_ws)
                 self.launches += 1
 
-    def _tiled(self, a):
+    def _tiled(self, a, d: int = 0):
         """Tiled (TMA-staged) layout of `a`, built on first use; None when too
-        little of the matrix falls into dense tiles to pay off."""
+        little of the matrix falls into dense tiles to pay off.  Rows of 33-48
+        columns use their own factored layout with 255-column windows
+        (HB_NARROW_WINDOW) when the operator factors."""
         key = id(a)
         if key not in self._tiles:
             t = ops.TiledCsr(a)
             self._tiles[key] = t if t.tiled_fraction >= 0.5 else None
-        return self._tiles[key]
+        t = self._tiles[key]
+        if t is not None and t.binary and 32 < d <= 48 and self.narrow_window != 64:
+            nkey = (key, "narrow")
+            if nkey not in self._tiles:
+                self._tiles[nkey] = ops.TiledCsr(a, factored=True, block_rows=64, window=self.narrow_window)
+            t = self._tiles[nkey]
+        return t
 
     def _spmm(self, a, x, y, d: int):
         """K3/K4: the TMA-staged tiled kernel where the matrix has dense
         (community) blocks, the row-gather kernel otherwise."""
         # auto: the tiled kernel for wide (> 128) and narrow (<= 64, row-per-
         # lane-group consumers) panels of community-structured blocks
-        t = self._tiled(a) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and (d > 128 or d <= 64))) \
+        t = self._tiled(a, d) if (self.spmm_impl == "tiled" or (self.spmm_impl == "auto" and (d > 128 or d <= 64))) \
             else None
         name = "spmm_rows" if t is None else ("spmm_tiled_narrow" if d <= 64 else "spmm_tiled")
         with self.timer(name, *_spmm_cost(a, d)):

@@ -76,11 +76,11 @@ def test_spmm_random_power_law_rows(d):
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None, block_rows=None):
+def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None, block_rows=None, window=64):
     from paper_2303_01277_b200 import ops
     rows, d = len(rp) - 1, x.shape[1]
     A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
-    T = ops.TiledCsr(A, threshold=threshold, factored=factored, block_rows=block_rows)
+    T = ops.TiledCsr(A, threshold=threshold, factored=factored, block_rows=block_rows, window=window)
     X = torch.zeros(ncols, d + ld_pad, device="cuda")
     X[:, :d] = torch.from_numpy(x)
     Y = torch.full((rows, d + ld_pad), 7.0, device="cuda")
@@ -239,11 +239,12 @@ def narrow_variant(request):
     ops.spmm_set_narrow(1)
 
 
+@pytest.mark.parametrize("window", [64, 128, 255])
 @pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn"])
 @pytest.mark.parametrize("d", [33, 36, 41, 44, 47, 48, 20])
-def test_spmm_tiled_factored_narrow_variants(kind, d, narrow_variant):
+def test_spmm_tiled_factored_narrow_variants(kind, d, window, narrow_variant):
     """Every narrow consumer layout (d <= 48; tail pairs for 32 < d <= 48,
-    odd and even record runs, rows with a single nonzero) vs scipy f64."""
+    odd and even record runs), with 64- and 128-column windows, vs scipy f64."""
     import scipy.sparse as sp
     rng = np.random.default_rng(7 * d + len(kind))
     rows, comm, halo = 1300, 260, 900
@@ -268,7 +269,14 @@ def test_spmm_tiled_factored_narrow_variants(kind, d, narrow_variant):
     x = rng.standard_normal((a.shape[1], d)).astype(np.float32)
     ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
     for threshold in (1, 64):
-        got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=64)
-        assert T.binary
+        got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=64,
+                            window=window)
+        assert T.binary and T.W == window
+        tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
+        assert np.all(np.abs(got - ref) <= tol), (threshold, np.abs(got - ref).max())
+        if window == 255 and d > 32:           # 128-row blocks with 255-column windows
+            got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True,
+                                block_rows=128, window=window)
+            assert T.RB == 128 and T.W == 255
         tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
         assert np.all(np.abs(got - ref) <= tol), (threshold, np.abs(got - ref).max())

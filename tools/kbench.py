@@ -98,6 +98,8 @@ def spmm(args):
         Y = torch.zeros(M.rows, ld, device="cuda")
         comp = 8 * (M.rows + 1) + 8 * M.nnz + 4 * M.cols * d + 4 * M.rows * d
         variants = [("rows", 0)] + ([("tiled", 0), ("tiled_bin64", 0), ("tiled_bin128", 0)] if args.config == "reddit" else []) + \
+            ([("tiled_bin64w128", 0), ("tiled_bin64w255", 0), ("tiled_bin128w255", 0)]
+             if args.config == "reddit" and d <= 48 else []) + \
             ([("rows", 4), ("rows", 16)] if d <= 64 else []) + ([("rows", 1), ("rows", 4)] if d > 256 else [])
         if args.tiled_only:
             variants = [v for v in variants if v[0].startswith("tiled")]
@@ -106,14 +108,16 @@ def spmm(args):
                 key = (name, algo)
                 if key not in tiled:
                     t0 = time.time()
-                    rb = int(algo[len("tiled_bin"):]) if algo.startswith("tiled_bin") else None
-                    tiled[key] = ops.TiledCsr(M, factored=rb is not None, block_rows=rb)
+                    spec = algo[len("tiled_bin"):] if algo.startswith("tiled_bin") else None
+                    rb = int(spec.split("w")[0]) if spec else None
+                    win = int(spec.split("w")[1]) if spec and "w" in spec else 64
+                    tiled[key] = ops.TiledCsr(M, factored=rb is not None, block_rows=rb, window=win)
                     torch.cuda.synchronize()
                     print(json.dumps({"tiled": name, "algo": algo, "build_s": round(time.time() - t0, 2),
                                       "tiles": tiled[key].ntiles,
                                       "tiled_fraction": round(tiled[key].tiled_fraction, 4)}), flush=True)
                 T = tiled[key]
-                if T.binary and d <= 48 and T.RB == 64:
+                if T.binary and d <= 48 and T.RB == 64:           # (both window sizes)
                     for nv in (0, 1, 2, 3):         # narrow consumer layouts (hb_spmm_set_narrow)
                         ops.spmm_set_narrow(nv)
                         ms = _time(lambda: ops.spmm_tiled(T, X, Y, d), reps=5)
