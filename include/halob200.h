@@ -241,6 +241,16 @@ int hb_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, i
 int hb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
                  float b2, float eps, double bc1, double bc2, void* stream);
 
+/* hb_adam_step that skips the update on the device when *loss (device f64)
+ * is not finite or a flag word (flags, flags2: device words, nullable) is
+ * non-zero: the reference's check before Adam (trainer.py:361-366) without a
+ * host synchronisation, so an epoch's loss can be read back after the next
+ * epoch is issued (a failed epoch leaves the weights untouched, as the
+ * reference's abort does). */
+int hb_adam_step_guarded(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                         float b2, float eps, double bc1, double bc2, const double* loss,
+                         const uint32_t* flags, const uint32_t* flags2, void* stream);
+
 /* Argmax accuracy counts for evaluate() (trainer.py:129-144):
  * counts[2*k] = #rows with mask==k+1, counts[2*k+1] = #correct among them, k=0..2. */
 int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

@@ -19,7 +19,7 @@ cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaSt
 cudaError_t launch_relu_grad_mul(const float*, int64_t, const float*, int64_t, int, int, float*, int64_t,
                                  cudaStream_t);
 cudaError_t launch_adam(float*, const float*, float*, float*, int64_t, float, float, float, float, double,
-                        double, cudaStream_t);
+                        double, const double*, const uint32_t*, const uint32_t*, cudaStream_t);
 cudaError_t launch_argmax_accuracy(const float*, int64_t, int, int, const int32_t*, const uint8_t*,
                                    int64_t*, cudaStream_t);
 cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, uint64_t, float, float*,
@@ -245,7 +245,16 @@ int hb_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, i
 int hb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                  float eps, double bc1, double bc2, void* stream) {
   if (n < 0 || bc1 <= 0 || bc2 <= 0) return fail(HB_EINVAL, "hb_adam_step: bad arguments");
-  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, S(stream)), "hb_adam_step");
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, nullptr, nullptr, nullptr, S(stream)),
+               "hb_adam_step");
+}
+
+int hb_adam_step_guarded(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                         float eps, double bc1, double bc2, const double* loss, const uint32_t* flags,
+                         const uint32_t* flags2, void* stream) {
+  if (n < 0 || bc1 <= 0 || bc2 <= 0 || !loss) return fail(HB_EINVAL, "hb_adam_step_guarded: bad arguments");
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, loss, flags, flags2, S(stream)),
+               "hb_adam_step_guarded");
 }
 
 int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

@@ -354,10 +354,18 @@ def relu_grad_mul(j, h, m, n: int, d: int, stream=None):
               m.stride(0), stream_handle(stream))
 
 
-def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None):
-    """``linalg.adam_step`` (linalg.py:127-140) in place on device tensors."""
-    _lib.call("hb_adam_step", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
-              float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, stream_handle(stream))
+def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None, guard=None):
+    """``linalg.adam_step`` (linalg.py:127-140) in place on device tensors.
+    guard = (loss f64, flags u32, flags2 u32 or None) device tensors: the step is
+    skipped on the device when the loss is not finite or a flag is set."""
+    if guard is None:
+        _lib.call("hb_adam_step", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
+                  float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, stream_handle(stream))
+    else:
+        loss, flags, flags2 = guard
+        _lib.call("hb_adam_step_guarded", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
+                  float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, ptr(loss), ptr(flags), ptr(flags2),
+                  stream_handle(stream))
 
 
 def argmax_accuracy(logits, C: int, labels, mask, counts, stream=None):

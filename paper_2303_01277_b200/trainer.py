@@ -252,6 +252,7 @@ class DeviceRank:
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
         self.xent_partials = torch.zeros(ops.XENT_PARTIALS, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._deferred, self._snap, self._snap_next = [], [], 0       # run_epoch(defer=True) bookkeeping
         self.proto_flags = torch.zeros(1, dtype=torch.int32, device=dev)   # written on the comm stream only
         self.counts = torch.zeros(9, dtype=torch.int64, device=dev)
         self.multilabel = cfg.loss == "multilabel"
@@ -686,11 +687,13 @@ class DeviceRank:
                 reduce_gradients(self.gflat, self.loss_dev, self.group)
             cur.wait_stream(self.comm_stream)
 
-    def adam(self):
-        """adam_step per layer (trainer.py:365-366)."""
+    def adam(self, guarded: bool = False):
+        """adam_step per layer (trainer.py:365-366); guarded: skipped on the
+        device when the epoch's loss is not finite or a flag is set."""
         self.adam_t += 1
+        guard = (self.loss_dev, self.flags, self.proto_flags) if guarded else None
         for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
-            ops.adam_step(w, g, m, v, self.lr, self.adam_t)
+            ops.adam_step(w, g, m, v, self.lr, self.adam_t, guard=guard)
             self.launches += 1
 
     def swap_features(self, buf):
@@ -706,31 +709,60 @@ class DeviceRank:
         self.Ht[1] = buf
         return old
 
-    def run_epoch(self, epoch: int, check: bool = True) -> str:
+    def run_epoch(self, epoch: int, check: bool = True, defer: bool = False) -> str:
+        """One epoch.  check: the reference's host checks before Adam
+        (trainer.py:358-366; a host synchronisation).  defer: Adam is guarded
+        on the device instead (skipped when the loss is not finite or a codec /
+        protocol flag is set) and the epoch's loss and flags are copied to
+        pinned host memory; ``finish_epoch`` raises or records the loss later,
+        so the host can issue the next epoch first.  A failed epoch leaves the
+        weights untouched either way."""
         epoch_mode = staleness_adaptor(epoch, self.mode)
         logits = self.forward(epoch, epoch_mode)
         self.backward(epoch, epoch_mode, logits)
         self.reduce(epoch)
+        if defer:
+            torch = self.torch
+            self.adam(guarded=True)
+            if not self._snap:
+                self._snap = [tuple(torch.zeros(1, dtype=t.dtype).pin_memory()
+                                    for t in (self.loss_dev, self.flags, self.proto_flags)) for _ in range(3)]
+            slot = self._snap[self._snap_next % len(self._snap)]
+            self._snap_next += 1
+            for host, dev in zip(slot, (self.loss_dev, self.flags, self.proto_flags)):
+                host.copy_(dev.view(-1)[:1], non_blocking=True)
+            self._deferred.append((epoch, torch.cuda.current_stream().record_event(), slot))
+            if len(self._deferred) >= len(self._snap):      # at most len(_snap) epochs in flight
+                self.finish_epoch()
+            return epoch_mode
         if check:                 # on the all-reduced loss, before Adam (trainer.py:358-366)
             self.check_epoch(epoch)
         self.adam()
         return epoch_mode
+
+    def finish_epoch(self):
+        """Host checks of the oldest deferred epoch (``run_epoch(defer=True)``)."""
+        epoch, ev, (loss_h, flags_h, proto_h) = self._deferred.pop(0)
+        self._check(epoch, ev, lambda: float(loss_h[0]), lambda: int(flags_h[0]), lambda: int(proto_h[0]))
 
     def check_epoch(self, epoch: int):
         """Host checks of the reference (codec.py:167-168, trainer.py:361-363),
         after waiting at most ``timeout`` seconds for the epoch to finish on
         the device (the reference's recv timeout, transport.py:115-124: with
         NCCL a stalled or diverged peer leaves the comm stream waiting)."""
-        wait_device(self.torch.cuda.current_stream().record_event(), self.timeout,
+        self._check(epoch, self.torch.cuda.current_stream().record_event(), lambda: float(self.loss_dev.item()),
+                    lambda: int(self.flags.item()), lambda: int(self.proto_flags.item()))
+
+    def _check(self, epoch, event, loss_fn, flags_fn, proto_fn):
+        wait_device(event, self.timeout,
                     f"epoch {epoch} did not complete within {self.timeout:g} s (a peer rank stalled "
                     "or the ranks diverged)")
-        if int(self.proto_flags.item()):
+        if proto_fn():
             raise ProtocolError(f"tag mismatch in an exchange of epoch {epoch}: the ranks diverged")
-        flags = int(self.flags.item())
-        if flags & 1:
+        if flags_fn() & 1:
             raise TrainingError(f"worker {self.layout.ids[0]} aborted: "
                                 f"{CodecError('non-finite values in quantizer input')}")
-        loss = float(self.loss_dev.item())
+        loss = loss_fn()
         if not math.isfinite(loss):
             raise TrainingError(f"worker {self.layout.ids[0]} aborted: NaN/inf loss at epoch {epoch}: "
                                 "learning rate too high or codec error")

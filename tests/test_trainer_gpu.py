@@ -343,3 +343,50 @@ def test_multilabel_training_serial_equivalence():
     acc = evaluate(a.final_weights, g, cfg)
     assert acc["test_acc"] == pytest.approx(a.metrics[-1].test_acc, abs=2e-3)
     assert 0.0 < acc["test_acc"] <= 1.0
+
+
+def _engine(seed=3, widths=(32, 16, 4), model="sage", bits=1, mode=("sync", 0)):
+    from paper_2303_01277_b200.codec import QuantConfig
+    from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
+    from paper_2303_01277_b200.transport import RankLayout
+    g = _graph(seed=seed, npc=40)
+    parts = _parts(g, 4, model)
+    lay = RankLayout({p.id: p for p in parts}, [0] * 4, 0)
+    return DeviceRank(lay, ModelConfig(widths, model), TrainMode(*mode), QuantConfig(bits), 5, 0.01,
+                      int(g.train_mask.sum()))
+
+
+@pytest.mark.parametrize("mode", [("sync", 0), ("async", 2)])
+def test_deferred_check_is_the_same_epoch(mode):
+    """run_epoch(defer=True) (device-guarded Adam, host check one epoch later)
+    trains bit-identically to the synchronous host check before Adam."""
+    a, b = _engine(mode=mode), _engine(mode=mode)
+    la, lb = [], []
+    for e in range(1, 6):
+        a.run_epoch(e)
+        la.append(a.epoch_loss)
+        b.run_epoch(e, defer=True)
+        if e > 1:
+            b.finish_epoch()
+            lb.append(b.epoch_loss)
+    b.finish_epoch()
+    lb.append(b.epoch_loss)
+    assert la == lb
+    for wa, wb in zip(a.weights_host(), b.weights_host()):
+        assert np.array_equal(wa, wb)
+
+
+def test_deferred_check_failed_epoch_leaves_weights():
+    """A non-finite quantizer input under the deferred check: the guarded Adam
+    skips the update on the device and finish_epoch raises the reference's
+    abort (codec.py:167-168, trainer.py:361-363)."""
+    from paper_2303_01277_b200.trainer import TrainingError
+    eng = _engine()
+    eng.run_epoch(1)
+    before = [w.copy() for w in eng.weights_host()]
+    eng.Ht[1][0, 0] = float("nan")
+    eng.run_epoch(2, defer=True)
+    with pytest.raises(TrainingError, match="aborted"):
+        eng.finish_epoch()
+    for w0, w1 in zip(before, eng.weights_host()):
+        assert np.array_equal(w0, w1)
