@@ -78,10 +78,19 @@ def factor_scales(a: DeviceCsr):
     r[di] = vd[dmask].sqrt()
     c[di] = r[di]
     del m
-    sel = torch.isnan(r[rows]) & ~torch.isnan(c[col])
-    r.scatter_(0, rows[sel], vd[sel] / c[col[sel]])
-    sel = torch.isnan(c[col]) & ~torch.isnan(r[rows])
-    c.scatter_(0, col[sel], vd[sel] / r[rows[sel]])
+    # a missing factor comes from the row's (column's) first qualifying
+    # nonzero in CSR order: scatter_ with repeated indices would keep an
+    # arbitrary one, and the candidates differ in their last bits, which made
+    # two identical runs differ (min-index scatter_reduce is order-independent)
+    nnz_idx = torch.arange(v.numel(), device=dev)
+    for fill, known, fk, ok in ((r, c, rows, col), (c, r, col, rows)):
+        sel = torch.isnan(fill[fk]) & ~torch.isnan(known[ok])
+        if bool(sel.any()):
+            first_nz = torch.full((fill.numel(),), v.numel(), dtype=torch.int64, device=dev)
+            first_nz.scatter_reduce_(0, fk[sel], nnz_idx[sel], reduce="amin")
+            tgt = (first_nz < v.numel()).nonzero().view(-1)
+            e = first_nz[tgt]
+            fill[tgt] = vd[e] / known[ok[e]]
     rr, cc = r[rows], c[col]
     if bool(torch.isnan(rr).any() | torch.isnan(cc).any()):
         return None

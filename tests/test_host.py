@@ -182,3 +182,27 @@ def test_tiled_layout_reconstructs_matrix(kind):
     assert T.binary == (kind != "general")
     assert T.RB == (128 if kind == "gcn" else 64) and 0 < T.tiled_fraction < 1
     np.testing.assert_allclose(_tile_dense(T), m.toarray(), rtol=3e-7, atol=0)
+
+
+def test_factor_scales_deterministic_first_nonzero():
+    """GCN partition blocks: a halo column's factor is derived from its first
+    nonzero in CSR order (not an arbitrary one: the candidates differ in their
+    last bits, and picking any of them made identical runs differ)."""
+    torch = pytest.importorskip("torch")
+    from paper_2303_01277_b200 import ops
+    from paper_2303_01277_b200.datasets import SbmSpec, generate_sbm
+    from paper_2303_01277_b200.graph import build_partitions
+    g = generate_sbm(SbmSpec(nodes_per_community=20, communities=4, feature_dim=8, seed=13))
+    for p in build_partitions(g, 3, "contiguous", 0, "gcn")[2]:
+        a = p.adj_block
+        d = ops.DeviceCsr.from_csr(a, torch.device("cpu"))
+        r, c = ops.factor_scales(d)
+        rp, ci = np.asarray(a.row_ptr), np.asarray(a.col_idx)
+        v = np.asarray(a.values, dtype=np.float32).astype(np.float64)     # device values are fp32
+        rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+        diag = np.zeros(len(rp) - 1)
+        diag[rows[ci == rows]] = np.sqrt(v[ci == rows])
+        for j in range(len(rp) - 1, a.cols):          # halo columns: no diagonal entry
+            e = np.flatnonzero(ci == j)
+            if len(e):
+                assert float(c[j]) == np.float32(v[e[0]] / diag[rows[e[0]]])
