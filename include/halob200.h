@@ -251,6 +251,23 @@ int hb_adam_step_guarded(float* w, const float* g, float* m, float* v, int64_t n
                          float b2, float eps, double bc1, double bc2, const double* loss,
                          const uint32_t* flags, const uint32_t* flags2, void* stream);
 
+/* Stream-ordered copy of `bytes` from PINNED host memory to the device: the
+ * per-epoch words (K1 descriptor tables with the epoch's Philox keys, Adam's
+ * bias corrections).  Up to 1 MiB from a mapped pinned buffer it is a one-CTA
+ * kernel reading the buffer through its device mapping (no copy engine, so it
+ * never queues behind a large feature upload on another stream); otherwise a
+ * cudaMemcpyAsync.  Inside a CUDA-graph capture it becomes a node that reads
+ * the host buffer when the graph replays. */
+int hb_upload_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* hb_adam_step_guarded with the bias corrections read from device memory
+ * (bc[0] = 1-b1^t, bc[1] = 1-b2^t, f64): the launch's arguments no longer
+ * change from epoch to epoch, so a captured CUDA graph of the epoch replays it
+ * (the host uploads bc with the epoch's other per-epoch words). */
+int hb_adam_step_dev(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                     float b2, float eps, const double* bc, const double* loss, const uint32_t* flags,
+                     const uint32_t* flags2, void* stream);
+
 /* Argmax accuracy counts for evaluate() (trainer.py:129-144):
  * counts[2*k] = #rows with mask==k+1, counts[2*k+1] = #correct among them, k=0..2. */
 int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

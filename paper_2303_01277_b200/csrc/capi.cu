@@ -19,7 +19,7 @@ cudaError_t launch_relu(const float*, int64_t, int, int, float*, int64_t, cudaSt
 cudaError_t launch_relu_grad_mul(const float*, int64_t, const float*, int64_t, int, int, float*, int64_t,
                                  cudaStream_t);
 cudaError_t launch_adam(float*, const float*, float*, float*, int64_t, float, float, float, float, double,
-                        double, const double*, const uint32_t*, const uint32_t*, cudaStream_t);
+                        double, const double*, const uint32_t*, const uint32_t*, const double*, cudaStream_t);
 cudaError_t launch_argmax_accuracy(const float*, int64_t, int, int, const int32_t*, const uint8_t*,
                                    int64_t*, cudaStream_t);
 cudaError_t launch_dropout(const float*, int64_t, int, int64_t, int, uint64_t, uint64_t, float, float*,
@@ -245,7 +245,7 @@ int hb_relu_grad_mul(const float* j, int64_t ldj, const float* h, int64_t ldh, i
 int hb_adam_step(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                  float eps, double bc1, double bc2, void* stream) {
   if (n < 0 || bc1 <= 0 || bc2 <= 0) return fail(HB_EINVAL, "hb_adam_step: bad arguments");
-  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, nullptr, nullptr, nullptr, S(stream)),
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, nullptr, nullptr, nullptr, nullptr, S(stream)),
                "hb_adam_step");
 }
 
@@ -253,8 +253,42 @@ int hb_adam_step_guarded(float* w, const float* g, float* m, float* v, int64_t n
                          float eps, double bc1, double bc2, const double* loss, const uint32_t* flags,
                          const uint32_t* flags2, void* stream) {
   if (n < 0 || bc1 <= 0 || bc2 <= 0 || !loss) return fail(HB_EINVAL, "hb_adam_step_guarded: bad arguments");
-  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, loss, flags, flags2, S(stream)),
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, loss, flags, flags2, nullptr, S(stream)),
                "hb_adam_step_guarded");
+}
+
+// Per-epoch words are small (K1 tables: 40 B per message): the copy is a
+// one-CTA kernel reading the pinned buffer through its device mapping, not a
+// copy-engine transfer — a copy engine busy with the next step's 562 MB feature
+// upload would otherwise hold the compute stream up to the end of that upload.
+__global__ void fetch_host_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t bytes) {
+  const bool w4 = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 3) == 0;
+  const int64_t nw = w4 ? bytes >> 2 : 0;
+  for (int64_t i = threadIdx.x; i < nw; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const volatile uint32_t*>(src)[i];
+  for (int64_t i = nw * 4 + threadIdx.x; i < bytes; i += blockDim.x)
+    dst[i] = reinterpret_cast<const volatile uint8_t*>(src)[i];
+}
+
+int hb_upload_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(HB_EINVAL, "hb_upload_async: bad arguments");
+  if (bytes == 0) return HB_OK;
+  void* dsrc = nullptr;
+  if (bytes <= (1 << 20) && cudaHostGetDevicePointer(&dsrc, const_cast<void*>(src), 0) == cudaSuccess && dsrc) {
+    fetch_host_kernel<<<1, 256, 0, S(stream)>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(dsrc),
+                                                bytes);
+    return check(cudaGetLastError(), "hb_upload_async");
+  }
+  cudaGetLastError();            // not a mapped pinned buffer (or large): a copy-engine transfer
+  return check(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, S(stream)), "hb_upload_async");
+}
+
+int hb_adam_step_dev(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                     float eps, const double* bc, const double* loss, const uint32_t* flags, const uint32_t* flags2,
+                     void* stream) {
+  if (n < 0 || !bc || !loss) return fail(HB_EINVAL, "hb_adam_step_dev: bad arguments");
+  return check(hb::launch_adam(w, g, m, v, n, lr, b1, b2, eps, 1.0, 1.0, loss, flags, flags2, bc, S(stream)),
+               "hb_adam_step_dev");
 }
 
 int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

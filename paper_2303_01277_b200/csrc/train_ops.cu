@@ -171,8 +171,13 @@ static int rows_grid(int n) {
 __global__ void adam_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps,
                             double bc1, double bc2, const double* __restrict__ loss,
-                            const uint32_t* __restrict__ flags, const uint32_t* __restrict__ flags2) {
+                            const uint32_t* __restrict__ flags, const uint32_t* __restrict__ flags2,
+                            const double* __restrict__ bc) {
   if (loss != nullptr && !isfinite(*loss)) return;
+  if (bc != nullptr) {          // bias corrections from device memory (CUDA-graph replays)
+    bc1 = bc[0];
+    bc2 = bc[1];
+  }
   if (flags != nullptr && *flags != 0u) return;
   if (flags2 != nullptr && *flags2 != 0u) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -347,9 +352,9 @@ cudaError_t launch_relu_grad_mul(const float* j, int64_t ldj, const float* h, in
 
 cudaError_t launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1,
                         float b2, float eps, double bc1, double bc2, const double* loss, const uint32_t* flags,
-                        const uint32_t* flags2, cudaStream_t st) {
+                        const uint32_t* flags2, const double* bc, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  adam_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, loss, flags, flags2);
+  adam_kernel<<<grid_for(n, 256), 256, 0, st>>>(w, g, m, v, n, lr, b1, b2, eps, bc1, bc2, loss, flags, flags2, bc);
   return cudaGetLastError();
 }
 

@@ -363,11 +363,17 @@ def relu_grad_mul(j, h, m, n: int, d: int, stream=None):
               m.stride(0), stream_handle(stream))
 
 
-def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None, guard=None):
+def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None, guard=None, bc=None):
     """``linalg.adam_step`` (linalg.py:127-140) in place on device tensors.
     guard = (loss f64, flags u32, flags2 u32 or None) device tensors: the step is
-    skipped on the device when the loss is not finite or a flag is set."""
-    if guard is None:
+    skipped on the device when the loss is not finite or a flag is set.
+    bc: device f64[2] holding (1-b1^t, 1-b2^t) (needs guard; t is then unused):
+    the launch's arguments do not change with the epoch (CUDA-graph replays)."""
+    if bc is not None:
+        loss, flags, flags2 = guard
+        _lib.call("hb_adam_step_dev", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
+                  float(b2), float(eps), ptr(bc), ptr(loss), ptr(flags), ptr(flags2), stream_handle(stream))
+    elif guard is None:
         _lib.call("hb_adam_step", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
                   float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, stream_handle(stream))
     else:
@@ -375,6 +381,15 @@ def adam_step(w, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, stream=None, guard=
         _lib.call("hb_adam_step_guarded", ptr(w), ptr(g), ptr(m), ptr(v), w.numel(), float(lr), float(b1),
                   float(b2), float(eps), 1.0 - b1 ** t, 1.0 - b2 ** t, ptr(loss), ptr(flags), ptr(flags2),
                   stream_handle(stream))
+
+
+def upload(dst, host, stream=None):
+    """Stream-ordered copy of the pinned host tensor `host` into `dst` (same
+    byte size) through hb_upload_async: capturable as a graph memcpy node."""
+    n = host.numel() * host.element_size()
+    if dst.numel() * dst.element_size() < n:
+        raise ValueError("upload: destination smaller than the host buffer")
+    _lib.call("hb_upload_async", ptr(dst), host.data_ptr(), n, stream_handle(stream))
 
 
 def argmax_accuracy(logits, C: int, labels, mask, counts, stream=None):

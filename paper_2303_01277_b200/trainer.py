@@ -34,7 +34,7 @@ from .graph import Graph, Partition
 from .linalg import ShapeError
 from .profiling import null_timer
 from .rngstream import BACKWARD, FORWARD, derive_key, keyed_generator
-from .transport import ExchangeBuffers, ProtocolError, RankLayout, TransportStats, nccl_exchange
+from .transport import SEG_BYTES, ExchangeBuffers, ProtocolError, RankLayout, TransportStats, nccl_exchange
 
 MODELS = ("gcn", "sage")
 
@@ -180,6 +180,40 @@ def _transpose_device(a: "ops.DeviceCsr") -> "ops.DeviceCsr":
     return t
 
 
+class EpochGraph:
+    """One training epoch captured as a CUDA graph (``DeviceRank.run_epoch_graphed``).
+
+    The epoch's launches are identical from epoch to epoch except for a few
+    per-epoch words: each exchange's K1 descriptor table (the Philox keys
+    derive from the epoch, rngstream.py:19-23) and Adam's bias corrections
+    (linalg.py:127-140).  Those reach the device through memcpy nodes that
+    read pinned host buffers owned by the graph; ``replay`` re-fills them for
+    the replayed epoch, then launches the graph.  The host bookkeeping of an
+    epoch (slot tags with their staleness checks, byte meters, Adam's step
+    count) is recorded at capture and re-applied per replay."""
+
+    def __init__(self, torch):
+        self.graph = torch.cuda.CUDAGraph()
+        self.fills = []            # callables(epoch) re-filling the pinned buffers
+        self._host = {}            # id(owner) -> pinned host tensor
+        self.consumed = []         # (layer, phase) slots consumed (tag checks)
+        self.set_slots = []        # (layer, phase) slots this epoch fills
+        self.stats = {}            # partition -> byte-meter deltas
+        self.launches = 0
+        self.done = None           # event after the last replay (its pinned buffers are free)
+
+    def pinned(self, owner, nbytes: int):
+        return self._host[id(owner)][:nbytes]
+
+    def alloc(self, torch, owner, nbytes: int, dtype=None):
+        t = torch.zeros(max(1, nbytes), dtype=dtype or torch.uint8).pin_memory()
+        self._host[id(owner)] = t
+        return t
+
+    def add_fill(self, fn):
+        self.fills.append(fn)
+
+
 class DeviceRank:
     """One rank's share of the training: buffers, exchanges, epoch loop."""
 
@@ -253,6 +287,8 @@ class DeviceRank:
         self.xent_partials = torch.zeros(ops.XENT_PARTIALS, dtype=torch.float64, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self._deferred, self._snap, self._snap_next = [], [], 0       # run_epoch(defer=True) bookkeeping
+        self._graphs, self._cap = {}, None                           # run_epoch_graphed
+        self.adam_bc = torch.zeros(2, dtype=torch.float64, device=dev)  # (1-b1^t, 1-b2^t) for graph replays
         self.proto_flags = torch.zeros(1, dtype=torch.int32, device=dev)   # written on the comm stream only
         self.counts = torch.zeros(9, dtype=torch.int64, device=dev)
         self.multilabel = cfg.loss == "multilabel"
@@ -396,6 +432,8 @@ class DeviceRank:
 
     def _consume(self, epoch: int, layer: int, phase: str) -> int:
         """trainer.py:232-246 — tags are tracked on the host."""
+        if self._cap is not None:
+            self._cap.consumed.append((layer, phase))
         tag = self.slots.get((layer, phase))
         if tag is None:
             if epoch > 1:
@@ -692,8 +730,21 @@ class DeviceRank:
         device when the epoch's loss is not finite or a flag is set."""
         self.adam_t += 1
         guard = (self.loss_dev, self.flags, self.proto_flags) if guarded else None
+        bc = None
+        if self._cap is not None:
+            # graph capture: the bias corrections come from device memory,
+            # uploaded from a pinned pair the replays re-fill
+            cap = self._cap
+            host = cap.pinned(self.adam_bc, 16).view(self.torch.float64)
+
+            def fill(_epoch, h=host):
+                h[0], h[1] = 1.0 - 0.9 ** self.adam_t, 1.0 - 0.999 ** self.adam_t
+            fill(0)
+            ops.upload(self.adam_bc, host)
+            cap.add_fill(fill)
+            bc = self.adam_bc
         for w, g, m, v in zip(self.Wp, self.Gp, self.adam_m, self.adam_v):
-            ops.adam_step(w, g, m, v, self.lr, self.adam_t, guard=guard)
+            ops.adam_step(w, g, m, v, self.lr, self.adam_t, guard=guard, bc=bc)
             self.launches += 1
 
     def swap_features(self, buf):
@@ -722,23 +773,113 @@ class DeviceRank:
         self.backward(epoch, epoch_mode, logits)
         self.reduce(epoch)
         if defer:
-            torch = self.torch
             self.adam(guarded=True)
-            if not self._snap:
-                self._snap = [tuple(torch.zeros(1, dtype=t.dtype).pin_memory()
-                                    for t in (self.loss_dev, self.flags, self.proto_flags)) for _ in range(3)]
-            slot = self._snap[self._snap_next % len(self._snap)]
-            self._snap_next += 1
-            for host, dev in zip(slot, (self.loss_dev, self.flags, self.proto_flags)):
-                host.copy_(dev.view(-1)[:1], non_blocking=True)
-            self._deferred.append((epoch, torch.cuda.current_stream().record_event(), slot))
-            if len(self._deferred) >= len(self._snap):      # at most len(_snap) epochs in flight
-                self.finish_epoch()
+            self._defer_tail(epoch)
             return epoch_mode
         if check:                 # on the all-reduced loss, before Adam (trainer.py:358-366)
             self.check_epoch(epoch)
         self.adam()
         return epoch_mode
+
+    def _defer_tail(self, epoch: int):
+        """Copy the epoch's loss and flags to a pinned slot (read by finish_epoch)."""
+        torch = self.torch
+        if not self._snap:
+            self._snap = [tuple(torch.zeros(1, dtype=t.dtype).pin_memory()
+                                for t in (self.loss_dev, self.flags, self.proto_flags)) for _ in range(3)]
+        slot = self._snap[self._snap_next % len(self._snap)]
+        self._snap_next += 1
+        for host, dev in zip(slot, (self.loss_dev, self.flags, self.proto_flags)):
+            host.copy_(dev.view(-1)[:1], non_blocking=True)
+        self._deferred.append((epoch, torch.cuda.current_stream().record_event(), slot))
+        if len(self._deferred) >= len(self._snap):      # at most len(_snap) epochs in flight
+            self.finish_epoch()
+
+    def graphable(self) -> bool:
+        """CUDA-graph epochs: one rank (NCCL exchanges stay eager), no dropout
+        (its per-epoch keys are launch arguments), no probe (host callbacks
+        inside the epoch), the tcgen05 GEMMs."""
+        return self.world == 1 and not self.drop and self.probe is None and self.gemm_impl != "cublas"
+
+    def run_epoch_graphed(self, epoch: int) -> str:
+        """``run_epoch(epoch, defer=True)`` replayed from a CUDA graph of the
+        epoch: one graph launch instead of ~40 kernel launches + descriptor
+        uploads from Python, so the host issue time no longer tracks the device
+        time.  Graphs are keyed by (epoch mode, epoch parity, layer-1 input
+        buffer); the first two epochs (the Sylvie-A pipeline's start-up, and
+        first-use allocations) run eagerly, and a graph is captured the first
+        time its key comes up.  Falls back to eager epochs when not
+        ``graphable()``."""
+        if not self.graphable() or epoch <= 2:
+            return self.run_epoch(epoch, defer=True)
+        torch = self.torch
+        epoch_mode = staleness_adaptor(epoch, self.mode)
+        key = (epoch_mode, epoch % 2, self.Ht[1].data_ptr())
+        ent = self._graphs.get(key)
+        if ent is None:
+            self._graphs[key] = self._capture_epoch(epoch, epoch_mode)
+        else:
+            if ent.done is not None:
+                ent.done.synchronize()          # its pinned buffers are free again
+            for layer, phase in ent.consumed:
+                self._consume(epoch, layer, phase)
+            self.adam_t += 1
+            for fill in ent.fills:
+                fill(epoch)
+            ent.graph.replay()
+            ent.done = torch.cuda.current_stream().record_event()
+            for k in ent.set_slots:
+                self.slots[k] = epoch
+            for p, delta in ent.stats.items():
+                st = self.stats[p]
+                for k, v in delta.items():
+                    setattr(st, k, getattr(st, k) + v)
+            self.launches += ent.launches
+        self._defer_tail(epoch)
+        return epoch_mode
+
+    def _capture_epoch(self, epoch: int, epoch_mode: str) -> EpochGraph:
+        """Capture (and run) one epoch as a CUDA graph."""
+        torch = self.torch
+        ent = EpochGraph(torch)
+        bufs = list(self.xf.values()) + list(self.xb.values())
+        for b in bufs:
+            ent.alloc(torch, b, b.n_send * SEG_BYTES)
+        ent.alloc(torch, self.adam_bc, 16)
+        stats0 = {p: s.snapshot() for p, s in self.stats.items()}
+        slots0 = dict(self.slots)
+        launches0 = self.launches
+        timer, self.timer = self.timer, null_timer
+        if getattr(self, "_cap_stream", None) is None:
+            self._cap_stream = torch.cuda.Stream(device=self.dev)
+        for b in bufs:
+            b.capture = ent
+        self._cap = ent
+        # no finalizers mid-capture: a collected pinned buffer or event of an
+        # earlier engine would make an API call that invalidates the capture
+        import gc
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(ent.graph, stream=self._cap_stream, capture_error_mode="thread_local"):
+                logits = self.forward(epoch, epoch_mode)
+                self.backward(epoch, epoch_mode, logits)
+                self.reduce(epoch)
+                self.adam(guarded=True)
+        finally:
+            if gc_was:
+                gc.enable()
+            for b in bufs:
+                b.capture = None
+            self._cap = None
+            self.timer = timer
+        ent.launches = self.launches - launches0
+        ent.stats = {p: {k: v - stats0[p][k] for k, v in s.snapshot().items()} for p, s in self.stats.items()}
+        ent.set_slots = [k for k, v in self.slots.items() if v == epoch and slots0.get(k) != epoch]
+        ent.graph.replay()                      # a capture records the work; this runs it
+        ent.done = torch.cuda.current_stream().record_event()
+        return ent
 
     def finish_epoch(self):
         """Host checks of the oldest deferred epoch (``run_epoch(defer=True)``)."""

@@ -267,6 +267,7 @@ class ExchangeBuffers:
         self._seg_host = None
         self._seg_ev = [None, None]
         self._seg_slot = 0
+        self.capture = None                    # an EpochGraph while one is being captured
 
     def send_table(self, seed: int, epoch: int, layer: int, parity: int) -> np.ndarray:
         """hb_segment_t rows for this exchange (keys depend on the epoch)."""
@@ -292,13 +293,28 @@ class ExchangeBuffers:
         if self._dev.type != "cuda":
             self._seg_dev.copy_(torch.from_numpy(tab.copy()))
             return self._seg_dev
+        cap = self.capture
+        if cap is not None:
+            # inside a CUDA-graph capture: the copy becomes a memcpy node reading
+            # a pinned buffer the graph owns (allocated before the capture);
+            # each replay re-fills it with the replayed epoch's table first
+            host = cap.pinned(self, tab.size)
+            host.numpy()[:] = tab
+            _lib.call("hb_upload_async", self._seg_dev.data_ptr(), host.data_ptr(), tab.size,
+                      _lib.stream_handle())
+            cap.add_fill(lambda e, b=host: b.numpy().__setitem__(
+                slice(None), self.send_table(seed, e, layer, parity).view(np.uint8)))
+            return self._seg_dev
         if self._seg_host is None:
             self._seg_host = [torch.empty(tab.size, dtype=torch.uint8).pin_memory() for _ in range(2)]
         k = self._seg_slot = self._seg_slot ^ 1
         if self._seg_ev[k] is not None:
             self._seg_ev[k].synchronize()          # the copy from this slot two uploads ago
         self._seg_host[k].numpy()[:] = tab
-        self._seg_dev.copy_(self._seg_host[k], non_blocking=True)
+        # a kernel reading the mapped pinned slot (hb_upload_async), not a
+        # copy-engine transfer that would queue behind a feature upload
+        _lib.call("hb_upload_async", self._seg_dev.data_ptr(), self._seg_host[k].data_ptr(), tab.size,
+                  _lib.stream_handle())
         self._seg_ev[k] = torch.cuda.current_stream(self._dev).record_event()
         return self._seg_dev
 
