@@ -44,6 +44,10 @@ __device__ __forceinline__ int find_segment(const hb_segment_t* segs, int nseg, 
 // Number of SMs of the current device (cached per process).
 int num_sms();
 
+// Xs[j, :d] = c[j] * X[j, :d], 16-byte aligned rows (spmm_bin.cu)
+cudaError_t launch_scale_rows(const float* X, int64_t ldx, int xrows, int d, const float* c, float* xs,
+                              int64_t ldxs, cudaStream_t stream);
+
 }  // namespace hb
 
 // ---- mbarrier + TMA bulk copy (sm_90+/sm_100a) ------------------------------

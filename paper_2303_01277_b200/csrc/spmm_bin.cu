@@ -467,6 +467,17 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
 
 }  // namespace sb
 
+// Xs[j, :d] = c[j] * X[j, :d] (the column scaling of the factored operators)
+cudaError_t launch_scale_rows(const float* X, int64_t ldx, int xrows, int d, const float* c, float* xs,
+                              int64_t ldxs, cudaStream_t stream) {
+  const int d4 = (d + 3) / 4;
+  const int64_t total = (int64_t)xrows * d4;
+  int grid = (int)((total + 255) / 256);
+  if (grid > num_sms() * 16) grid = num_sms() * 16;
+  if (grid > 0) sb::scale_rows_kernel<<<grid, 256, 0, stream>>>(X, ldx, xrows, d4, c, xs, ldxs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32_t* tile_ptr,
                                   const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
                                   const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
@@ -477,12 +488,7 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
   if (col_scale) {
     if (!xs || (ldxs & 3) || (((uintptr_t)xs) & 15) || ldxs < d) return cudaErrorInvalidValue;
-    const int d4 = (d + 3) / 4;
-    const int64_t total = (int64_t)xrows * d4;
-    int grid = (int)((total + 255) / 256);
-    if (grid > num_sms() * 16) grid = num_sms() * 16;
-    if (grid > 0) sb::scale_rows_kernel<<<grid, 256, 0, stream>>>(X, ldx, xrows, d4, col_scale, xs, ldxs);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_scale_rows(X, ldx, xrows, d, col_scale, xs, ldxs, stream);
     if (e != cudaSuccess) return e;
     X = xs;
     ldx = ldxs;
