@@ -154,21 +154,6 @@ int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32
                       float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, int32_t block_rows,
                       int32_t window_cols, void* stream);
 
-/* K3/K4, factored tiles in column-major form (ops.TiledCsr(fmt="cm")): a
- * 128-row block's tiles hold, per warp of 8 rows, the u16 entries
- * (column in the 64-column window | 8-bit row mask << 8) of every column any
- * of its rows touches, ascending, each warp's run padded with zero entries to
- * a multiple of 8; tile_woff[t][0..16] the warps' entry offsets (24 u16 per
- * tile), tile_off[t] the byte offset of tile t's entries (16-byte multiples).
- * An X row staged in shared memory is read once per entry and added to every
- * masked row.  Otherwise as hb_spmm_tiled_bin with block_rows = 128,
- * window_cols = 64 (same summation order). */
-int hb_spmm_tiled_cm(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr,
-                     const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_woff,
-                     const uint16_t* tile_ent, const int64_t* res_ptr, const int32_t* res_col,
-                     const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
-                     float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, void* stream);
-
 /* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
  * tensor cores with the 3xTF32 split (fp32 accuracy):
  *   C[m, n] = sum_k A(m, k) B(k, n) (+ beta * C[m, n])

@@ -26,7 +26,7 @@ assert SEGMENT_DTYPE.itemsize == 40
 
 EXPORTS = (
     "hb_version", "hb_last_error", "hb_philox_uniforms", "hb_quantize_gather",
-    "hb_dequant_gather", "hb_spmm_csr", "hb_spmm_csr_ex", "hb_spmm_tiled", "hb_spmm_tiled_bin", "hb_spmm_tiled_cm", "hb_gemm_f32", "hb_gemm2_f32", "hb_gemm_set_path", "hb_spmm_set_narrow", "hb_softmax_xent", "hb_relu", "hb_relu_grad_mul",
+    "hb_dequant_gather", "hb_spmm_csr", "hb_spmm_csr_ex", "hb_spmm_tiled", "hb_spmm_tiled_bin", "hb_gemm_f32", "hb_gemm2_f32", "hb_gemm_set_path", "hb_spmm_set_narrow", "hb_softmax_xent", "hb_relu", "hb_relu_grad_mul",
     "hb_adam_step", "hb_adam_step_guarded", "hb_adam_step_dev", "hb_upload_async", "hb_argmax_accuracy", "hb_dropout", "hb_sigmoid_bce", "hb_multilabel_counts",
 )
 
@@ -45,8 +45,6 @@ _SIGS = {
     "hb_spmm_tiled": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64, P, P],
     "hb_spmm_tiled_bin": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64,
                           P, c_int64, P, c_int32, c_int32, P],
-    "hb_spmm_tiled_cm": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64,
-                         P, c_int64, P, P],
     "hb_spmm_csr_ex": [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, c_int64, c_int32, c_int32, c_int32, P, P],
     "hb_softmax_xent": [P, c_int64, c_int32, c_int32, P, P, c_double, P, c_int64, P, P, c_int32, P, P],
     "hb_relu": [P, c_int64, c_int32, c_int32, P, c_int64, P],

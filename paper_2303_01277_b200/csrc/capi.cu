@@ -41,9 +41,6 @@ extern int g_gemm_ts;
 cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                               const int2*, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
                               float*, int64_t, int*, cudaStream_t);
-cudaError_t launch_spmm_tiled_cm(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
-                                 const uint16_t*, const int64_t*, const int32_t*, const float*, const float*,
-                                 const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, cudaStream_t);
 cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                                   const uint8_t*, const int64_t*, const int32_t*, const float*, const float*,
                                   const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, int, int,
@@ -163,22 +160,6 @@ int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32
   if (e == cudaErrorNotSupported)
     return fail(HB_EINVAL, "hb_spmm_tiled_bin: X/Y need 16-byte aligned rows (ld % 4 == 0)");
   return check(e, "hb_spmm_tiled_bin");
-}
-
-int hb_spmm_tiled_cm(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr,
-                     const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_woff,
-                     const uint16_t* tile_ent, const int64_t* res_ptr, const int32_t* res_col,
-                     const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
-                     float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, void* stream) {
-  if (nrows < 0 || d < 0 || ldx < d || ldy < d || nblocks != (nrows + 127) / 128 ||
-      (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y || !work)) || (col_scale && (!xs || ldxs < d)))
-    return fail(HB_EINVAL, "hb_spmm_tiled_cm: bad arguments");
-  const cudaError_t e = hb::launch_spmm_tiled_cm(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_woff,
-                                                 tile_ent, res_ptr, res_col, row_scale, col_scale, X, ldx, d, Y,
-                                                 ldy, xs, ldxs, work, S(stream));
-  if (e == cudaErrorNotSupported)
-    return fail(HB_EINVAL, "hb_spmm_tiled_cm: X/Y need 16-byte aligned rows (ld % 4 == 0)");
-  return check(e, "hb_spmm_tiled_cm");
 }
 
 int hb_gemm_f32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda_m, int64_t lda_k, const float* B,

@@ -117,20 +117,13 @@ class TiledCsr:
       at most 48 columns) doubles the nonzeros per (row, tile)."""
 
     def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None,
-                 block_rows: int | None = None, window: int = 64, fmt: str = "rows"):
+                 block_rows: int | None = None, window: int = 64):
         import torch
         dev = a.row_ptr.device
-        if fmt not in ("rows", "cm"):
-            raise ValueError(f"unknown tile format {fmt!r}")
         scales = factor_scales(a) if factored in (None, True) else None
-        if (factored is True or fmt == "cm") and scales is None:
+        if factored is True and scales is None:
             raise ValueError("matrix values do not factor into diagonal scalings of a 0/1 pattern")
         self.binary = scales is not None
-        # "cm": column-major factored tiles (hb_spmm_tiled_cm), 128-row blocks,
-        # 64-column windows, one (column, 8-row mask) entry per warp and column
-        self.fmt = fmt
-        if fmt == "cm":
-            block_rows, window = 128, 64
         self.row_scale, self.col_scale = scales if self.binary else (None, None)
         if self.binary:
             import os
@@ -169,8 +162,6 @@ class TiledCsr:
         # bytes per row); denser (block, window) groups become several tiles
         # of the same window
         cap = self.MAXREC - 3 * RB if self.binary else self.MAXREC
-        if fmt == "cm":
-            cap = RB * W              # at most 16 x 64 entries: a window never splits
         nsplit = (grp_cnt + cap - 1) // cap
         sub_of_grp = torch.repeat_interleave(torch.arange(grp_key.numel(), device=dev), nsplit)
         first_sub = torch.zeros(grp_key.numel() + 1, dtype=torch.int64, device=dev)
@@ -195,31 +186,7 @@ class TiledCsr:
         lr = rows[didx] % RB
         per = torch.bincount(tile_of * RB + lr, minlength=self.ntiles * RB).view(self.ntiles, RB)
         ro = torch.zeros((self.ntiles, self.ROWOFF), dtype=torch.int64, device=dev)
-        if fmt == "cm":
-            # entries (column | 8-row mask << 8) per (tile, warp, column), sorted;
-            # the masks are integer sums of distinct bits (order-independent)
-            key = (tile_of * 16 + lr // 8) * W + rel
-            ukey, inv = torch.unique(key, sorted=True, return_inverse=True)
-            mask = torch.zeros(ukey.numel(), dtype=torch.int64, device=dev)
-            mask.scatter_add_(0, inv, torch.ones_like(inv) << (lr % 8))
-            tw = ukey // W                                    # tile * 16 + warp
-            per_w = torch.bincount(tw, minlength=self.ntiles * 16).view(self.ntiles, 16)
-            pad_w = (per_w + 7) // 8 * 8
-            wo = torch.zeros((self.ntiles, 24), dtype=torch.int64, device=dev)
-            wo[:, 1:17] = torch.cumsum(pad_w, 1)
-            off = torch.zeros(self.ntiles + 1, dtype=torch.int64, device=dev)
-            off[1:] = torch.cumsum(wo[:, 16], 0)                 # entries (multiples of 8)
-            wstart = torch.zeros(self.ntiles * 16 + 1, dtype=torch.int64, device=dev)
-            wstart[1:] = torch.cumsum(per_w.view(-1), 0)
-            t_of, w_of = tw // 16, tw % 16
-            pos = off[t_of] + wo[t_of, w_of] + (torch.arange(ukey.numel(), device=dev) - wstart[tw])
-            ent = torch.zeros(max(8, int(off[-1].item())), dtype=torch.int32, device=dev)
-            ent[pos] = ((ukey % W) | (mask << 8)).to(torch.int32)
-            self.tile_nz = ent.to(torch.int16)                   # read as uint16
-            self.tile_off = off * 2                              # byte offsets
-            self.tile_rowoff = wo.to(torch.int16).contiguous()   # warp offsets (entries)
-            self.cm_entries = int(ukey.numel())
-        elif self.binary:
+        if self.binary:
             # row runs padded to 4-byte words (0xFF fills the padding): the
             # kernel reads a row's records one word at a time
             pc = (per + 3) // 4 * 4
@@ -245,8 +212,7 @@ class TiledCsr:
             nz[pos, 1] = a.values[didx].view(torch.int32)
             self.tile_nz = nz
             self.tile_off = off                               # record (8-byte) offsets
-        if fmt != "cm":
-            self.tile_rowoff = ro.to(torch.int16).contiguous()  # values <= MAXREC, read as uint16
+        self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= MAXREC, read as uint16
         keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
         keep[didx] = False
         rp = torch.zeros(a.rows + 1, dtype=torch.int64, device=dev)
@@ -272,13 +238,6 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
     """``linalg.spmm`` (linalg.py:71-75) through the TMA-staged tiled kernel
     (the factored one-byte-record kernel when ``t.binary``)."""
     d = x.shape[1] if d is None else d
-    if t.fmt == "cm":
-        xs = t.col_scaled_scratch(x.stride(0), x.device) if t.col_scale is not None else None
-        _lib.call("hb_spmm_tiled_cm", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),
-                  ptr(t.tile_off), ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col),
-                  ptr(t.row_scale), ptr(t.col_scale), ptr(x), x.stride(0), d, ptr(out), out.stride(0),
-                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), stream_handle(stream))
-        return out
     if t.binary:
         xs = t.col_scaled_scratch(x.stride(0), x.device) if t.col_scale is not None else None
         _lib.call("hb_spmm_tiled_bin", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),

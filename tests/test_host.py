@@ -207,63 +207,3 @@ def test_factor_scales_deterministic_first_nonzero():
             if len(e):
                 assert float(c[j]) == np.float32(v[e[0]] / diag[rows[e[0]]])
 
-
-def _tile_dense_cm(T):
-    """Rebuild the dense matrix a column-major ("cm") TiledCsr describes, and
-    check the entry layout: per warp ascending columns, zero padding only at
-    the end of a run, runs of multiples of 8 entries."""
-    out = np.zeros((T.rows, T.cols))
-    tp, win = T.tile_ptr.numpy(), T.tile_win.numpy()
-    off = T.tile_off.numpy() // 2
-    wo = T.tile_rowoff.numpy().astype(np.int64) & 0xFFFF
-    ent = T.tile_nz.numpy().astype(np.int64) & 0xFFFF
-    rs = T.row_scale.double().numpy() if T.row_scale is not None else np.ones(T.rows)
-    cs = T.col_scale.double().numpy() if T.col_scale is not None else np.ones(T.cols)
-    for b in range(T.nblocks):
-        for t in range(tp[b], tp[b + 1]):
-            assert off[t] % 8 == 0
-            for w in range(16):
-                assert wo[t, w] % 8 == 0 and wo[t, w + 1] >= wo[t, w]
-                run = ent[off[t] + wo[t, w]: off[t] + wo[t, w + 1]]
-                live = run[(run >> 8) != 0]
-                assert np.all((run >> 8)[:len(live)] != 0)          # padding only at the end
-                assert len(run) - len(live) < 8
-                assert np.all(np.diff(live & 0xFF) > 0)              # ascending columns
-                for e in live:
-                    c = win[t] * 64 + int(e & 0xFF)
-                    for bit in range(8):
-                        if (e >> 8) >> bit & 1:
-                            r = b * 128 + w * 8 + bit
-                            out[r, c] += rs[r] * cs[c]
-    rp, rc = T.res_ptr.numpy(), T.res_col.numpy()
-    for r in range(T.rows):
-        for k in range(rp[r], rp[r + 1]):
-            out[r, rc[k]] += rs[r] * cs[rc[k]]
-    return out
-
-
-@pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn"])
-def test_tiled_cm_layout_reconstructs_matrix(kind):
-    """Column-major factored tiles (hb_spmm_tiled_cm): (column, 8-row mask)
-    entries per warp describe exactly the trainer's operators."""
-    import scipy.sparse as sp
-    from paper_2303_01277_b200 import ops
-    rng = np.random.default_rng(5)
-    rows, cols = 300, 420
-    pat = (rng.random((rows, cols)) < 0.01)
-    pat[130:290, 64:192] |= rng.random((160, 128)) < 0.4
-    pat = pat.astype(np.float64)
-    if kind.startswith("mean"):
-        a = pat / np.maximum(pat.sum(1), 1)[:, None]
-        if kind == "mean_T":
-            a = a.T.copy()
-    else:
-        np.fill_diagonal(pat, 1.0)
-        dinv = 1 / np.sqrt(rng.integers(1, 50, cols))
-        a = dinv[:rows, None] * pat * dinv[None, :]
-    m = sp.csr_matrix(a.astype(np.float32))
-    A = ops.DeviceCsr(m.shape[0], m.shape[1], m.indptr, m.indices, m.data, "cpu")
-    T = ops.TiledCsr(A, threshold=100, fmt="cm")
-    assert T.RB == 128 and T.W == 64 and 0 < T.tiled_fraction < 1
-    assert T.cm_entries < T.tiled_nnz                      # columns shared by rows of a warp
-    np.testing.assert_allclose(_tile_dense_cm(T), m.toarray(), rtol=3e-7, atol=0)
