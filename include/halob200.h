@@ -137,22 +137,25 @@ int hb_spmm_tiled(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* 
  * D^-1 A, its transpose A^T D^-1, GCN D^-1/2 (A+I) D^-1/2):
  *   Y[i, 0:d) = r[i] * sum_{(i,j) in pattern} c[j] * X[j, 0:d)
  * row_scale r / col_scale c may each be NULL (= 1).  Tiles are block_rows
- * (64 or 128) rows x window_cols columns: 64; for d <= 48 also 128 (64-row
- * blocks) or 255 (64-row blocks, or 128-row blocks with 32 < d <= 48;
- * records up to 4096 bytes per tile then) (nblocks = ceil(nrows / block_rows)); a record is one byte, the
- * column inside the tile's window;
+ * (64, 120 or 128) rows x window_cols columns: 64; for d <= 48 also 128
+ * (64-row blocks) or 255 (64-row blocks, or 128-row blocks with 32 < d <= 48;
+ * records up to 4096 bytes per tile then) (nblocks = ceil(nrows /
+ * block_rows)); a record is one byte, the column inside the tile's window;
  * tile_rec[tile_off[t] .. tile_off[t+1]) (byte offsets, multiples of 16) are
  * tile t's row-sorted records and tile_rowoff[t*R .. +block_rows+1) their
- * row offsets (R = 72 for 64-row blocks, 136 for 128); res_ptr / res_col the
- * residual pattern.  With col_scale, c X is first written to xs (xrows x
- * ldxs floats, 16-byte aligned rows).  fp32 accumulation, tile-then-residual
- * order (same fp32 tolerance contract as hb_spmm_csr).  work as hb_spmm_tiled. */
+ * row offsets (R = 72 for 64-row blocks, 136 for 120 and 128); res_ptr /
+ * res_col the residual pattern.  With col_scale, c X is first written to xs
+ * (xrows x ldxs floats, 16-byte aligned rows).  block_order (nullable): a
+ * permutation of the row blocks, the order in which the dynamically
+ * scheduled work items are handed out (heaviest first balances the SMs; the
+ * results do not depend on it).  fp32 accumulation, tile-then-residual order
+ * (same fp32 tolerance contract as hb_spmm_csr).  work as hb_spmm_tiled. */
 int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32_t* tile_ptr,
                       const int32_t* tile_win, const int64_t* tile_off, const uint16_t* tile_rowoff,
                       const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                       const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
                       float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, int32_t block_rows,
-                      int32_t window_cols, void* stream);
+                      int32_t window_cols, const int32_t* block_order, void* stream);
 
 /* K5-K7 — the dense combine GEMMs (trainer.py:294, 313, 318-321) on tcgen05
  * tensor cores with the 3xTF32 split (fp32 accuracy):

@@ -44,7 +44,7 @@ _SIGS = {
     "hb_spmm_set_narrow": [c_int32],
     "hb_spmm_tiled": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64, P, P],
     "hb_spmm_tiled_bin": [c_int32, c_int32, c_int32, P, P, P, P, P, P, P, P, P, P, c_int64, c_int32, P, c_int64,
-                          P, c_int64, P, c_int32, c_int32, P],
+                          P, c_int64, P, c_int32, c_int32, P, P],
     "hb_spmm_csr_ex": [c_int32, P, P, P, P, c_int64, c_int32, P, c_int64, c_int64, c_int32, c_int32, c_int32, P, P],
     "hb_softmax_xent": [P, c_int64, c_int32, c_int32, P, P, c_double, P, c_int64, P, P, c_int32, P, P],
     "hb_relu": [P, c_int64, c_int32, c_int32, P, c_int64, P],

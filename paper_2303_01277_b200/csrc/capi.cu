@@ -44,7 +44,7 @@ cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, con
 cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                                   const uint8_t*, const int64_t*, const int32_t*, const float*, const float*,
                                   const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, int, int,
-                                  cudaStream_t);
+                                  const int32_t*, cudaStream_t);
 
 int num_sms() {
   static int cached = 0;
@@ -146,17 +146,18 @@ int hb_spmm_tiled_bin(int32_t nrows, int32_t xrows, int32_t nblocks, const int32
                       const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                       const float* row_scale, const float* col_scale, const float* X, int64_t ldx, int32_t d,
                       float* Y, int64_t ldy, float* xs, int64_t ldxs, int32_t* work, int32_t block_rows,
-                      int32_t window_cols, void* stream) {
-  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (block_rows != 64 && block_rows != 128) ||
+                      int32_t window_cols, const int32_t* block_order, void* stream) {
+  if (nrows < 0 || d < 0 || ldx < d || ldy < d || (block_rows != 64 && block_rows != 120 && block_rows != 128) ||
       (window_cols != 64 && window_cols != 128 && window_cols != 255) ||
       (window_cols != 64 && d > 48) || (window_cols == 128 && block_rows != 64) ||
-      (window_cols == 255 && block_rows == 128 && d <= 32) ||
+      (window_cols == 255 && block_rows == 128 && d <= 32) || (block_rows == 120 && window_cols != 64) ||
       nblocks != (nrows + block_rows - 1) / block_rows ||
       (nrows > 0 && (!tile_ptr || !res_ptr || !X || !Y || !work)) || (col_scale && (!xs || ldxs < d)))
     return fail(HB_EINVAL, "hb_spmm_tiled_bin: bad arguments");
   const cudaError_t e = hb::launch_spmm_tiled_bin(nrows, xrows, nblocks, tile_ptr, tile_win, tile_off, tile_rowoff,
                                                   tile_rec, res_ptr, res_col, row_scale, col_scale, X, ldx, d, Y,
-                                                  ldy, xs, ldxs, work, block_rows, window_cols, S(stream));
+                                                  ldy, xs, ldxs, work, block_rows, window_cols, block_order,
+                                                  S(stream));
   if (e == cudaErrorNotSupported)
     return fail(HB_EINVAL, "hb_spmm_tiled_bin: X/Y need 16-byte aligned rows (ld % 4 == 0)");
   return check(e, "hb_spmm_tiled_bin");

@@ -48,7 +48,7 @@ namespace sb {
 constexpr int max_rec(int rb, int kw) { return rb == 128 && kw == 255 ? 4096 : 2048; }
 // consumer warps per CTA (CW; a warp owns RB / CW rows of the block) + 1 producer
 // u16 row offsets per tile: RB + 1 used, padded to a 16-byte multiple
-constexpr int row_off_count(int rb) { return rb == 128 ? 136 : 72; }
+constexpr int row_off_count(int rb) { return rb == 64 ? 72 : 136; }
 constexpr int kQ = 4;
 
 struct Args {
@@ -66,6 +66,7 @@ struct Args {
   int64_t ldx;
   float* Y;
   int64_t ldy;
+  const int32_t* block_order;     // nullable: item i works on row block block_order[i / npanels]
 };
 
 template <int RB, int NV, int G, int S, int KW = 64, bool TP = false>
@@ -115,7 +116,7 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 // groups (64-byte accesses, two rows per quarter-warp) the two halves of a
 // quarter-warp collide in 7 of 8 bank alignments.
 template <int RB, int NV, int G, int S, int MINB, int CW, bool TP = false, int KW = 64>
-__global__ void __maxnreg__(MINB == 1 ? 96 : 56)
+__global__ void __maxnreg__(MINB == 1 ? (CW >= 24 ? 64 : 96) : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   using S_ = Smem<RB, NV, G, S, KW, TP>;
   constexpr int P = S_::P;
@@ -163,7 +164,8 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
       }
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= items) break;
-      const int b = item / a.npanels, pn = item % a.npanels;
+      const int bi = item / a.npanels, pn = item % a.npanels;
+      const int b = a.block_order ? __ldg(a.block_order + bi) : bi;
       const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
       for (int t = t0; t < t1; ++t, ++it) {
         if (lane >= S || it % S != lane) continue;
@@ -198,7 +200,8 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&iempty[q]);
     if (item >= items) break;
-    const int b = item / a.npanels, pn = item % a.npanels;
+    const int bi = item / a.npanels, pn = item % a.npanels;
+    const int b = a.block_order ? __ldg(a.block_order + bi) : bi;
     const int r0 = b * RB + warp * kRPW;
     const int col0 = pn * P;
     float4 acc[RPG][NV];
@@ -238,7 +241,7 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
         if constexpr (G == 32) {
           // records in flight per warp: 4, or 2 when the accumulators of a
           // 128-row block (8 rows x NV float4) leave no registers for more
-          constexpr int kU = RPG * NV > 8 ? 2 : 4;
+          constexpr int kU = RPG * NV > 8 || CW >= 24 ? 2 : 4;
           for (; w + 1 < w1; ++w) {
             const uint32_t q = rec32[w];                           // 4 records, one broadcast
 #pragma unroll
@@ -483,7 +486,8 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
                                   const uint8_t* tile_rec, const int64_t* res_ptr, const int32_t* res_col,
                                   const float* row_scale, const float* col_scale, const float* X, int64_t ldx,
                                   int d, float* Y, int64_t ldy, float* xs, int64_t ldxs, int* work,
-                                  int block_rows, int window_cols, cudaStream_t stream) {
+                                  int block_rows, int window_cols, const int32_t* block_order,
+                                  cudaStream_t stream) {
   if (nrows <= 0 || d <= 0) return cudaSuccess;
   if ((ldx & 3) || (ldy & 3) || (((uintptr_t)X) & 15) || (((uintptr_t)Y) & 15)) return cudaErrorNotSupported;
   if (col_scale) {
@@ -497,7 +501,7 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
   a.nrows = nrows; a.nblocks = nblocks; a.d = d; a.work = work;
   a.tile_ptr = tile_ptr; a.tile_win = tile_win; a.tile_off = tile_off; a.tile_rowoff = tile_rowoff;
   a.tile_rec = tile_rec; a.res_ptr = res_ptr; a.res_col = res_col; a.row_scale = row_scale;
-  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
+  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.block_order = block_order;
   const int narrow = g_bin_narrow;
   if (window_cols == 255) {
     // 255-column windows (one-byte records 0..254, 0xFF = padding)
@@ -534,6 +538,13 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
     if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2>(a, xrows, stream);   // 4 rows of a warp in parallel
     if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1>(a, xrows, stream);
     return sb::launch_nv<64, 2, 32, 3, 1>(a, xrows, stream);              // 256-column panels
+  }
+  if (block_rows == 120) {
+    // 30 consumer warps x 4 rows (64 registers, two records in flight): the
+    // staged X window serves 120 rows, so its TMA writes into shared memory
+    // cost 0.53x of a 64-row block's per nonzero
+    if (d <= 128) return sb::launch_nv<120, 1, 32, 5, 1, 30>(a, xrows, stream);
+    return sb::launch_nv<120, 2, 32, 3, 1, 30>(a, xrows, stream);
   }
   if (block_rows != 128) return cudaErrorInvalidValue;
   // 128-row blocks: 8 rows per warp; a TMA-staged X window serves twice the

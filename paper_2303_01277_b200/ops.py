@@ -117,7 +117,7 @@ class TiledCsr:
       at most 48 columns) doubles the nonzeros per (row, tile)."""
 
     def __init__(self, a: DeviceCsr, threshold: int = 64, factored: bool | None = None,
-                 block_rows: int | None = None, window: int = 64):
+                 block_rows: int | None = None, window: int = 64, block_order: str | None = None):
         import torch
         dev = a.row_ptr.device
         scales = factor_scales(a) if factored in (None, True) else None
@@ -127,14 +127,16 @@ class TiledCsr:
         self.row_scale, self.col_scale = scales if self.binary else (None, None)
         if self.binary:
             import os
-            rb = block_rows or int(os.environ.get("HB_BIN_RB", "64"))
-            if rb not in (64, 128):
-                raise ValueError(f"factored tiles are 64 or 128 rows, not {rb}")
-            self.RB, self.ROWOFF, self.MAXREC = rb, (136 if rb == 128 else 72), 2048
+            # 120-row blocks (30 consumer warps x 4 rows): the staged X window
+            # serves 120 rows (profiles/r2_kbench_spmm_wide.jsonl)
+            rb = block_rows or int(os.environ.get("HB_BIN_RB", "120"))
+            if rb not in (64, 120, 128):
+                raise ValueError(f"factored tiles are 64, 120 or 128 rows, not {rb}")
+            self.RB, self.ROWOFF, self.MAXREC = rb, (72 if rb == 64 else 136), 2048
         else:
             self.RB, self.ROWOFF, self.MAXREC = 64, 72, 1024
         if window not in (64, 128, 255) or (window != 64 and not self.binary) or \
-                (window == 128 and self.RB != 64):
+                (window == 128 and self.RB != 64) or (window != 64 and self.RB == 120):
             raise ValueError("128-column windows need factored 64-row tiles, 255-column ones factored tiles")
         if window == 255 and self.RB == 128:
             self.MAXREC = 4096
@@ -213,6 +215,25 @@ class TiledCsr:
             self.tile_nz = nz
             self.tile_off = off                               # record (8-byte) offsets
         self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= MAXREC, read as uint16
+        # work-item order (hb_spmm_tiled_bin block_order): ascending blocks by
+        # default (neighbouring blocks share X windows in L2); "lpt": heaviest
+        # block first (the dynamically scheduled tail is made of light blocks)
+        # "tail": ascending, but the last 3 x 148 blocks heaviest first (the
+        # final scheduling round is made of the lightest of them)
+        self.block_order = None
+        if block_order in ("lpt", "tail"):
+            blk_nnz = torch.zeros(self.nblocks, dtype=torch.int64, device=dev)
+            blk_nnz.index_add_(0, torch.div(rows, RB, rounding_mode="floor"), torch.ones_like(rows))
+            if block_order == "lpt":
+                order = torch.sort(-blk_nnz, stable=True).indices
+            else:
+                k = min(self.nblocks, 3 * 148)
+                order = torch.arange(self.nblocks, device=dev)
+                tail = order[self.nblocks - k:]
+                order[self.nblocks - k:] = tail[torch.sort(-blk_nnz[tail], stable=True).indices]
+            self.block_order = order.to(torch.int32).contiguous()
+        elif block_order is not None:
+            raise ValueError(f"unknown block order {block_order!r}")
         keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
         keep[didx] = False
         rp = torch.zeros(a.rows + 1, dtype=torch.int64, device=dev)
@@ -243,7 +264,8 @@ def spmm_tiled(t: TiledCsr, x, out, d: int | None = None, stream=None):
         _lib.call("hb_spmm_tiled_bin", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win),
                   ptr(t.tile_off), ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col),
                   ptr(t.row_scale), ptr(t.col_scale), ptr(x), x.stride(0), d, ptr(out), out.stride(0),
-                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), t.RB, t.W, stream_handle(stream))
+                  ptr(xs), xs.stride(0) if xs is not None else 0, ptr(t.work), t.RB, t.W, ptr(t.block_order),
+                  stream_handle(stream))
         return out
     _lib.call("hb_spmm_tiled", t.rows, t.cols, t.nblocks, ptr(t.tile_ptr), ptr(t.tile_win), ptr(t.tile_off),
               ptr(t.tile_rowoff), ptr(t.tile_nz), ptr(t.res_ptr), ptr(t.res_col), ptr(t.res_val), ptr(x),

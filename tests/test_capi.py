@@ -66,14 +66,18 @@ def test_argument_validation_without_a_device():
     lib.hb_spmm_tiled.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, i64, i32, P, i64, P, P]
     rc = lib.hb_spmm_tiled(64, 64, 1, 1, 1, 1, 1, 1, 1, 1, 1, 16, 8, 8, 16, 8, None, None)
     assert rc == -1 and b"hb_spmm_tiled" in lib.hb_last_error()
-    lib.hb_spmm_tiled_bin.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, P, i64, i32, P, i64, P, i64, P, P]
-    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, None, None)
+    lib.hb_spmm_tiled_bin.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, P, P, P, i64, i32, P, i64, P, i64, P,
+                                      i32, i32, P, P]
+    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, None,
+                               128, 64, None, None)
     assert rc == -1 and b"hb_spmm_tiled_bin" in lib.hb_last_error()
     # a column scale needs the scratch copy of X
-    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, 16, 16, 8, 8, 16, 8, None, 0, 16, None)
+    rc = lib.hb_spmm_tiled_bin(128, 128, 1, 1, 1, 1, 1, 1, 1, 1, None, 16, 16, 8, 8, 16, 8, None, 0, 16,
+                               128, 64, None, None)
     assert rc == -1
     # 128-row blocks
-    rc = lib.hb_spmm_tiled_bin(128, 128, 2, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, 16, None)
+    rc = lib.hb_spmm_tiled_bin(128, 128, 2, 1, 1, 1, 1, 1, 1, 1, None, None, 16, 8, 8, 16, 8, None, 0, 16,
+                               128, 64, None, None)
     assert rc == -1
     # > 16384 rows: the loss reduction needs the caller's partials
     lib.hb_softmax_xent.argtypes = [P, i64, i32, i32, P, P, ctypes.c_double, P, i64, P, P, i32, P, P]

@@ -180,7 +180,7 @@ def test_tiled_layout_reconstructs_matrix(kind):
     A = ops.DeviceCsr(m.shape[0], m.shape[1], m.indptr, m.indices, m.data, "cpu")
     T = ops.TiledCsr(A, threshold=100, block_rows=128 if kind == "gcn" else None)
     assert T.binary == (kind != "general")
-    assert T.RB == (128 if kind == "gcn" else 64) and 0 < T.tiled_fraction < 1
+    assert T.RB == (128 if kind == "gcn" else 120 if T.binary else 64) and 0 < T.tiled_fraction < 1
     np.testing.assert_allclose(_tile_dense(T), m.toarray(), rtol=3e-7, atol=0)
 
 

@@ -76,11 +76,13 @@ def test_spmm_random_power_law_rows(d):
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None, block_rows=None, window=64):
+def _tiled_run(rp, ci, v, x, ncols, threshold, ld_pad=0, factored=None, block_rows=None, window=64,
+               block_order=None):
     from paper_2303_01277_b200 import ops
     rows, d = len(rp) - 1, x.shape[1]
     A = ops.DeviceCsr(rows, ncols, rp, ci, v, "cuda")
-    T = ops.TiledCsr(A, threshold=threshold, factored=factored, block_rows=block_rows, window=window)
+    T = ops.TiledCsr(A, threshold=threshold, factored=factored, block_rows=block_rows, window=window,
+                     block_order=block_order)
     X = torch.zeros(ncols, d + ld_pad, device="cuda")
     X[:, :d] = torch.from_numpy(x)
     Y = torch.full((rows, d + ld_pad), 7.0, device="cuda")
@@ -121,7 +123,7 @@ def _community_pattern(rng, rows, comm, halo_cols, lo=20, hi=120):
     return np.asarray(rp, dtype=np.int64), np.concatenate(ci).astype(np.int64)
 
 
-@pytest.mark.parametrize("rb", [64, 128])
+@pytest.mark.parametrize("rb", [64, 120, 128])
 @pytest.mark.parametrize("kind", ["mean", "mean_T", "gcn", "gcn_T"])
 @pytest.mark.parametrize("d", [41, 100, 128, 256, 602])
 @pytest.mark.parametrize("threshold", [1, 64])
@@ -156,12 +158,17 @@ def test_spmm_tiled_factored_operators(kind, d, threshold, rb):
     ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
     got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=rb)
     assert T.binary and T.RB == rb
+    for order in ("lpt", "tail"):
+        # the work-item order changes which CTA runs a block, not the result
+        got_o, _ = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True,
+                              block_rows=rb, block_order=order)
+        assert np.array_equal(got_o, got)
     assert (T.row_scale is None) == (kind == "mean_T") and (T.col_scale is None) == (kind == "mean")
     tol = 1e-5 * _bound(rp2, ci2, v, x) + 1e-30
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-@pytest.mark.parametrize("rb", [64, 128])
+@pytest.mark.parametrize("rb", [64, 120, 128])
 @pytest.mark.parametrize("d", [41, 256])
 def test_spmm_tiled_factored_splits_dense_tiles(d, rb):
     """A fully dense 128x64 block (8192 one-byte records) exceeds a factored
