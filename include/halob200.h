@@ -201,8 +201,10 @@ int hb_gemm_set_path(int32_t path);
  * warps x 8 rows (3 CTAs/SM) — the default; 2 / 3 = "tail pairs" (32 < d <=
  * 48): 8-lane groups read a nonzero's first 32 columns as one 128-byte
  * access and the tails of two nonzeros in a third (16 / 8 consumer warps).
- * 255-column windows: 1 or 3 (default) = tail pairs, 2 CTAs/SM; 2 = tail
- * pairs, 1 CTA/SM; 0 = 4-lane groups. */
+ * 255-column windows: 1 or 4 (default) = tail pairs with two lane groups
+ * sharing each row (record pairs round-robin: balanced run lengths), 2
+ * CTAs/SM; 3 = tail pairs, a lane group per row, 2 CTAs/SM; 2 = the same,
+ * 1 CTA/SM; 0 = 4-lane groups.  64- and 128-column windows treat 4 as 1. */
 int hb_spmm_set_narrow(int32_t variant);
 
 /* K8 — softmax_cross_entropy (linalg.py:87-112) on the rows of one rank:

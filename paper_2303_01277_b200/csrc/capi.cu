@@ -196,8 +196,8 @@ int hb_gemm_set_path(int32_t path) {
 }
 
 int hb_spmm_set_narrow(int32_t variant) {
-  if (variant < 0 || variant > 3)
-    return fail(HB_EINVAL, "hb_spmm_set_narrow: variant must be 0..3");
+  if (variant < 0 || variant > 4)
+    return fail(HB_EINVAL, "hb_spmm_set_narrow: variant must be 0..4");
   hb::g_bin_narrow = variant;
   return HB_OK;
 }

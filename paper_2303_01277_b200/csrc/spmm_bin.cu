@@ -34,8 +34,8 @@
 
 namespace hb {
 
-// narrow-row consumer layout (hb_spmm_set_narrow); 1 measured fastest at
-// d = 41 on Reddit (1.41 ms vs 1.54 / 1.56 / 1.61 ms for 0 / 2 / 3)
+// narrow-row consumer layout (hb_spmm_set_narrow); 1 = the measured fastest
+// per window width (255-column windows: balanced tail pairs)
 int g_bin_narrow = getenv("HB_BIN_NARROW") ? atoi(getenv("HB_BIN_NARROW")) : 1;
 // 128-row blocks, d > 128: 1 = 256-column panels (two records in flight), 0 = 128-column panels
 int g_bin_wide128 = getenv("HB_BIN_WIDE128") ? atoi(getenv("HB_BIN_WIDE128")) : 1;
@@ -115,6 +115,65 @@ __device__ __forceinline__ void add_row(float4 (&acc)[NV], const float4* __restr
 // tail sums, folded across the half-groups before the store.  With 4-lane
 // groups (64-byte accesses, two rows per quarter-warp) the two halves of a
 // quarter-warp collide in 7 of 8 bank alignments.
+// barrier setup shared by the consumer layouts: S ring stages, kQ work-item slots
+template <int S, int CW>
+__device__ __forceinline__ void bin_init(uint64_t* full, uint64_t* empty, uint64_t* ifull, uint64_t* iempty) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+    for (int q = 0; q < kQ; ++q) {
+      mbar_init(&ifull[q], 1);
+      mbar_init(&iempty[q], CW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// producer warp: lane 0 claims work items (row block, panel) and posts them to
+// the consumers; lane s feeds ring stage s (X window by TMA, the tile's
+// records and row offsets by bulk copies)
+template <class S_, int S, int KW, int kRowOff>
+__device__ __forceinline__ void bin_producer(const CUtensorMap* tmX, const Args& a, uint8_t* smem, uint64_t* full,
+                                             uint64_t* empty, uint64_t* ifull, uint64_t* iempty, int* item_q,
+                                             int lane, int items, int P) {
+  int it = 0;
+  for (int qi = 0;; ++qi) {
+    int item = 0;
+    if (lane == 0) {
+      item = atomicAdd(a.work, 1);
+      const int q = qi % kQ;
+      mbar_wait(&iempty[q], ((qi / kQ) & 1) ^ 1);
+      item_q[q] = item;
+      mbar_arrive_cta(&ifull[q]);
+      if (item >= items && atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
+        atomicExch(a.work, 0);
+        atomicExch(a.work + 1, 0);
+      }
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= items) break;
+    const int bi = item / a.npanels, pn = item % a.npanels;
+    const int b = a.block_order ? __ldg(a.block_order + bi) : bi;
+    const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
+    for (int t = t0; t < t1; ++t, ++it) {
+      if (lane >= S || it % S != lane) continue;
+      const int s = it % S;
+      mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+      uint8_t* st = smem + s * S_::STAGE;
+      const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
+      const uint32_t rb = (uint32_t)(o1 - o0);
+      mbar_expect_tx(&full[s], (uint32_t)(KW * a.pw * 4) + rb + S_::RO_BYTES);
+      tma_2d(st, tmX, pn * P, a.tile_win[t] * KW, &full[s]);
+      if (rb) tma_load_1d(st + S_::X_BYTES, a.tile_rec + o0, rb, &full[s]);
+      tma_load_1d(st + S_::X_BYTES + S_::MAXREC, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES, &full[s]);
+    }
+  }
+  __syncwarp();
+}
+
 template <int RB, int NV, int G, int S, int MINB, int CW, bool TP = false, int KW = 64>
 __global__ void __maxnreg__(MINB == 1 ? (CW >= 24 ? 64 : 96) : 56)
 spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
@@ -132,55 +191,11 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   __shared__ int item_q[kQ];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hg = lane / G, gl = lane % G;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
-    }
-    for (int q = 0; q < kQ; ++q) {
-      mbar_init(&ifull[q], 1);
-      mbar_init(&iempty[q], kConsumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
+  bin_init<S, kConsumers>(full, empty, ifull, iempty);
   const int items = a.nblocks * a.npanels;
 
   if (warp == kConsumers) {
-    // ---------------- producer: lane 0 claims items, lane s feeds ring stage s
-    int it = 0;
-    for (int qi = 0;; ++qi) {
-      int item = 0;
-      if (lane == 0) {
-        item = atomicAdd(a.work, 1);
-        const int q = qi % kQ;
-        mbar_wait(&iempty[q], ((qi / kQ) & 1) ^ 1);
-        item_q[q] = item;
-        mbar_arrive_cta(&ifull[q]);
-        if (item >= items && atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
-          atomicExch(a.work, 0);
-          atomicExch(a.work + 1, 0);
-        }
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= items) break;
-      const int bi = item / a.npanels, pn = item % a.npanels;
-      const int b = a.block_order ? __ldg(a.block_order + bi) : bi;
-      const int t0 = a.tile_ptr[b], t1 = a.tile_ptr[b + 1];
-      for (int t = t0; t < t1; ++t, ++it) {
-        if (lane >= S || it % S != lane) continue;
-        const int s = it % S;
-        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-        uint8_t* st = smem + s * S_::STAGE;
-        const int64_t o0 = a.tile_off[t], o1 = a.tile_off[t + 1];
-        const uint32_t rb = (uint32_t)(o1 - o0);
-        mbar_expect_tx(&full[s], (uint32_t)(KW * a.pw * 4) + rb + S_::RO_BYTES);
-        tma_2d(st, &tmX, pn * P, a.tile_win[t] * KW, &full[s]);
-        if (rb) tma_load_1d(st + S_::X_BYTES, a.tile_rec + o0, rb, &full[s]);
-        tma_load_1d(st + S_::X_BYTES + S_::MAXREC, a.tile_rowoff + (int64_t)t * kRowOff, S_::RO_BYTES, &full[s]);
-      }
-    }
-    __syncwarp();
+    bin_producer<S_, S, KW, kRowOff>(&tmX, a, smem, full, empty, ifull, iempty, item_q, lane, items, P);
     return;
   }
 
@@ -412,6 +427,154 @@ spmm_bin_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
   }
 }
 
+// Narrow rows (32 < d <= 48), 64-row blocks, tail pairs with GPR lane groups
+// per row.  The tail-pair layout of spmm_bin_kernel gives each 8-lane group
+// its own row, so a warp's four groups walk runs of different lengths and the
+// warp waits for the longest; here GPR groups share one row, taking its
+// record pairs round-robin (trip counts differ by at most one), and their
+// partial sums are added with shuffles once the block is done.  A warp still
+// owns 4 rows: SLOTS = 4 / GPR rows are in flight at a time, KS = GPR row
+// sets in turn (acc holds KS rows x {main, tail}).  The summation order
+// inside a row differs from CSR order (tolerance contract of hb_spmm_csr).
+template <int S, int MINB, int GPR, int KW>
+__global__ void __maxnreg__(MINB == 1 ? 96 : 56)
+spmm_bin_tpb_kernel(const __grid_constant__ CUtensorMap tmX, Args a) {
+  constexpr int RB = 64, CW = 16, G = 8, NV = 2;
+  using S_ = Smem<RB, NV, G, S, KW, true>;
+  constexpr int kRPW = RB / CW, NG = 32 / G, SLOTS = NG / GPR, KS = kRPW / SLOTS;
+  constexpr int kRowOff = row_off_count(RB);
+  static_assert(kRPW == 4 && NG == 4 && KS == GPR, "4 rows x 4 lane groups per warp");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full[S], empty[S], ifull[kQ], iempty[kQ];
+  __shared__ int item_q[kQ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bin_init<S, CW>(full, empty, ifull, iempty);
+  const int items = a.nblocks * a.npanels;
+  if (warp == CW) {
+    bin_producer<S_, S, KW, kRowOff>(&tmX, a, smem, full, empty, ifull, iempty, item_q, lane, items, S_::P);
+    return;
+  }
+  const int hg = lane >> 3, gl = lane & 7;
+  const int slot = hg / GPR, sub = hg % GPR;
+  const int pw4 = a.pw / 4;
+  const int tl = gl & 3;
+  const bool tail_lane = (8 + tl) * 4 < a.pw;       // tail float4 8 + tl exists
+  int it = 0;
+  for (int qi = 0;; ++qi) {
+    const int q = qi % kQ;
+    mbar_wait(&ifull[q], (qi / kQ) & 1);
+    const int item = item_q[q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&iempty[q]);
+    if (item >= items) break;
+    const int bi = item / a.npanels;
+    const int b = a.block_order ? __ldg(a.block_order + bi) : bi;
+    const int r0 = b * RB + warp * kRPW;
+    float4 acc[KS][2];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      acc[k][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc[k][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int t = a.tile_ptr[b]; t < a.tile_ptr[b + 1]; ++t, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint8_t* st = smem + s * S_::STAGE;
+      const float4* xs = reinterpret_cast<const float4*>(st);
+      const uint32_t* rec32 = reinterpret_cast<const uint32_t*>(st + S_::X_BYTES);
+      const uint16_t* ro = reinterpret_cast<const uint16_t*>(st + S_::X_BYTES + S_::MAXREC) + warp * kRPW;
+      const uint64_t ro4 = *reinterpret_cast<const uint64_t*>(ro);     // the warp's 4 row offsets
+      const int ro_end = ro[kRPW];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const int rr = k * SLOTS + slot;
+        const int w0 = (int)((ro4 >> (16 * rr)) & 0xffffu) >> 2;
+        const int w1 = (rr + 1 < kRPW ? (int)((ro4 >> (16 * (rr + 1))) & 0xffffu) : ro_end) >> 2;
+        const int np = 2 * (w1 - w0);                              // record pairs (the last may be padding)
+        for (int pp = sub; pp < np; pp += GPR) {
+          const uint32_t qw = rec32[w0 + (pp >> 1)] >> (16 * (pp & 1));
+          const int j0 = (int)(qw & 0xffu), j1 = (int)((qw >> 8) & 0xffu);
+          if (j0 == 0xFF) break;                                   // padding ends the run
+          const bool has1 = j1 != 0xFF;
+          const float4 m0 = xs[j0 * pw4 + gl];
+          float4 m1 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (has1) m1 = xs[j1 * pw4 + gl];
+          // one quarter-warp access for both tails: lanes 0-3 the first's, 4-7 the second's
+          const int jt = gl < 4 ? j0 : j1;
+          float4 tv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (tail_lane && (gl < 4 || has1)) tv = xs[jt * pw4 + 8 + tl];
+          acc[k][0].x += m0.x; acc[k][0].y += m0.y; acc[k][0].z += m0.z; acc[k][0].w += m0.w;
+          if (has1) {
+            acc[k][0].x += m1.x; acc[k][0].y += m1.y; acc[k][0].z += m1.z; acc[k][0].w += m1.w;
+          }
+          acc[k][1].x += tv.x; acc[k][1].y += tv.y; acc[k][1].z += tv.z; acc[k][1].w += tv.w;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
+    }
+    // fold the second records' tails (lanes 4-7) into lanes 0-3, then add the
+    // partial sums of the GPR groups that shared each row
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      float4& tv = acc[k][1];
+      const float x = __shfl_down_sync(0xffffffffu, tv.x, 4, 8), y = __shfl_down_sync(0xffffffffu, tv.y, 4, 8);
+      const float z = __shfl_down_sync(0xffffffffu, tv.z, 4, 8), w = __shfl_down_sync(0xffffffffu, tv.w, 4, 8);
+      if (gl < 4) { tv.x += x; tv.y += y; tv.z += z; tv.w += w; }
+#pragma unroll
+      for (int o = 8; o < 8 * GPR; o <<= 1) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          float4& u = acc[k][v];
+          u.x += __shfl_xor_sync(0xffffffffu, u.x, o);
+          u.y += __shfl_xor_sync(0xffffffffu, u.y, o);
+          u.z += __shfl_xor_sync(0xffffffffu, u.z, o);
+          u.w += __shfl_xor_sync(0xffffffffu, u.w, o);
+        }
+      }
+    }
+    // group (slot, sub) finishes row set k = sub: residual gathers, row scale, store
+    float4 am = make_float4(0.f, 0.f, 0.f, 0.f), at = am;
+#pragma unroll
+    for (int k = 0; k < KS; ++k)
+      if (k == sub) { am = acc[k][0]; at = acc[k][1]; }
+    const int r = r0 + sub * SLOTS + slot;
+    if (r < a.nrows) {
+      const int64_t e0 = a.res_ptr[r], e1 = a.res_ptr[r + 1];
+      const bool has_t = gl < 4 && tail_lane;
+      for (int64_t k = e0; k < e1; ++k) {
+        const float4* xr = reinterpret_cast<const float4*>(a.X + (int64_t)__ldg(a.res_col + k) * a.ldx);
+        if (gl * 4 < a.d) {
+          const float4 t4 = __ldg(xr + gl);
+          am.x += t4.x; am.y += t4.y; am.z += t4.z; am.w += t4.w;
+        }
+        if (has_t) {
+          const float4 t4 = __ldg(xr + 8 + gl);
+          at.x += t4.x; at.y += t4.y; at.z += t4.z; at.w += t4.w;
+        }
+      }
+      const float sc = a.row_scale ? __ldg(a.row_scale + r) : 1.f;
+      float* y = a.Y + (int64_t)r * a.ldy;
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        if (v == 1 && !has_t) continue;
+        const float4 u = v == 0 ? am : at;
+        const int col = v == 0 ? gl * 4 : (8 + gl) * 4;
+        const int rem = a.d - col;
+        const float4 o = make_float4(u.x * sc, u.y * sc, u.z * sc, u.w * sc);
+        if (rem >= 4) {
+          *reinterpret_cast<float4*>(y + col) = o;
+        } else if (rem > 0) {
+          y[col] = o.x;
+          if (rem > 1) y[col + 1] = o.y;
+          if (rem > 2) y[col + 2] = o.z;
+        }
+      }
+    }
+  }
+}
+
 // Xs[j, :d] = c[j] * X[j, :d]  (float4 rows: ld % 4 == 0, 16-byte aligned)
 __global__ void scale_rows_kernel(const float* __restrict__ X, int64_t ldx, int rows, int d4,
                                   const float* __restrict__ c, float* __restrict__ Xs, int64_t ldxs) {
@@ -468,6 +631,37 @@ static cudaError_t launch_nv(const Args& a0, int xrows, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <int S, int MINB, int GPR, int KW>
+static cudaError_t launch_tpb(const Args& a0, int xrows, cudaStream_t stream) {
+  using S_ = Smem<64, 2, 8, S, KW, true>;
+  static_assert(MINB * S_::TOTAL <= 227 * 1024, "smem");
+  Args a = a0;
+  a.npanels = 1;
+  a.pw = (a.d + 3) / 4 * 4;
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)a.d, (cuuint64_t)xrows};
+  cuuint64_t strides[1] = {(cuuint64_t)(a.ldx * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)a.pw, (cuuint32_t)KW};
+  cuuint32_t es[2] = {1u, 1u};
+  if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.X), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(spmm_bin_tpb_kernel<S, MINB, GPR, KW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S_::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int items = a.nblocks;
+  const int grid = items < MINB * num_sms() ? items : MINB * num_sms();
+  if (grid > 0) spmm_bin_tpb_kernel<S, MINB, GPR, KW><<<grid, 32 * 17, S_::TOTAL, stream>>>(map, a);
+  return cudaGetLastError();
+}
+
 }  // namespace sb
 
 // Xs[j, :d] = c[j] * X[j, :d] (the column scaling of the factored operators)
@@ -513,10 +707,13 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
       return sb::launch_nv<128, 2, 8, 2, 2, 16, true, 255>(a, xrows, stream);
     }
     if (block_rows != 64) return cudaErrorInvalidValue;
-    // default (1, 3): tail pairs, 2 CTAs per SM (1.03 ms at d = 41 on Reddit);
-    // 2: tail pairs, 1 CTA per SM; 0 (or d <= 32): 4-lane groups
+    // default (1, 4): tail pairs with two lane groups per row, 2 CTAs per SM
+    // (0.95 / 1.00 ms at d = 41 on Reddit's mean operator / its transpose);
+    // 3: tail pairs, a lane group per row (1.03 / 1.08 ms); 2: the same, 1
+    // CTA per SM; 0 (or d <= 32): 4-lane groups
+    if (d > 32 && (narrow == 1 || narrow == 4)) return sb::launch_tpb<2, 2, 2, 255>(a, xrows, stream);
     if (d > 32 && narrow == 2) return sb::launch_nv<64, 2, 8, 2, 1, 16, true, 255>(a, xrows, stream);
-    if (d > 32 && narrow != 0) return sb::launch_nv<64, 2, 8, 2, 2, 16, true, 255>(a, xrows, stream);
+    if (d > 32 && narrow == 3) return sb::launch_nv<64, 2, 8, 2, 2, 16, true, 255>(a, xrows, stream);
     return sb::launch_nv<64, 3, 4, 2, 2, 8, false, 255>(a, xrows, stream);
   }
   if (window_cols == 128) {
@@ -534,7 +731,7 @@ cudaError_t launch_spmm_tiled_bin(int nrows, int xrows, int nblocks, const int32
     // 8 rows in parallel (one per group), 3 CTAs per SM
     if (d > 32 && d <= 48 && narrow == 2) return sb::launch_nv<64, 2, 8, 4, 2, 16, true>(a, xrows, stream);
     if (d > 32 && d <= 48 && narrow == 3) return sb::launch_nv<64, 2, 8, 4, 3, 8, true>(a, xrows, stream);
-    if (d <= 48 && narrow == 1) return sb::launch_nv<64, 3, 4, 4, 3, 8>(a, xrows, stream);
+    if (d <= 48 && (narrow == 1 || narrow == 4)) return sb::launch_nv<64, 3, 4, 4, 3, 8>(a, xrows, stream);
     if (d <= 64) return sb::launch_nv<64, 2, 8, 4, 2>(a, xrows, stream);   // 4 rows of a warp in parallel
     if (d <= 128) return sb::launch_nv<64, 1, 32, 5, 1>(a, xrows, stream);
     return sb::launch_nv<64, 2, 32, 3, 1>(a, xrows, stream);              // 256-column panels

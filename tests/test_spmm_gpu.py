@@ -238,7 +238,7 @@ def test_spmm_tiled_splits_dense_tiles(d):
     assert np.all(np.abs(got - ref) <= tol), np.abs(got - ref).max()
 
 
-@pytest.fixture(params=[0, 1, 2, 3], ids=["g8", "g4x3", "tail_pairs16", "tail_pairs8"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["g8", "g4x3_or_balanced_pairs", "tail_pairs16", "tail_pairs8"])
 def narrow_variant(request):
     from paper_2303_01277_b200 import ops
     ops.spmm_set_narrow(request.param)
