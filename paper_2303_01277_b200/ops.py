@@ -216,24 +216,25 @@ class TiledCsr:
             self.tile_off = off                               # record (8-byte) offsets
         self.tile_rowoff = ro.to(torch.int16).contiguous()     # values <= MAXREC, read as uint16
         # work-item order (hb_spmm_tiled_bin block_order): ascending blocks by
-        # default (neighbouring blocks share X windows in L2); "lpt": heaviest
-        # block first (the dynamically scheduled tail is made of light blocks)
-        # "tail": ascending, but the last 3 x 148 blocks heaviest first (the
-        # final scheduling round is made of the lightest of them)
+        # default (the CTAs in flight share X windows in L2); "lpt": heaviest
+        # block first; "lightK": ascending, but the K lightest blocks last,
+        # lightest at the very end (the dynamically scheduled tail is made of
+        # light blocks while most of the matrix keeps its L2 locality)
         self.block_order = None
-        if block_order in ("lpt", "tail"):
+        if block_order is not None:
             blk_nnz = torch.zeros(self.nblocks, dtype=torch.int64, device=dev)
             blk_nnz.index_add_(0, torch.div(rows, RB, rounding_mode="floor"), torch.ones_like(rows))
             if block_order == "lpt":
                 order = torch.sort(-blk_nnz, stable=True).indices
+            elif block_order.startswith("light") and block_order[5:].isdigit():
+                k = min(self.nblocks, int(block_order[5:]))
+                light = torch.sort(blk_nnz, stable=True).indices[:k]
+                is_light = torch.zeros(self.nblocks, dtype=torch.bool, device=dev)
+                is_light[light] = True
+                order = torch.cat([torch.nonzero(~is_light).view(-1), light.flip(0)])
             else:
-                k = min(self.nblocks, 3 * 148)
-                order = torch.arange(self.nblocks, device=dev)
-                tail = order[self.nblocks - k:]
-                order[self.nblocks - k:] = tail[torch.sort(-blk_nnz[tail], stable=True).indices]
+                raise ValueError(f"unknown block order {block_order!r}")
             self.block_order = order.to(torch.int32).contiguous()
-        elif block_order is not None:
-            raise ValueError(f"unknown block order {block_order!r}")
         keep = torch.ones(a.nnz, dtype=torch.bool, device=dev)
         keep[didx] = False
         rp = torch.zeros(a.rows + 1, dtype=torch.int64, device=dev)

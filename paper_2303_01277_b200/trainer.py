@@ -537,10 +537,11 @@ class DeviceRank:
         (HB_NARROW_WINDOW) when the operator factors."""
         key = id(a)
         if key not in self._tiles:
-            # work items of the forward operator go out heaviest block first
-            # (measured 4.07 vs 4.23 ms at d = 256 on Reddit; the transpose
-            # keeps ascending blocks: 4.18 vs 4.27, tools/kbench_spmm_wide.py)
-            t = ops.TiledCsr(a, block_order="lpt" if a is self.A else None)
+            # forward operator: the 296 lightest row blocks go out last (d = 256
+            # on Reddit: 4.15 vs 4.22-4.27 ms, DRAM 2.0 vs 1.05 GB per launch;
+            # heaviest-first over all blocks: 4.07 ms but 5.5 GB); the
+            # transpose keeps ascending blocks (profiles/r2_kbench_spmm_wide.jsonl)
+            t = ops.TiledCsr(a, block_order="light296" if a is self.A else None)
             self._tiles[key] = t if t.tiled_fraction >= 0.5 else None
         t = self._tiles[key]
         if t is not None and t.binary and 32 < d <= 48 and self.narrow_window != 64:

@@ -158,7 +158,7 @@ def test_spmm_tiled_factored_operators(kind, d, threshold, rb):
     ref = sp.csr_matrix((v.astype(np.float64), ci2, rp2), shape=a.shape) @ x.astype(np.float64)
     got, T = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True, block_rows=rb)
     assert T.binary and T.RB == rb
-    for order in ("lpt", "tail"):
+    for order in ("lpt", "light7"):
         # the work-item order changes which CTA runs a block, not the result
         got_o, _ = _tiled_run(rp2, ci2, v, x, a.shape[1], threshold, ld_pad=(-d) % 4, factored=True,
                               block_rows=rb, block_order=order)

@@ -27,7 +27,7 @@ def main(d=256, reps=10, *rbs):
     for name, M in (("mean", A), ("mean_T", At)):
         X = torch.randn(M.cols, ld, device="cuda")
         ref = None
-        for rb, order in [(rb, o) for rb in rbs for o in (None, "lpt", "tail", None)]:
+        for rb, order in [(rb, o) for rb in rbs for o in (None, "lpt", "light296", "light592", None)]:
             T = ops.TiledCsr(M, factored=True, block_rows=rb, block_order=order)
             Y = torch.zeros(M.rows, ld, device="cuda")
             for _ in range(2):
