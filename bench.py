@@ -299,6 +299,10 @@ def workload_config(args) -> dict:
             "bits": args.bits, "mode": args.mode, "staleness": args.staleness,
             "model": MODEL[args.config], "widths": list(WIDTHS[args.config]), "loss": LOSS[args.config],
             "scale": getattr(args, "scale", 1.0),
+            "exchange": ("in-GPU (all partitions on one GPU)" if args.gpus == 1 else
+                         "peer memory (CUDA IPC)" if getattr(args, "p2p", None) or (
+                             getattr(args, "p2p", None) is None and not getattr(args, "share_gpu", False)) else
+                         "gloo, host-staged" if getattr(args, "share_gpu", False) else "NCCL send/recv"),
             "l2": "n/a (CPU)" if args.impl == "reference" else None}
 
 
@@ -334,7 +338,7 @@ def run_b200(args):
     layout = RankLayout(parts, owner, rank)
     eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config], loss=LOSS[args.config]),
                      TrainMode(args.mode, args.staleness), QuantConfig(args.bits), args.seed, 0.01, gnorm,
-                     device=torch.device("cuda", local))
+                     device=torch.device("cuda", local), p2p=args.p2p)
     # the step's input features, pinned and laid out like the device buffer
     # (16-byte padded rows) so each step's upload is one contiguous copy
     feats = np.concatenate([np.asarray(p.features, dtype=np.float32) for p in layout.parts])
@@ -387,7 +391,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier()
     launches = eng.launches - launches0
-    halo_net = _halo_net(eng, world, args.steps)
+    halo_net = _halo_net(eng, world, args.steps, timer.summary())
     eng.comm_events = None
     eng.timer = KernelTimer()
     eng.timer.enabled = False
@@ -531,7 +535,7 @@ def run_b200(args):
         torch.cuda.empty_cache()
         eng = DeviceRank(layout, ModelConfig(WIDTHS[args.config], MODEL[args.config], loss=LOSS[args.config]),
                          TrainMode("async", 0), QuantConfig(args.bits), args.seed, 0.01, gnorm,
-                         device=torch.device("cuda", local))
+                         device=torch.device("cuda", local), p2p=args.p2p)
         aepoch = 0                       # a fresh run: epoch 1 has no stale buffers yet
         for _ in range(args.warmup):
             aepoch += 1
@@ -647,7 +651,9 @@ def run_b200(args):
                               "K1 writes each wire block straight into its receiver's buffer") if world == 1 else
                              ("rank 0's wire bytes; same-rank messages are written straight into the receiver's "
                               "buffer, the rest move per peer rank over " +
-                              ("gloo with host staging (--share-gpu: all ranks on one GPU)" if args.share_gpu
+                              ("peer memory: K1 writes them into the peers' receive buffers (CUDA IPC), "
+                               "counters order arrival and reuse" if eng.p2p is not None else
+                               "gloo with host staging (--share-gpu: all ranks on one GPU)" if args.share_gpu
                                else "NCCL send/recv on the comm stream"))},
             "gpu_launches": launches,
             "halo_network": halo_net,
@@ -689,10 +695,26 @@ def _working_set_bytes(eng) -> float:
     return float(act + csr)
 
 
-def _halo_net(eng, world: int, steps: int):
+def _halo_net(eng, world: int, steps: int, ksum=None):
     """Halo GB/s over the network leg (N>1): remote wire bytes / NCCL span,
-    both from the comm-stream events of the timed epochs."""
-    if world == 1 or not eng.comm_events:
+    both from the comm-stream events of the timed epochs.  With
+    the peer-memory exchange the transfer happens inside K1 (its stores land
+    in the peers' buffers): remote wire bytes / K1 time, a lower bound on the
+    link rate since K1 is bound by its Philox stream."""
+    if world == 1:
+        return None
+    if eng.p2p is not None:
+        nbytes = sum(n for b in eng.p2p.ex for _, (_, n) in b.send_group.items())
+        k1 = (ksum or {}).get("quantize_gather")
+        if not k1 or k1["ms"] <= 0:
+            return None
+        ms = _max_over_ranks(k1["ms"] / steps, world)
+        return {"transport": "peer memory (CUDA IPC, K1 stores into the peers' receive buffers)",
+                "wire_bytes_per_epoch": nbytes, "k1_ms_per_epoch": ms,
+                "halo_gbps": nbytes / ms / 1e6 if ms > 0 else None, "nvlink_peak_gbps": 900.0,
+                "frac": (nbytes / ms / 1e6) / 900.0 if ms > 0 else None,
+                "note": "this rank's remote wire bytes / its K1 time (the link leg overlaps the quantize)"}
+    if not eng.comm_events:
         return None
     ms = sum(a.elapsed_time(b) for a, b, _ in eng.comm_events)
     nbytes = sum(n for _, _, n in eng.comm_events)
@@ -750,6 +772,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-async-line", action="store_true", help="skip the Sylvie-A sub-line")
     ap.add_argument("--no-graphs", action="store_true", help="eager epochs only (no CUDA-graph replays)")
+    ap.add_argument("--p2p", dest="p2p", action="store_true", default=None,
+                    help="N>1: peer-memory halo exchange (K1 writes into the peers' receive buffers over "
+                         "CUDA IPC mappings; the default on NCCL process groups)")
+    ap.add_argument("--nccl-exchange", dest="p2p", action="store_false",
+                    help="N>1: halo blocks over NCCL send/recv instead of peer memory")
     ap.add_argument("--e2e-serial", action="store_true",
                     help="e2e with the serial upload only (no double-buffered input pipeline)")
     ap.add_argument("--partitions", type=int, default=None,

@@ -273,6 +273,31 @@ int hb_adam_step_dev(float* w, const float* g, float* m, float* v, int64_t n, fl
                      float b2, float eps, const double* bc, const double* loss, const uint32_t* flags,
                      const uint32_t* flags2, void* stream);
 
+/* ---- peer-memory halo exchange (N > 1, one process per GPU) ---------------
+ * Replaces the NCCL send/recv of `exchange` (transport.py:172-205): every
+ * rank's receive buffers are exported once as CUDA IPC handles and mapped by
+ * the other ranks, K1 writes remote messages straight into the receiver's
+ * buffer over NVLink, and 64-bit counters order arrival and reuse.
+ *
+ * hb_ipc_get_handle: the 64-byte cudaIpcMemHandle of the allocation holding
+ * ptr, and ptr's byte offset in it.  hb_ipc_open_handle / hb_ipc_close: map /
+ * unmap a peer's allocation (base address; add the offset). */
+int hb_ipc_get_handle(const void* ptr, void* handle, int64_t* offset);
+int hb_ipc_open_handle(const void* handle, void** base);
+int hb_ipc_close(void* base);
+
+/* Stream-ordered: after the work queued before it, atomically add 1 to each
+ * of the n counters (device array of n pointers, peer-mapped addresses
+ * allowed) with system-scope release semantics. */
+int hb_p2p_signal(uint64_t* const* counters, int32_t n, void* stream);
+
+/* Stream-ordered: block the stream until *counter >= target (system-scope
+ * acquire).  After timeout_ns the wait gives up and ORs flag_bit into *flags
+ * (nullable) — a stalled or diverged peer surfaces as an error at the next
+ * host check instead of a hung GPU. */
+int hb_p2p_wait(const uint64_t* counter, uint64_t target, uint32_t* flags, uint32_t flag_bit, uint64_t timeout_ns,
+                void* stream);
+
 /* Argmax accuracy counts for evaluate() (trainer.py:129-144):
  * counts[2*k] = #rows with mask==k+1, counts[2*k+1] = #correct among them, k=0..2. */
 int hb_argmax_accuracy(const float* logits, int64_t ld, int32_t n, int32_t C, const int32_t* labels,

@@ -8,7 +8,7 @@ every device entry point raises.  The library is built in-tree by
 from __future__ import annotations
 
 import ctypes
-from ctypes import c_double, c_float, c_int32, c_int64, c_uint64, c_void_p
+from ctypes import c_double, c_float, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 from pathlib import Path
 
 import numpy as np
@@ -27,7 +27,8 @@ assert SEGMENT_DTYPE.itemsize == 40
 EXPORTS = (
     "hb_version", "hb_last_error", "hb_philox_uniforms", "hb_quantize_gather",
     "hb_dequant_gather", "hb_spmm_csr", "hb_spmm_csr_ex", "hb_spmm_tiled", "hb_spmm_tiled_bin", "hb_gemm_f32", "hb_gemm2_f32", "hb_gemm_set_path", "hb_spmm_set_narrow", "hb_softmax_xent", "hb_relu", "hb_relu_grad_mul",
-    "hb_adam_step", "hb_adam_step_guarded", "hb_adam_step_dev", "hb_upload_async", "hb_argmax_accuracy", "hb_dropout", "hb_sigmoid_bce", "hb_multilabel_counts",
+    "hb_adam_step", "hb_adam_step_guarded", "hb_adam_step_dev", "hb_upload_async", "hb_ipc_get_handle", "hb_ipc_open_handle",
+    "hb_ipc_close", "hb_p2p_signal", "hb_p2p_wait", "hb_argmax_accuracy", "hb_dropout", "hb_sigmoid_bce", "hb_multilabel_counts",
 )
 
 P = c_void_p
@@ -55,6 +56,11 @@ _SIGS = {
     "hb_adam_step_guarded": [P, P, P, P, c_int64, c_float, c_float, c_float, c_float, c_double, c_double, P, P, P,
                              P],
     "hb_upload_async": [P, P, c_int64, P],
+    "hb_ipc_get_handle": [P, P, P],
+    "hb_ipc_open_handle": [P, P],
+    "hb_ipc_close": [P],
+    "hb_p2p_signal": [P, c_int32, P],
+    "hb_p2p_wait": [P, c_uint64, P, c_uint32, c_uint64, P],
     "hb_adam_step_dev": [P, P, P, P, c_int64, c_float, c_float, c_float, c_float, P, P, P, P, P],
     "hb_argmax_accuracy": [P, c_int64, c_int32, c_int32, P, P, P, P],
     "hb_dropout": [P, c_int64, c_int32, c_int64, c_int32, c_uint64, c_uint64, c_float, P, c_int64, P],

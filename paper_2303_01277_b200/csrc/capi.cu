@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include "common.cuh"
 
@@ -45,6 +46,11 @@ cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*,
                                   const uint8_t*, const int64_t*, const int32_t*, const float*, const float*,
                                   const float*, int64_t, int, float*, int64_t, float*, int64_t, int*, int, int,
                                   const int32_t*, cudaStream_t);
+
+cudaError_t launch_p2p_signal(unsigned long long* const*, int, cudaStream_t);
+cudaError_t launch_p2p_wait(const unsigned long long*, unsigned long long, uint32_t*, uint32_t, unsigned long long,
+                            cudaStream_t);
+cudaError_t alloc_base(const void*, void**);
 
 int num_sms() {
   static int cached = 0;
@@ -303,6 +309,45 @@ int hb_dropout(const float* x, int64_t ldx, int32_t nrows, int64_t row0, int32_t
                float p, float* out, int64_t ldo, void* stream) {
   if (nrows < 0 || d < 0 || row0 < 0 || !(p >= 0.f && p < 1.f)) return fail(HB_EINVAL, "hb_dropout: bad arguments");
   return check(hb::launch_dropout(x, ldx, nrows, row0, d, key0, key1, p, out, ldo, S(stream)), "hb_dropout");
+}
+
+int hb_ipc_get_handle(const void* ptr, void* handle, int64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(HB_EINVAL, "hb_ipc_get_handle: bad arguments");
+  void* base = nullptr;
+  cudaError_t e = hb::alloc_base(ptr, &base);
+  if (e != cudaSuccess) return check(e, "hb_ipc_get_handle (allocation base)");
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, base);
+  if (e != cudaSuccess) return check(e, "hb_ipc_get_handle");
+  memcpy(handle, &h, sizeof(h));
+  *offset = static_cast<const char*>(ptr) - static_cast<const char*>(base);
+  return HB_OK;
+}
+
+int hb_ipc_open_handle(const void* handle, void** base) {
+  if (!handle || !base) return fail(HB_EINVAL, "hb_ipc_open_handle: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return check(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess), "hb_ipc_open_handle");
+}
+
+int hb_ipc_close(void* base) {
+  if (!base) return fail(HB_EINVAL, "hb_ipc_close: bad arguments");
+  return check(cudaIpcCloseMemHandle(base), "hb_ipc_close");
+}
+
+int hb_p2p_signal(uint64_t* const* counters, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && !counters)) return fail(HB_EINVAL, "hb_p2p_signal: bad arguments");
+  return check(hb::launch_p2p_signal(reinterpret_cast<unsigned long long* const*>(counters), n, S(stream)),
+               "hb_p2p_signal");
+}
+
+int hb_p2p_wait(const uint64_t* counter, uint64_t target, uint32_t* flags, uint32_t flag_bit, uint64_t timeout_ns,
+                void* stream) {
+  if (!counter) return fail(HB_EINVAL, "hb_p2p_wait: bad arguments");
+  return check(hb::launch_p2p_wait(reinterpret_cast<const unsigned long long*>(counter), target, flags, flag_bit,
+                                   timeout_ns, S(stream)),
+               "hb_p2p_wait");
 }
 
 }  // extern "C"

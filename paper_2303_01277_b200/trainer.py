@@ -219,7 +219,7 @@ class DeviceRank:
 
     def __init__(self, layout: RankLayout, cfg: ModelConfig, mode: TrainMode, quant: QuantConfig,
                  seed: int, lr: float, global_norm: int, device=None, group=None, probe=None,
-                 features=None, agg_order=None, timeout: float = 60.0):
+                 features=None, agg_order=None, timeout: float = 60.0, p2p: bool | None = None):
         import torch
         self.torch = torch
         self.dev = torch.device(device or "cuda")
@@ -342,6 +342,22 @@ class DeviceRank:
         self.xb = {l: ExchangeBuffers(layout, layout.bwd, W[l - 1], quant.bits, dev, par)
                    for l in range(2, L + 1)}
         self.xeval = None
+        # peer-memory halo exchange (K1 writes into the peers' receive buffers;
+        # transport.PeerLinks) instead of NCCL send/recv: the default for N > 1
+        # on an NCCL process group (one node, NVLink); HB_P2P=0/1 overrides,
+        # gloo groups (host-staged test runs) use it only when asked
+        if p2p is None:
+            env = os.environ.get("HB_P2P")
+            if env is not None:
+                p2p = env == "1"
+            else:
+                from .transport import host_staged
+                p2p = self.world > 1 and not host_staged(group)
+        self.p2p = None
+        if p2p and self.world > 1:
+            from .transport import PeerLinks
+            self.p2p = PeerLinks(list(self.xf.values()) + list(self.xb.values()), group, dev, self.timeout,
+                                 parities=par)
         self.slots = {}
         self.stats = {p: TransportStats() for p in layout.ids}
         self.epoch_loss = 0.0
@@ -367,6 +383,9 @@ class DeviceRank:
         # the comm stream (Sylvie-A, or a drained slot at an adaptor-sync
         # epoch) must have left it first
         self._wait_comm(bufs)
+        p2p = self.p2p if self.p2p is not None and id(bufs) in self.p2p.index else None
+        if p2p is not None:
+            p2p.before_send(bufs, parity, self.proto_flags)     # the peers no longer read what K1 overwrites
         if bufs.n_send:
             segs = bufs.upload_send_table(self.seed, epoch, layer, parity)
             R = int(bufs.plan.send_rows.size)
@@ -377,7 +396,9 @@ class DeviceRank:
             self.launches += 1
             if self.probe and count:      # the evaluation forward is centralized in the reference: no events
                 self._probe_out(bufs, epoch, layer)
-        if self.world > 1:
+        if p2p is not None:
+            p2p.after_send(bufs, parity)                         # the blocks are in the peers' buffers
+        elif self.world > 1:
             ev = torch.cuda.current_stream().record_event()
             with torch.cuda.stream(self.comm_stream):
                 self.comm_stream.wait_event(ev)
@@ -409,9 +430,14 @@ class DeviceRank:
 
     def _recv(self, bufs: ExchangeBuffers, parity: int, dst, accumulate: bool):
         """K2: forward scatter into halo rows / backward ascending-peer integration."""
+        p2p = self.p2p if self.p2p is not None and id(bufs) in self.p2p.index else None
         if bufs.n_recv == 0:
+            if p2p is not None:
+                p2p.after_recv(bufs, parity)
             return
         self._wait_comm(bufs, parity)
+        if p2p is not None:
+            p2p.before_recv(bufs, parity, self.proto_flags)
         pd = bufs.plan.dev
         nd, ns = int(bufs.plan.dst_rows.size), int(bufs.plan.src_rows.size)
         nbytes = bufs.wire_bytes_total() + nd * bufs.d * 4 * (2 if accumulate else 1) + 4 * (2 * nd + ns)
@@ -419,6 +445,8 @@ class DeviceRank:
             dequant_gather(bufs.recv_segs[parity], bufs.n_recv, pd["dst_rows"], pd["src_ptr"],
                            pd["src_rows"], bufs.d, bufs.bits, dst, accumulate)
         self.launches += 1
+        if p2p is not None:
+            p2p.after_recv(bufs, parity)                         # the senders may overwrite it now
 
     def _probe_out(self, bufs, epoch, layer):
         for m in bufs.plan.send_msgs:

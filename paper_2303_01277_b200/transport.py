@@ -33,6 +33,7 @@ B200 design:
 
 from __future__ import annotations
 
+import ctypes
 import threading
 from dataclasses import dataclass
 
@@ -268,6 +269,9 @@ class ExchangeBuffers:
         self._seg_ev = [None, None]
         self._seg_slot = 0
         self.capture = None                    # an EpochGraph while one is being captured
+        # peer-memory exchange (PeerLinks): receiving rank's mapped receive
+        # buffer base per (rank, parity), message offsets on the receiver
+        self.peer_recv, self.peer_off = None, None
 
     def send_table(self, seed: int, epoch: int, layer: int, parity: int) -> np.ndarray:
         """hb_segment_t rows for this exchange (keys depend on the epoch)."""
@@ -278,8 +282,12 @@ class ExchangeBuffers:
             if m.src not in keys:
                 keys[m.src] = derive_key((seed, m.src, epoch, layer, self.plan.phase)) \
                     if self.bits != 32 else (0, 0)
-            if self.layout.owner[m.dst] == me:
+            r = self.layout.owner[m.dst]
+            if r == me:
                 out = self.recv[parity].data_ptr() + self.recv_off[(m.src, m.dst)]
+            elif self.peer_recv is not None:
+                # peer-memory exchange: straight into the receiving rank's buffer
+                out = self.peer_recv[(r, parity)] + self.peer_off[(m.src, m.dst)]
             else:
                 out = self.send.data_ptr() + self.send_off[(m.src, m.dst)]
             k = keys[m.src]
@@ -340,6 +348,134 @@ def host_staged(group=None) -> bool:
     over NVLink)."""
     import torch.distributed as dist
     return dist.get_backend(group) != "nccl"
+
+
+class PeerLinks:
+    """Peer-memory halo exchange (``hb_p2p_*``, N > 1 with one process per GPU).
+
+    Replaces the NCCL send/recv of ``nccl_exchange`` for the halo blocks (the
+    reference's ``exchange``, transport.py:172-205): every rank exports its
+    receive buffers once as CUDA IPC handles; the other ranks map them, and
+    K1 writes each remote message's wire block straight into the receiver's
+    buffer (NVLink / NVSwitch peer stores) — the transfer happens inside the
+    quantize kernel.  Arrival and buffer reuse are ordered by monotonically
+    increasing 64-bit counters, one block per rank: ``cnt[e, p, 0]`` counts
+    arrivals into this rank's receive buffer of exchange e, parity p;
+    ``cnt[e, p, 1 + r]`` counts receiver r's consumptions of what this rank
+    wrote there.  All ranks run the same exchange schedule, so a rank derives
+    every target from its own history:
+
+    * before K1 (use n of (e, p)): wait until each remote receiver r has
+      consumed (e, p) as often as this rank has (``cnt[e, p, 1 + r] >=
+      own consumptions``) — the data about to be overwritten is no longer
+      read, Sylvie-A re-reads included;
+    * after K1: +1 on each remote receiver's ``cnt[e, p, 0]``;
+    * before K2: wait until ``cnt[e, p, 0] >= own sends into (e, p) x remote
+      senders`` — the latest blocks have all arrived;
+    * after K2: +1 on each remote sender's ``cnt[e, p, 1 + me]``.
+
+    A wait that times out sets FLAG_PROTOCOL in the rank's device flag word."""
+
+    def __init__(self, exchanges: list, group, device, timeout: float, parities: int = 2):
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        self.ex = list(exchanges)
+        self.index = {id(b): i for i, b in enumerate(self.ex)}
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.timeout_ns = int(timeout * 1e9)
+        E, P, W = len(self.ex), parities, self.world
+        self.cnt = torch.zeros((E, P, 1 + W), dtype=torch.int64, device=device)
+        self.sends = np.zeros((E, P), dtype=np.int64)
+        self.consumes = np.zeros((E, P), dtype=np.int64)
+        me = self.rank
+
+        def export(t):
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _lib.call("hb_ipc_get_handle", t.data_ptr(), h, ctypes.byref(off))
+            return bytes(h), int(off.value)
+        mine = {"cnt": export(self.cnt),
+                "recv": [[export(b.recv[p]) for p in range(len(b.recv))] for b in self.ex],
+                "recv_off": [dict(b.recv_off) for b in self.ex]}
+        allr = [None] * W
+        dist.all_gather_object(allr, mine, group=group)
+        self.opened = []
+
+        def open_(h):
+            base = ctypes.c_void_p()
+            _lib.call("hb_ipc_open_handle", h[0], ctypes.byref(base))
+            self.opened.append(base.value)
+            return base.value + h[1]
+        cnt_addr = {r: (self.cnt.data_ptr() if r == me else open_(allr[r]["cnt"])) for r in range(W)}
+        stride = self.cnt.stride()
+        el = self.cnt.element_size()
+
+        def caddr(r, e, p, k):
+            return cnt_addr[r] + el * (e * stride[0] + p * stride[1] + k * stride[2])
+        self.send_ranks, self.recv_ranks = [], []
+        sig_send, sig_recv = [], []
+        for e, b in enumerate(self.ex):
+            sr = sorted(b.send_group)                       # remote ranks this rank writes to
+            rr = sorted(r for r in b.recv_group if r != me)  # remote ranks writing here
+            self.send_ranks.append(sr)
+            self.recv_ranks.append(rr)
+            b.peer_recv = {(r, p): open_(allr[r]["recv"][e][p]) for r in sr for p in range(len(b.recv))}
+            b.peer_off = {}
+            for r in sr:
+                b.peer_off.update({k: v for k, v in allr[r]["recv_off"][e].items()})
+            sig_send.append([[caddr(r, e, p, 0) for r in sr] for p in range(P)])
+            sig_recv.append([[caddr(r, e, p, 1 + me) for r in rr] for p in range(P)])
+        # device arrays of counter addresses for hb_p2p_signal, per (e, p)
+        self._sig = {}
+        for e in range(E):
+            for p in range(P):
+                for kind, lst in (("send", sig_send[e][p]), ("recv", sig_recv[e][p])):
+                    if lst:
+                        self._sig[(kind, e, p)] = torch.tensor(lst, dtype=torch.int64, device=device)
+
+    def _wait(self, e, p, k, target, flags, stream):
+        if target <= 0:
+            return
+        addr = self.cnt.data_ptr() + self.cnt.element_size() * (
+            e * self.cnt.stride(0) + p * self.cnt.stride(1) + k * self.cnt.stride(2))
+        _lib.call("hb_p2p_wait", addr, int(target), _lib.ptr(flags), FLAG_PROTOCOL, self.timeout_ns,
+                  _lib.stream_handle(stream))
+
+    def _signal(self, kind, e, p, stream):
+        a = self._sig.get((kind, e, p))
+        if a is not None:
+            _lib.call("hb_p2p_signal", a.data_ptr(), a.numel(), _lib.stream_handle(stream))
+
+    def before_send(self, bufs, parity, flags, stream=None):
+        """Before K1 writes into the peers' (e, parity) buffers."""
+        e = self.index[id(bufs)]
+        for r in self.send_ranks[e]:
+            self._wait(e, parity, 1 + r, self.consumes[e, parity], flags, stream)
+
+    def after_send(self, bufs, parity, stream=None):
+        e = self.index[id(bufs)]
+        self.sends[e, parity] += 1
+        self._signal("send", e, parity, stream)
+
+    def before_recv(self, bufs, parity, flags, stream=None):
+        """Before K2 reads the (e, parity) receive buffer."""
+        e = self.index[id(bufs)]
+        self._wait(e, parity, 0, self.sends[e, parity] * len(self.recv_ranks[e]), flags, stream)
+
+    def after_recv(self, bufs, parity, stream=None):
+        e = self.index[id(bufs)]
+        self.consumes[e, parity] += 1
+        self._signal("recv", e, parity, stream)
+
+    def close(self):
+        for base in self.opened:
+            try:
+                _lib.call("hb_ipc_close", base)
+            except Exception:
+                pass
+        self.opened = []
 
 
 ENVELOPE_MAGIC = int.from_bytes(b"HBM1", "little")

@@ -7,6 +7,13 @@ remote messages into the send buffer and local ones straight into the
 receiver's slot, the per-peer-rank send/recv groups, comm-stream ordering and
 Sylvie-A deferral, the gradient/loss all-reduce — is the production N>1 code.
 
+The same runs with the peer-memory exchange (``DeviceRank(p2p=True)``,
+``transport.PeerLinks``): each rank maps the other's receive buffers through
+CUDA IPC handles, K1 writes the remote wire blocks straight into them, and
+the arrival / reuse counters order K1 and K2 across the two processes — must
+train bit-identically to the host-staged exchange (same blocks, same K2
+inputs).
+
 Checks against the single-process run of the same 4 partitions:
 * passthrough (bits 32): global losses every epoch rel 1e-5 and final weights
   max-abs/max 1e-5 (fp32 summation order of the all-reduce differs), sync and
@@ -45,14 +52,15 @@ def _setup():
     return g, build_partitions(g, 4, "hash", 0, "sage")[2]
 
 
-def _run(rank, world, owner, variant, st, bits):
+def _run(rank, world, owner, variant, st, bits, p2p=False):
     from paper_2303_01277_b200.codec import QuantConfig
     from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
     from paper_2303_01277_b200.transport import RankLayout
     g, parts = _setup()
     lay = RankLayout({p.id: p for p in parts if owner[p.id] == rank}, owner, rank)
     eng = DeviceRank(lay, ModelConfig((32, 16, 8), "sage"), TrainMode(variant, st), QuantConfig(bits), 3, 0.01,
-                     int(g.train_mask.sum()), device="cuda:0")
+                     int(g.train_mask.sum()), device="cuda:0", p2p=p2p)
+    assert (eng.p2p is not None) == (p2p and world > 1)
     losses, meters = [], []
     prev = eng.total_stats()
     for e in range(1, EPOCHS + 1):
@@ -73,6 +81,7 @@ def _worker(rank, world, port, q):
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         out = {c: _run(rank, world, [0, 1, 1, 0], *c) for c in CASES}
+        out.update({("p2p",) + c: _run(rank, world, [0, 1, 1, 0], *c, p2p=True) for c in CASES})
         q.put((rank, "ok", out))
     except Exception:
         q.put((rank, "fail", traceback.format_exc()))
@@ -111,3 +120,26 @@ def test_two_ranks_on_one_gpu_match_single_rank():
             assert max(np.abs(a - b).max() for a, b in zip(w0, single[2])) / scale < 1e-5, case
         else:
             assert l0[0] == pytest.approx(single[0][0], rel=1e-6)
+        # the peer-memory exchange moves the same blocks: bit-identical training
+        lp, mp_, wp = res[0][("p2p",) + case]
+        assert lp == l0 and mp_ == m0, case
+        for a, b in zip(wp, w0):
+            np.testing.assert_array_equal(a, b)
+        assert res[1][("p2p",) + case][0] == l1
+
+
+def test_p2p_counter_kernels():
+    """hb_p2p_signal adds 1 (system-scope release) to every counter of its
+    address list; hb_p2p_wait returns once the counter reaches the target and
+    gives up after its timeout with the flag bit set instead of hanging."""
+    from paper_2303_01277_b200 import _lib
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    addrs = torch.tensor([cnt.data_ptr() + 8 * i for i in (0, 2, 2)], dtype=torch.int64, device="cuda")
+    _lib.call("hb_p2p_signal", addrs.data_ptr(), 3, _lib.stream_handle())
+    _lib.call("hb_p2p_wait", cnt.data_ptr() + 16, 2, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
+    torch.cuda.synchronize()
+    assert cnt.tolist() == [1, 0, 2, 0] and int(flags) == 0
+    _lib.call("hb_p2p_wait", cnt.data_ptr() + 8, 1, flags.data_ptr(), 2, 2 * 10**6, _lib.stream_handle())
+    torch.cuda.synchronize()
+    assert int(flags) == 2
