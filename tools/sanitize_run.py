@@ -1,7 +1,10 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck):
 a few epochs of each model on a small graph (K1, K2, both SpMM kernels,
-tcgen05 GEMMs, K8) plus wide and narrow tiled SpMM, the row-parallel gather,
-dual / ReLU-only tall GEMMs and a split-K weight-gradient GEMM."""
+tcgen05 GEMMs, K8), CUDA-graph epochs (the pinned-buffer fetch kernel, the
+device-guarded Adam), plus wide and narrow tiled SpMM (general records, and
+factored one-byte records: 120-row blocks, 255-column windows with balanced
+tail pairs), the row-parallel gather, dual / ReLU-only tall GEMMs, a split-K
+weight-gradient GEMM and the peer-exchange counter kernels."""
 import sys
 from pathlib import Path
 
@@ -25,7 +28,18 @@ def main():
                          int(g.train_mask.sum()))
         for e in range(1, 4):
             eng.run_epoch(e)
-        T = ops.TiledCsr(eng.A, threshold=1)
+        geng = DeviceRank(lay, ModelConfig((40, 24, 6), model), TrainMode("sync", 0), QuantConfig(bits), 1, 0.01,
+                          int(g.train_mask.sum()))
+        for e in range(1, 6):
+            geng.run_epoch_graphed(e)
+        while geng._deferred:
+            geng.finish_epoch()
+        for kw in (dict(factored=True), dict(factored=True, block_rows=64, window=255)):
+            Tb = ops.TiledCsr(eng.A, threshold=1, **kw)
+            Xb = torch.randn(eng.A.cols, 256, device="cuda")
+            Yb = torch.zeros(eng.A.rows, 256, device="cuda")
+            ops.spmm_tiled(Tb, Xb, Yb, 256 if kw.get("window", 64) == 64 else 41)
+        T = ops.TiledCsr(eng.A, threshold=1, factored=False)
         X = torch.randn(eng.A.cols, 256, device="cuda")
         Y = torch.zeros(eng.A.rows, 256, device="cuda")
         ops.spmm_tiled(T, X, Y, 256)
@@ -46,6 +60,12 @@ def main():
     G = torch.empty(300, 64, device="cuda")
     ws = torch.empty(64 * 300 * 64, device="cuda")
     ops.gemm(A.t(), m, G, ws=ws)
+    from paper_2303_01277_b200 import _lib
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    addrs = torch.tensor([cnt.data_ptr(), cnt.data_ptr() + 8], dtype=torch.int64, device="cuda")
+    _lib.call("hb_p2p_signal", addrs.data_ptr(), 2, _lib.stream_handle())
+    _lib.call("hb_p2p_wait", cnt.data_ptr(), 1, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
     torch.cuda.synchronize()
     print("sanitize workload done")
 
