@@ -188,9 +188,8 @@ int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1
 /* Selects the K5-K7 kernel: 0 = TMA-fed warp-specialised tcgen05 kernel
  * whenever both operands are TMA-describable (16-byte aligned, unit stride on
  * one axis, 16-byte row stride), else the SIMT-staged tcgen05 kernel;
- * 1 = SIMT-staged kernel only; 2 = as 0 but 128 < N <= 256 runs on CTA
- * pairs (tcgen05.mma.cta_group::2, 256-row tiles, half of B per SM);
- * 3 = the A-in-TMEM kernel for every shape (A split into tf32 hi/lo in
+ * 1 = SIMT-staged kernel only (2 is not a path: the CTA-pair kernel
+ * measured no faster and was removed); 3 = the A-in-TMEM kernel for every shape (A split into tf32 hi/lo in
  * registers and stored with tcgen05.st, MMAs take A from TMEM).  Under 0 the
  * A-in-TMEM kernel already runs tall GEMMs (>= 148 output tiles). */
 int hb_gemm_set_path(int32_t path);

@@ -37,7 +37,6 @@ cudaError_t launch_gemm2_tf32x3(int, int, int, const float*, int64_t, int64_t, c
                                 float*, int64_t, float*, int64_t, cudaStream_t);
 extern int g_gemm_path;
 extern int g_bin_narrow;
-extern int g_gemm_pair;
 extern int g_gemm_ts;
 cudaError_t launch_spmm_tiled(int, int, int, const int32_t*, const int32_t*, const int64_t*, const uint16_t*,
                               const int2*, const int64_t*, const int32_t*, const float*, const float*, int64_t, int,
@@ -193,10 +192,9 @@ int hb_gemm2_f32(int32_t M, int32_t N, int32_t K1, const float* A1, int64_t lda1
 }
 
 int hb_gemm_set_path(int32_t path) {
-  if (path < 0 || path > 3)
-    return fail(HB_EINVAL, "hb_gemm_set_path: path must be 0 (auto), 1 (SIMT-staged), 2 (CTA pair) or 3 (A in TMEM)");
+  if (path < 0 || path > 3 || path == 2)
+    return fail(HB_EINVAL, "hb_gemm_set_path: path must be 0 (auto), 1 (SIMT-staged) or 3 (A in TMEM)");
   hb::g_gemm_path = path == 1 ? 1 : 0;
-  hb::g_gemm_pair = path == 2 ? 1 : 0;
   hb::g_gemm_ts = path == 3 ? 1 : 0;
   return HB_OK;
 }

@@ -295,7 +295,6 @@ cudaError_t launch_gemm_tma(int, int, int, const float*, int64_t, int64_t, const
                             int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
 
 int g_gemm_path = 0;   // 0: TMA warp-specialised kernel when operands allow; 1: SIMT-staged kernel only
-int g_gemm_pair = 0;   // 1: use the CTA-pair (cta_group::2) kernel for 128 < N <= 256
 int g_gemm_ts = 0;     // 1: A split into TMEM (tcgen05.mma A-from-TMEM) kernel
 
 cudaError_t launch_gemm_ts(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
@@ -335,8 +334,8 @@ cudaError_t launch_gemm2_tf32x3(int M, int N, int K1, const float* A1, int64_t l
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (K1 <= 0 || K2 <= 0) return cudaErrorInvalidValue;
   static const bool no_dual = getenv("HB_GEMM_NO_DUAL") != nullptr;
-  if (C == nullptr && (no_dual || g_gemm_path != 0 || g_gemm_pair)) return cudaErrorNotSupported;
-  if (!no_dual && g_gemm_path == 0 && !g_gemm_pair) {
+  if (C == nullptr && (no_dual || g_gemm_path != 0)) return cudaErrorNotSupported;
+  if (!no_dual && g_gemm_path == 0) {
     const cudaError_t e = launch_gemm_ts_dual(M, N, K1, A1, lda1_m, lda1_k, B1, ldb1_k, ldb1_n, K2, A2, lda2_m,
                                               lda2_k, B2, ldb2_k, ldb2_n, C, ldc, beta, relu_out, ldr, ws, ws_floats,
                                               st);

@@ -511,7 +511,7 @@ static cudaError_t launch_bn(int M, int N, int K, const float* A, int64_t lda_m,
 
 }  // namespace gt
 
-// host helpers shared with the CTA-pair kernel (gemm_tma2.cu)
+// host helpers shared with the A-in-TMEM kernels (gemm_ts.cu)
 bool gemm_make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld, int box_outer,
                    bool mn_major) {
   return gt::make_map(m, base, inner, outer, ld, box_outer, mn_major);
@@ -536,9 +536,6 @@ cudaError_t gemm_splitk_reduce(const float* ws, int splits, int M, int N, float*
   gt::splitk_reduce2_kernel<<<g, 256, 0, st>>>(ws, splits, M, N, C, ldc, beta, relu_out, ldr);
   return cudaGetLastError();
 }
-cudaError_t launch_gemm_tma_pair(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t,
-                                 float*, int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t);
-extern int g_gemm_pair;
 extern int g_gemm_ts;
 extern int g_gemm_path;
 cudaError_t launch_gemm_ts(int, int, int, const float*, int64_t, int64_t, const float*, int64_t, int64_t, float*,
@@ -552,14 +549,12 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
                             int64_t ldb_k, int64_t ldb_n, float* C, int64_t ldc, float beta, float* relu_out,
                             int64_t ldr, float* ws, int64_t ws_floats, cudaStream_t st) {
   if (!gt::tma_ok(A, lda_m, lda_k) || !gt::tma_ok(B, ldb_n, ldb_k)) return cudaErrorNotSupported;
-  // CTA-pair (cta_group::2) variant: opt-in — it halves the B bytes per SM but
-  // measured no faster than the single-CTA kernel on the trainer's shapes
   // A-in-TMEM kernel: default for tall GEMMs (many 128-row tiles, no split-K);
   // the long-K weight gradients (split-K) stay on the all-smem kernel, which
   // measured faster there
   static const int ts_env = getenv("HB_GEMM_TS") ? atoi(getenv("HB_GEMM_TS")) : -1;
   const bool tall = (int64_t)((M + 127) / 128) * ((N + 127) / 128) >= num_sms();
-  const bool use_ts = ts_env >= 0 ? ts_env == 1 : (g_gemm_ts || (g_gemm_path == 0 && !g_gemm_pair && tall));
+  const bool use_ts = ts_env >= 0 ? ts_env == 1 : (g_gemm_ts || (g_gemm_path == 0 && tall));
   if (use_ts) {
     const cudaError_t e = launch_gemm_ts(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                          ws_floats, st);
@@ -569,16 +564,10 @@ cudaError_t launch_gemm_tma(int M, int N, int K, const float* A, int64_t lda_m, 
   // decoupled A / B rings
   static const int dw_env = getenv("HB_GEMM_DW") ? atoi(getenv("HB_GEMM_DW")) : 1;
   const int tiles128 = ((M + 127) / 128) * ((N + 127) / 128);
-  if (dw_env && g_gemm_path == 0 && !g_gemm_pair && !g_gemm_ts && ws != nullptr && tiles128 < num_sms() &&
+  if (dw_env && g_gemm_path == 0 && !g_gemm_ts && ws != nullptr && tiles128 < num_sms() &&
       (K + 31) / 32 >= 8) {
     const cudaError_t e = launch_gemm_dw(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out, ldr, ws,
                                          ws_floats, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
-  static const bool pair = getenv("HB_GEMM_PAIR") != nullptr;
-  if ((pair || g_gemm_pair) && N > 128 && N <= 256) {
-    const cudaError_t e = launch_gemm_tma_pair(M, N, K, A, lda_m, lda_k, B, ldb_k, ldb_n, C, ldc, beta, relu_out,
-                                               ldr, ws, ws_floats, st);
     if (e != cudaErrorNotSupported) return e;
   }
   static const int max_bn = getenv("HB_GEMM_BN") ? atoi(getenv("HB_GEMM_BN")) : 256;

@@ -334,8 +334,8 @@ def spmm_set_narrow(variant: int):
 
 
 def gemm_set_path(path: int):
-    """0: TMA warp-specialised tcgen05 kernel where operands allow; 1: SIMT-staged kernel;
-    2: as 0 with CTA pairs (cta_group::2) for 128 < N <= 256."""
+    """0: TMA warp-specialised tcgen05 kernels where operands allow; 1: SIMT-staged kernel;
+    3: the A-in-TMEM kernel for every shape."""
     _lib.call("hb_gemm_set_path", int(path))
 
 
