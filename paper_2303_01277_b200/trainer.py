@@ -356,8 +356,16 @@ class DeviceRank:
         self.p2p = None
         if p2p and self.world > 1:
             from .transport import PeerLinks
-            self.p2p = PeerLinks(list(self.xf.values()) + list(self.xb.values()), group, dev, self.timeout,
-                                 parities=par)
+            try:
+                self.p2p = PeerLinks(list(self.xf.values()) + list(self.xb.values()), group, dev, self.timeout,
+                                     parities=par)
+            except Exception as exc:         # e.g. no CUDA IPC between these processes
+                if os.environ.get("HB_P2P") == "1":
+                    raise
+                import warnings
+                warnings.warn(f"peer-memory halo exchange unavailable ({exc}); using NCCL send/recv")
+                for b in list(self.xf.values()) + list(self.xb.values()):
+                    b.peer_recv, b.peer_off = None, None
         self.slots = {}
         self.stats = {p: TransportStats() for p in layout.ids}
         self.epoch_loss = 0.0
