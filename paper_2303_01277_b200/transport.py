@@ -396,18 +396,48 @@ class PeerLinks:
             off = ctypes.c_int64()
             _lib.call("hb_ipc_get_handle", t.data_ptr(), h, ctypes.byref(off))
             return bytes(h), int(off.value)
-        mine = {"cnt": export(self.cnt),
-                "recv": [[export(b.recv[p]) for p in range(len(b.recv))] for b in self.ex],
-                "recv_off": [dict(b.recv_off) for b in self.ex]}
+        # every rank takes part in each collective whatever happens locally, so
+        # a failure anywhere makes all ranks fall back together
+        try:
+            mine = {"cnt": export(self.cnt),
+                    "recv": [[export(b.recv[p]) for p in range(len(b.recv))] for b in self.ex],
+                    "recv_off": [dict(b.recv_off) for b in self.ex]}
+        except Exception:
+            mine = None
         allr = [None] * W
         dist.all_gather_object(allr, mine, group=group)
+        if any(x is None for x in allr):
+            raise RuntimeError("a rank could not export its receive buffers as CUDA IPC handles")
         self.opened = []
+        bases = {}
 
         def open_(h):
-            base = ctypes.c_void_p()
-            _lib.call("hb_ipc_open_handle", h[0], ctypes.byref(base))
-            self.opened.append(base.value)
-            return base.value + h[1]
+            # one mapping per exported allocation: the caching allocator packs
+            # small buffers (the counters) into shared segments, and a handle
+            # is opened once per process
+            if h[0] not in bases:
+                base = ctypes.c_void_p()
+                _lib.call("hb_ipc_open_handle", h[0], ctypes.byref(base))
+                bases[h[0]] = base.value
+                self.opened.append(base.value)
+            return bases[h[0]] + h[1]
+        try:
+            self._map(allr, open_, me, W, E, P)
+            ok = 1
+        except Exception:
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device="cpu" if host_staged(group) else device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()):
+            self.close()
+            for b in self.ex:
+                b.peer_recv, b.peer_off = None, None
+            raise RuntimeError("a rank could not map its peers' receive buffers")
+
+    def _map(self, allr, open_, me, W, E, P):
+        torch = self.torch
+        device = self.cnt.device
         cnt_addr = {r: (self.cnt.data_ptr() if r == me else open_(allr[r]["cnt"])) for r in range(W)}
         stride = self.cnt.stride()
         el = self.cnt.element_size()
