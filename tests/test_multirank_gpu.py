@@ -60,7 +60,7 @@ def _run(rank, world, owner, variant, st, bits, p2p=False):
     lay = RankLayout({p.id: p for p in parts if owner[p.id] == rank}, owner, rank)
     eng = DeviceRank(lay, ModelConfig((32, 16, 8), "sage"), TrainMode(variant, st), QuantConfig(bits), 3, 0.01,
                      int(g.train_mask.sum()), device="cuda:0", p2p=p2p)
-    assert (eng.p2p is not None) == (p2p and world > 1)
+    assert (eng.p2p is not None) == bool(p2p and world > 1 and os.environ.get("HB_FORCE_FALLBACK") is None)
     losses, meters = [], []
     prev = eng.total_stats()
     for e in range(1, EPOCHS + 1):
@@ -143,3 +143,57 @@ def test_p2p_counter_kernels():
     _lib.call("hb_p2p_wait", cnt.data_ptr() + 8, 1, flags.data_ptr(), 2, 2 * 10**6, _lib.stream_handle())
     torch.cuda.synchronize()
     assert int(flags) == 2
+
+
+def _fallback_worker(rank, world, port, q):
+    """Rank 1 cannot export its buffers: both ranks must agree to fall back to
+    the (here host-staged) send/recv exchange and train identically to it."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.pop("HB_P2P", None)
+    os.environ["HB_FORCE_FALLBACK"] = "1"         # _run: expect no peer links after the failure
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2303_01277_b200 import _lib
+        if rank == 1:
+            real = _lib.call
+
+            def broken(name, *args):
+                if name == "hb_ipc_get_handle":
+                    raise _lib.HaloLibError("hb_ipc_get_handle: simulated failure")
+                return real(name, *args)
+            _lib.call = broken
+        import warnings
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            out = _run(rank, world, [0, 1, 1, 0], "sync", 0, 1, p2p=True)
+        q.put((rank, "ok", (out, [str(x.message) for x in w])))
+    except Exception:
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_p2p_setup_failure_falls_back_on_every_rank():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, status, info = q.get(timeout=600)
+        assert status == "ok", f"rank {rank}:\n{info}"
+        res[rank] = info
+    for p in procs:
+        p.join(timeout=60)
+    (l0, m0, _), warn0 = res[0]
+    (l1, _, _), warn1 = res[1]
+    assert any("peer-memory halo exchange unavailable" in s for s in warn0)
+    assert any("peer-memory halo exchange unavailable" in s for s in warn1)
+    assert l0 == l1
