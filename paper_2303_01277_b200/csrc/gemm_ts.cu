@@ -161,7 +161,7 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // aligned by pointer arithmetic on the __shared__ array (an integer round
   // trip would hide the address space and turn every access generic)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t full[S], conv[S], empty[S], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[S], conv[S], empty[S], tfull[2], tempty[2], cbar[4];
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -177,6 +177,7 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    for (int a = 0; a < 4; ++a) mbar_init(&cbar[a], 1);     // epilogue warps' C-chunk loads
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -345,6 +346,7 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint8_t* stg = smem + S * C_::STAGE + (warp - kEpi0) * (2 * 4096);
     int sb = 0;
     int tc = 0;
+    uint32_t cph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tc) {
       int mi, ni, si;
       tile_coords(p, t, mi, ni, si);
@@ -380,6 +382,29 @@ gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[e]);
         if (p.tma_store) {
+          if (p.beta != 0.f) {
+            // accumulate: the C chunk arrives by TMA in the staging buffer's
+            // swizzled layout (coalesced, rows beyond M zero-filled), is added
+            // in registers, and the buffer is then reused for the store
+            uint8_t* lb = stg + sb * 4096;
+            if (lane == 0) {
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              mbar_expect_tx(&cbar[warp - kEpi0], 4096);
+              tma_2d(lb, &tmC, n0 + c0, row0, &cbar[warp - kEpi0]);
+            }
+            mbar_wait(&cbar[warp - kEpi0], cph);
+            cph ^= 1u;
+            const uint4* lr = reinterpret_cast<const uint4*>(lb + lane * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 q = lr[c ^ (lane & 7)];
+              v[4 * c] += p.beta * __uint_as_float(q.x);
+              v[4 * c + 1] += p.beta * __uint_as_float(q.y);
+              v[4 * c + 2] += p.beta * __uint_as_float(q.z);
+              v[4 * c + 3] += p.beta * __uint_as_float(q.w);
+            }
+            __syncwarp();
+          }
           if (p.C) {
             stage_and_store(stg + sb * 4096, v, &tmC, n0 + c0, row0, lane);
             sb ^= 1;
@@ -827,7 +852,9 @@ static cudaError_t launch_ts_bn(int M, int N, int K1, const float* A1, int64_t l
   // C == nullptr: only the ReLU copy is stored (a hidden layer's z is not
   // needed after the forward: the backward masks with h = relu(z) > 0)
   static const bool no_tma_store = getenv("HB_GEMM_NO_TMA_STORE") != nullptr;
-  p.tma_store = !no_tma_store && beta == 0.f && p.splits == 1 && (C == nullptr || gemm_tma_ok(C, ldc, 1)) &&
+  static const bool no_tma_acc = getenv("HB_GEMM_NO_TMA_ACC") != nullptr;
+  p.tma_store = !no_tma_store && (beta == 0.f || (C != nullptr && !no_tma_acc)) && p.splits == 1 &&
+                (C == nullptr || gemm_tma_ok(C, ldc, 1)) &&
                 (!p.relu_out || gemm_tma_ok(p.relu_out, ldr, 1)) &&
                 (C == nullptr || gemm_make_map(&tc, C, N, M, ldc, 32, false)) &&
                 (!p.relu_out || gemm_make_map(&tr, p.relu_out, N, M, ldr, 32, false));
