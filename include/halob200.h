@@ -291,11 +291,13 @@ int hb_ipc_close(void* base);
 int hb_p2p_signal(uint64_t* const* counters, int32_t n, void* stream);
 
 /* Stream-ordered: block the stream until *counter >= target (system-scope
- * acquire).  After timeout_ns the wait gives up and ORs flag_bit into *flags
- * (nullable) — a stalled or diverged peer surfaces as an error at the next
- * host check instead of a hung GPU. */
-int hb_p2p_wait(const uint64_t* counter, uint64_t target, uint32_t* flags, uint32_t flag_bit, uint64_t timeout_ns,
-                void* stream);
+ * acquire); target_dev (nullable, device memory) overrides target, so a
+ * captured CUDA graph can wait for a different count each replay.  After
+ * timeout_ns the wait gives up and ORs flag_bit into *flags (nullable) — a
+ * stalled or diverged peer surfaces as an error at the next host check
+ * instead of a hung GPU. */
+int hb_p2p_wait(const uint64_t* counter, uint64_t target, const uint64_t* target_dev, uint32_t* flags,
+                uint32_t flag_bit, uint64_t timeout_ns, void* stream);
 
 /* Argmax accuracy counts for evaluate() (trainer.py:129-144):
  * counts[2*k] = #rows with mask==k+1, counts[2*k+1] = #correct among them, k=0..2. */

@@ -60,7 +60,7 @@ _SIGS = {
     "hb_ipc_open_handle": [P, P],
     "hb_ipc_close": [P],
     "hb_p2p_signal": [P, c_int32, P],
-    "hb_p2p_wait": [P, c_uint64, P, c_uint32, c_uint64, P],
+    "hb_p2p_wait": [P, c_uint64, P, P, c_uint32, c_uint64, P],
     "hb_adam_step_dev": [P, P, P, P, c_int64, c_float, c_float, c_float, c_float, P, P, P, P, P],
     "hb_argmax_accuracy": [P, c_int64, c_int32, c_int32, P, P, P, P],
     "hb_dropout": [P, c_int64, c_int32, c_int64, c_int32, c_uint64, c_uint64, c_float, P, c_int64, P],

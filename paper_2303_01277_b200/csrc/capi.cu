@@ -47,8 +47,8 @@ cudaError_t launch_spmm_tiled_bin(int, int, int, const int32_t*, const int32_t*,
                                   const int32_t*, cudaStream_t);
 
 cudaError_t launch_p2p_signal(unsigned long long* const*, int, cudaStream_t);
-cudaError_t launch_p2p_wait(const unsigned long long*, unsigned long long, uint32_t*, uint32_t, unsigned long long,
-                            cudaStream_t);
+cudaError_t launch_p2p_wait(const unsigned long long*, unsigned long long, const unsigned long long*, uint32_t*,
+                            uint32_t, unsigned long long, cudaStream_t);
 cudaError_t alloc_base(const void*, void**);
 
 int num_sms() {
@@ -340,10 +340,11 @@ int hb_p2p_signal(uint64_t* const* counters, int32_t n, void* stream) {
                "hb_p2p_signal");
 }
 
-int hb_p2p_wait(const uint64_t* counter, uint64_t target, uint32_t* flags, uint32_t flag_bit, uint64_t timeout_ns,
-                void* stream) {
+int hb_p2p_wait(const uint64_t* counter, uint64_t target, const uint64_t* target_dev, uint32_t* flags,
+                uint32_t flag_bit, uint64_t timeout_ns, void* stream) {
   if (!counter) return fail(HB_EINVAL, "hb_p2p_wait: bad arguments");
-  return check(hb::launch_p2p_wait(reinterpret_cast<const unsigned long long*>(counter), target, flags, flag_bit,
+  return check(hb::launch_p2p_wait(reinterpret_cast<const unsigned long long*>(counter), target,
+                                   reinterpret_cast<const unsigned long long*>(target_dev), flags, flag_bit,
                                    timeout_ns, S(stream)),
                "hb_p2p_wait");
 }

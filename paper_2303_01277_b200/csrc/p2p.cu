@@ -35,8 +35,10 @@ __global__ void p2p_signal_kernel(unsigned long long* const* __restrict__ counte
 }
 
 __global__ void p2p_wait_kernel(const unsigned long long* __restrict__ counter, unsigned long long target,
-                                uint32_t* __restrict__ flags, uint32_t flag_bit, unsigned long long timeout_ns) {
+                                const unsigned long long* __restrict__ target_dev, uint32_t* __restrict__ flags,
+                                uint32_t flag_bit, unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
+  if (target_dev) target = *target_dev;        // CUDA-graph replays: the target changes per epoch
   unsigned long long t0, now, v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
@@ -57,9 +59,10 @@ cudaError_t launch_p2p_signal(unsigned long long* const* counters, int n, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_wait(const unsigned long long* counter, unsigned long long target, uint32_t* flags,
-                            uint32_t flag_bit, unsigned long long timeout_ns, cudaStream_t st) {
-  p2p_wait_kernel<<<1, 32, 0, st>>>(counter, target, flags, flag_bit, timeout_ns);
+cudaError_t launch_p2p_wait(const unsigned long long* counter, unsigned long long target,
+                            const unsigned long long* target_dev, uint32_t* flags, uint32_t flag_bit,
+                            unsigned long long timeout_ns, cudaStream_t st) {
+  p2p_wait_kernel<<<1, 32, 0, st>>>(counter, target, target_dev, flags, flag_bit, timeout_ns);
   return cudaGetLastError();
 }
 

@@ -201,6 +201,21 @@ class EpochGraph:
         self.stats = {}            # partition -> byte-meter deltas
         self.launches = 0
         self.done = None           # event after the last replay (its pinned buffers are free)
+        # N > 1 with the peer-memory exchange: the epoch's PeerLinks calls (re-run
+        # before each replay for the counter targets) and the targets' buffers
+        self.p2p_calls = []
+        self.p2p_host = self.p2p_dev = None
+        self.p2p_n = 0
+
+    def p2p_slot(self, target: int) -> int:
+        """Device address of the next wait-target slot (its capture-time value
+        is the target the first replay uses)."""
+        i = self.p2p_n
+        if i >= self.p2p_host.numel():
+            raise RuntimeError("more peer waits per epoch than target slots")
+        self.p2p_n += 1
+        self.p2p_host[i] = target
+        return self.p2p_dev.data_ptr() + 8 * i
 
     def pinned(self, owner, nbytes: int):
         return self._host[id(owner)][:nbytes]
@@ -836,10 +851,13 @@ class DeviceRank:
             self.finish_epoch()
 
     def graphable(self) -> bool:
-        """CUDA-graph epochs: one rank (NCCL exchanges stay eager), no dropout
-        (its per-epoch keys are launch arguments), no probe (host callbacks
-        inside the epoch), the tcgen05 GEMMs."""
-        return self.world == 1 and not self.drop and self.probe is None and self.gemm_impl != "cublas"
+        """CUDA-graph epochs: one rank, or several with the peer-memory halo
+        exchange (the gradient all-reduce and Adam then run eagerly after the
+        replay; NCCL halo exchanges are not captured); no dropout (its
+        per-epoch keys are launch arguments), no probe (host callbacks inside
+        the epoch), the tcgen05 GEMMs."""
+        return (self.world == 1 or self.p2p is not None) and not self.drop and self.probe is None \
+            and self.gemm_impl != "cublas"
 
     def run_epoch_graphed(self, epoch: int) -> str:
         """``run_epoch(epoch, defer=True)`` replayed from a CUDA graph of the
@@ -863,11 +881,18 @@ class DeviceRank:
                 ent.done.synchronize()          # its pinned buffers are free again
             for layer, phase in ent.consumed:
                 self._consume(epoch, layer, phase)
-            self.adam_t += 1
+            if self.world == 1:
+                self.adam_t += 1                # Adam is part of the graph
             for fill in ent.fills:
                 fill(epoch)
+            if ent.p2p_calls:
+                vals = self.p2p.replay_targets(ent.p2p_calls)
+                ent.p2p_host.numpy()[:len(vals)] = vals
             ent.graph.replay()
             ent.done = torch.cuda.current_stream().record_event()
+            if self.world > 1:
+                self.reduce(epoch)
+                self.adam(guarded=True)
             for k in ent.set_slots:
                 self.slots[k] = epoch
             for p, delta in ent.stats.items():
@@ -895,6 +920,11 @@ class DeviceRank:
         for b in bufs:
             b.capture = ent
         self._cap = ent
+        p2p = self.p2p
+        if p2p is not None:
+            ent.p2p_host = torch.zeros(1024, dtype=torch.int64).pin_memory()
+            ent.p2p_dev = torch.zeros(1024, dtype=torch.int64, device=self.dev)
+            p2p.capture = ent
         # no finalizers mid-capture: a collected pinned buffer or event of an
         # earlier engine would make an API call that invalidates the capture
         import gc
@@ -903,22 +933,30 @@ class DeviceRank:
         gc.disable()
         try:
             with torch.cuda.graph(ent.graph, stream=self._cap_stream, capture_error_mode="thread_local"):
+                if p2p is not None:
+                    ops.upload(ent.p2p_dev, ent.p2p_host)     # this replay's peer-wait targets
                 logits = self.forward(epoch, epoch_mode)
                 self.backward(epoch, epoch_mode, logits)
-                self.reduce(epoch)
-                self.adam(guarded=True)
+                if self.world == 1:
+                    self.reduce(epoch)
+                    self.adam(guarded=True)
         finally:
             if gc_was:
                 gc.enable()
             for b in bufs:
                 b.capture = None
             self._cap = None
+            if p2p is not None:
+                p2p.capture = None
             self.timer = timer
         ent.launches = self.launches - launches0
         ent.stats = {p: {k: v - stats0[p][k] for k, v in s.snapshot().items()} for p, s in self.stats.items()}
         ent.set_slots = [k for k, v in self.slots.items() if v == epoch and slots0.get(k) != epoch]
         ent.graph.replay()                      # a capture records the work; this runs it
         ent.done = torch.cuda.current_stream().record_event()
+        if self.world > 1:                      # the all-reduce and Adam stay eager
+            self.reduce(epoch)
+            self.adam(guarded=True)
         return ent
 
     def finish_epoch(self):

@@ -465,39 +465,81 @@ class PeerLinks:
                     if lst:
                         self._sig[(kind, e, p)] = torch.tensor(lst, dtype=torch.int64, device=device)
 
+    # CUDA-graph epochs (DeviceRank.run_epoch_graphed): while an EpochGraph is
+    # being captured, every wait reads its target from a device slot the graph
+    # uploads from its pinned buffer at the start of each replay; before a
+    # replay the recorded calls are re-run in "fill" mode, which only advances
+    # the counters and writes the targets the eager path would have used
+    capture = None
+    _fill = None
+
     def _wait(self, e, p, k, target, flags, stream):
-        if target <= 0:
+        if self._fill is not None:
+            self._fill.append(int(target))
             return
         addr = self.cnt.data_ptr() + self.cnt.element_size() * (
             e * self.cnt.stride(0) + p * self.cnt.stride(1) + k * self.cnt.stride(2))
-        _lib.call("hb_p2p_wait", addr, int(target), _lib.ptr(flags), FLAG_PROTOCOL, self.timeout_ns,
+        cap = self.capture
+        if cap is not None:
+            slot = cap.p2p_slot(int(target))
+            _lib.call("hb_p2p_wait", addr, 0, slot, _lib.ptr(flags), FLAG_PROTOCOL, self.timeout_ns,
+                      _lib.stream_handle(stream))
+            return
+        if target <= 0:
+            return
+        _lib.call("hb_p2p_wait", addr, int(target), None, _lib.ptr(flags), FLAG_PROTOCOL, self.timeout_ns,
                   _lib.stream_handle(stream))
 
     def _signal(self, kind, e, p, stream):
+        if self._fill is not None:
+            return
         a = self._sig.get((kind, e, p))
         if a is not None:
             _lib.call("hb_p2p_signal", a.data_ptr(), a.numel(), _lib.stream_handle(stream))
 
+    def _record(self, name, bufs, parity):
+        if self.capture is not None:
+            self.capture.p2p_calls.append((name, bufs, parity))
+
     def before_send(self, bufs, parity, flags, stream=None):
         """Before K1 writes into the peers' (e, parity) buffers."""
+        self._record("before_send", bufs, parity)
         e = self.index[id(bufs)]
         for r in self.send_ranks[e]:
             self._wait(e, parity, 1 + r, self.consumes[e, parity], flags, stream)
 
     def after_send(self, bufs, parity, stream=None):
+        self._record("after_send", bufs, parity)
         e = self.index[id(bufs)]
         self.sends[e, parity] += 1
         self._signal("send", e, parity, stream)
 
     def before_recv(self, bufs, parity, flags, stream=None):
         """Before K2 reads the (e, parity) receive buffer."""
+        self._record("before_recv", bufs, parity)
         e = self.index[id(bufs)]
         self._wait(e, parity, 0, self.sends[e, parity] * len(self.recv_ranks[e]), flags, stream)
 
     def after_recv(self, bufs, parity, stream=None):
+        self._record("after_recv", bufs, parity)
         e = self.index[id(bufs)]
         self.consumes[e, parity] += 1
         self._signal("recv", e, parity, stream)
+
+    def replay_targets(self, calls) -> list:
+        """Advance the counters through a captured epoch's calls and return
+        the wait targets in capture order (no launches)."""
+        out = []
+        self._fill = out
+        try:
+            for name, bufs, parity in calls:
+                if name in ("before_send", "before_recv"):
+                    getattr(self, name)(bufs, parity, None)
+                else:
+                    getattr(self, name)(bufs, parity)
+        finally:
+            self._fill = None
+        return out
 
     def close(self):
         for base in self.opened:

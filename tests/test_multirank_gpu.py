@@ -37,6 +37,7 @@ import torch.multiprocessing as mp  # noqa: E402
 
 EPOCHS = 4
 CASES = [("sync", 0, 32), ("async", 0, 32), ("async", 2, 32), ("sync", 0, 1)]
+GRAPH_CASES = [("sync", 0, 1), ("async", 0, 1), ("async", 2, 2)]
 
 
 def _free_port() -> int:
@@ -52,7 +53,7 @@ def _setup():
     return g, build_partitions(g, 4, "hash", 0, "sage")[2]
 
 
-def _run(rank, world, owner, variant, st, bits, p2p=False):
+def _run(rank, world, owner, variant, st, bits, p2p=False, graphed=False, epochs=EPOCHS):
     from paper_2303_01277_b200.codec import QuantConfig
     from paper_2303_01277_b200.trainer import DeviceRank, ModelConfig, TrainMode
     from paper_2303_01277_b200.transport import RankLayout
@@ -63,7 +64,19 @@ def _run(rank, world, owner, variant, st, bits, p2p=False):
     assert (eng.p2p is not None) == bool(p2p and world > 1 and os.environ.get("HB_FORCE_FALLBACK") is None)
     losses, meters = [], []
     prev = eng.total_stats()
-    for e in range(1, EPOCHS + 1):
+    if graphed:
+        # epochs 3.. replayed from CUDA graphs (peer waits with per-replay targets)
+        assert eng.graphable() == (eng.p2p is not None or world == 1)
+        for e in range(1, epochs + 1):
+            eng.run_epoch_graphed(e)
+            if e > 1:
+                eng.finish_epoch()
+                losses.append(eng.epoch_loss)
+        eng.finish_epoch()
+        losses.append(eng.epoch_loss)
+        torch.cuda.synchronize()
+        return losses, len(eng._graphs), [w.double().cpu().numpy() for w in eng.W]
+    for e in range(1, epochs + 1):
         eng.run_epoch(e)
         losses.append(eng.epoch_loss)
         t = eng.total_stats()
@@ -82,6 +95,9 @@ def _worker(rank, world, port, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         out = {c: _run(rank, world, [0, 1, 1, 0], *c) for c in CASES}
         out.update({("p2p",) + c: _run(rank, world, [0, 1, 1, 0], *c, p2p=True) for c in CASES})
+        for c in GRAPH_CASES:
+            out[("p2p_eager6",) + c] = _run(rank, world, [0, 1, 1, 0], *c, p2p=True, epochs=6)
+            out[("p2p_graph6",) + c] = _run(rank, world, [0, 1, 1, 0], *c, p2p=True, graphed=True, epochs=6)
         q.put((rank, "ok", out))
     except Exception:
         q.put((rank, "fail", traceback.format_exc()))
@@ -126,6 +142,15 @@ def test_two_ranks_on_one_gpu_match_single_rank():
         for a, b in zip(wp, w0):
             np.testing.assert_array_equal(a, b)
         assert res[1][("p2p",) + case][0] == l1
+    # CUDA-graph epochs over the peer-memory exchange: bit-identical to eager epochs
+    for case in GRAPH_CASES:
+        for r in (0, 1):
+            le, _, we = res[r][("p2p_eager6",) + case]
+            lg, ngraphs, wg = res[r][("p2p_graph6",) + case]
+            assert ngraphs >= 2, case
+            assert lg == le, (r, case)
+            for a, b in zip(wg, we):
+                np.testing.assert_array_equal(a, b)
 
 
 def test_p2p_counter_kernels():
@@ -137,10 +162,14 @@ def test_p2p_counter_kernels():
     flags = torch.zeros(1, dtype=torch.int32, device="cuda")
     addrs = torch.tensor([cnt.data_ptr() + 8 * i for i in (0, 2, 2)], dtype=torch.int64, device="cuda")
     _lib.call("hb_p2p_signal", addrs.data_ptr(), 3, _lib.stream_handle())
-    _lib.call("hb_p2p_wait", cnt.data_ptr() + 16, 2, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
+    _lib.call("hb_p2p_wait", cnt.data_ptr() + 16, 2, None, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
+    tgt = torch.tensor([3], dtype=torch.int64, device="cuda")      # target from device memory
+    _lib.call("hb_p2p_wait", cnt.data_ptr() + 16, 99, tgt.data_ptr(), flags.data_ptr(), 2, 2 * 10**6,
+              _lib.stream_handle())
     torch.cuda.synchronize()
-    assert cnt.tolist() == [1, 0, 2, 0] and int(flags) == 0
-    _lib.call("hb_p2p_wait", cnt.data_ptr() + 8, 1, flags.data_ptr(), 2, 2 * 10**6, _lib.stream_handle())
+    assert cnt.tolist() == [1, 0, 2, 0] and int(flags) == 2        # 2 < 3: the device target timed out
+    flags.zero_()
+    _lib.call("hb_p2p_wait", cnt.data_ptr() + 8, 1, None, flags.data_ptr(), 2, 2 * 10**6, _lib.stream_handle())
     torch.cuda.synchronize()
     assert int(flags) == 2
 

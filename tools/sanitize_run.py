@@ -65,7 +65,7 @@ def main():
     flags = torch.zeros(1, dtype=torch.int32, device="cuda")
     addrs = torch.tensor([cnt.data_ptr(), cnt.data_ptr() + 8], dtype=torch.int64, device="cuda")
     _lib.call("hb_p2p_signal", addrs.data_ptr(), 2, _lib.stream_handle())
-    _lib.call("hb_p2p_wait", cnt.data_ptr(), 1, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
+    _lib.call("hb_p2p_wait", cnt.data_ptr(), 1, None, flags.data_ptr(), 2, 10**9, _lib.stream_handle())
     torch.cuda.synchronize()
     print("sanitize workload done")
 
