@@ -621,8 +621,10 @@ def run_b200(args):
             kroof["gemm"] = {"bound": "tensor", "achieved": g["tflops"], "unit": "TFLOP/s",
                              "tf32_mma_tflops": 3.0 * g["tflops"], "peak": tf32_peak,
                              "frac": 3.0 * g["tflops"] / tf32_peak,
+                             "hbm_gbps": g["gbps"], "hbm_frac": g["gbps"] / peaks["hbm_gbs"],
                              "note": "3xTF32 (hi*hi + hi*lo + lo*hi per fp32 product); peak = dense TF32 = "
-                                     "measured bf16 / 2"}
+                                     "measured bf16 / 2; hbm_*: compulsory bytes (A, B, C, ReLU copy) of all "
+                                     "GEMM launches — the narrow-K shapes (K <= 128) are HBM-bound"}
         if dom == "gemm" and "gemm" in kroof and roof is not None:
             # the GEMMs dominate (e.g. the Yelp-shaped GCN): the headline roofline
             # is theirs; the SpMM's moves to kernel_rooflines

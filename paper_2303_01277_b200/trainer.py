@@ -552,7 +552,10 @@ class DeviceRank:
         """out (+)= a @ b (trainer.py:294,313,318-321).  out None: only
         relu_out = relu(a @ b) is stored (tcgen05 path)."""
         nl, nc = a.shape[0], b.shape[1]
-        with self.timer("gemm", 0, 2 * a.shape[0] * a.shape[1] * b.shape[1]):
+        # compulsory bytes: A, B once, C written (and read when accumulating), the ReLU copy
+        nbytes = 4 * (a.shape[0] * a.shape[1] + b.shape[0] * nc + nl * nc * (
+            (out is not None) + bool(accumulate) + (relu_out is not None)))
+        with self.timer("gemm", nbytes, 2 * a.shape[0] * a.shape[1] * b.shape[1]):
             if self.gemm_impl == "cublas":
                 if accumulate:
                     out.addmm_(a, b)
@@ -570,7 +573,9 @@ class DeviceRank:
         in one GEMM pass, without materialising the concatenation.  out None:
         only relu_out = relu(...) is stored (tcgen05 path)."""
         nl, nc = a1.shape[0], b1.shape[1]
-        with self.timer("gemm", 0, 2 * a1.shape[0] * (a1.shape[1] + a2.shape[1]) * b1.shape[1]):
+        nbytes = 4 * (nl * (a1.shape[1] + a2.shape[1]) + (b1.shape[0] + b2.shape[0]) * nc + nl * nc * (
+            (out is not None) + (relu_out is not None)))
+        with self.timer("gemm", nbytes, 2 * a1.shape[0] * (a1.shape[1] + a2.shape[1]) * b1.shape[1]):
             if self.gemm_impl == "cublas":
                 self.torch.mm(a1, b1, out=out)
                 out.addmm_(a2, b2)

@@ -32,6 +32,11 @@ def table(path):
             if r.get("unit") == "TFLOP/s":
                 ach = f"{r['achieved']:.0f} TF/s fp32-equiv ({r.get('tf32_mma_tflops', 0):.0f} TF/s TF32 MMA)"
                 bound, frac = "tensor (3xTF32)", f"{r['frac']:.2f}"
+                if r.get("hbm_frac") is not None:
+                    ach += f"; {r['hbm_gbps']:.0f} GB/s compulsory"
+                    frac += f" of tensor; {r['hbm_frac']:.2f} of HBM"
+                    if r["hbm_frac"] > r["frac"]:
+                        bound = "HBM (narrow K) / tensor"
             elif "philox_frac" in r:
                 ach = f"{r['achieved']:.0f} GB/s, {r['philox_gelem_s']:.0f} G elem/s"
                 bound, frac = "Philox issue rate", f"{r['philox_frac']:.2f} of 414 G/s"
