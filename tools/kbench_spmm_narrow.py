@@ -1,7 +1,8 @@
 """Narrow factored SpMM (32 < d <= 48) on the Reddit-shaped aggregation
 operators, 64-row blocks x 255-column windows, per consumer variant
 (hb_spmm_set_narrow): CUDA-event time per launch, max |diff| vs variant 1.
-One JSON line per (operator, variant).   python tools/kbench_spmm_narrow.py [d] [reps] [variants...]"""
+One JSON line per (operator, variant).
+  python tools/kbench_spmm_narrow.py [d] [reps] [block rows] [variants...]"""
 import json
 import sys
 from pathlib import Path
@@ -10,7 +11,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def main(d=41, reps=20, *variants):
+def main(d=41, reps=20, block_rows=64, *variants):
     import torch
     from bench import build_graph
     from paper_2303_01277_b200 import ops
@@ -26,7 +27,7 @@ def main(d=41, reps=20, *variants):
     ld = (d + 3) // 4 * 4
     for name, M in (("mean", A), ("mean_T", At)):
         X = torch.randn(M.cols, ld, device="cuda")
-        T = ops.TiledCsr(M, factored=True, block_rows=64, window=255)
+        T = ops.TiledCsr(M, factored=True, block_rows=block_rows, window=255)
         ref = None
         for var in variants:
             ops.spmm_set_narrow(var)
@@ -44,7 +45,7 @@ def main(d=41, reps=20, *variants):
             diff = None if ref is None else float((Y[:, :d] - ref).abs().max())
             if ref is None:
                 ref = Y[:, :d].clone()
-            print(json.dumps({"op": name, "d": d, "variant": var, "ms": round(ms, 4), "nnz": M.nnz,
+            print(json.dumps({"op": name, "d": d, "block_rows": block_rows, "variant": var, "ms": round(ms, 4), "nnz": M.nnz,
                               "max_diff_vs_first": diff,
                               "gathered_gbps": round(4.0 * M.nnz * d / ms / 1e6, 1)}), flush=True)
         ops.spmm_set_narrow(1)
