@@ -152,14 +152,6 @@ def _stack_csr(layout: RankLayout, which: str):
     return rp, ci, v
 
 
-def _transpose(rows, cols, rp, ci, v):
-    r = np.repeat(np.arange(rows, dtype=np.int64), np.diff(rp))
-    o = np.argsort(ci, kind="stable")
-    trp = np.zeros(cols + 1, dtype=np.int64)
-    np.cumsum(np.bincount(ci, minlength=cols), out=trp[1:])
-    return trp, r[o], v[o]
-
-
 def _transpose_device(a: "ops.DeviceCsr") -> "ops.DeviceCsr":
     """CSR of A^T built on the device (stable by row, so each row of A^T keeps
     ascending columns) — the reference precomputes the same transpose on the
