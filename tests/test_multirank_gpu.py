@@ -226,3 +226,49 @@ def test_p2p_setup_failure_falls_back_on_every_rank():
     assert any("peer-memory halo exchange unavailable" in s for s in warn0)
     assert any("peer-memory halo exchange unavailable" in s for s in warn1)
     assert l0 == l1
+
+
+def _world4_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        out = {}
+        for c in (("sync", 0, 1), ("async", 2, 2)):
+            out[("staged",) + c] = _run(rank, world, [0, 1, 2, 3], *c)
+            out[("p2p",) + c] = _run(rank, world, [0, 1, 2, 3], *c, p2p=True)
+        q.put((rank, "ok", out))
+    except Exception:
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_four_ranks_peer_memory_matches_staged():
+    """Four processes on one GPU, one partition each: every rank maps three
+    peers' receive buffers; the peer-memory exchange trains bit-identically to
+    the host-staged one (sync 1-bit, Sylvie-A with the adaptor at 2 bits)."""
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_world4_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, status, info = q.get(timeout=900)
+        assert status == "ok", f"rank {rank}:\n{info}"
+        res[rank] = info
+    for p in procs:
+        p.join(timeout=60)
+    for c in (("sync", 0, 1), ("async", 2, 2)):
+        for r in range(4):
+            ls, ms, ws = res[r][("staged",) + c]
+            lp, mp_, wp = res[r][("p2p",) + c]
+            assert lp == ls and mp_ == ms, (r, c)
+            for a, b in zip(wp, ws):
+                np.testing.assert_array_equal(a, b)
