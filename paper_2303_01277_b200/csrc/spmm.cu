@@ -313,8 +313,12 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
   if (vec && dyn && par && d <= 128) {
     // row-parallel lane groups (chunks rounded to whole groups of rows)
     const int ch = (chunk + 3) & ~3;
+    // d <= 64: 8-lane groups x 2 float4, 4 rows in flight per group; 64 < d <=
+    // 128: 8-lane groups x 4 float4, 2 in flight (17.5 TB/s gathered on the
+    // ogbn 128-wide operator, the raw L2 gather ceiling; 16-lane groups x 2
+    // float4: 16.5; profiles/r2_kbench_ogbn_rows.txt)
     if (d <= 64) spmm_rows_par_kernel<2, 8, 4><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, next_row, ch);
-    else spmm_rows_par_kernel<2, 16, 4><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, next_row, ch);
+    else spmm_rows_par_kernel<4, 8, 2><<<grid, kSpWarps * 32, 0, st>>>(nrows, row_ptr, col_idx, vals, X, ldx, d, Y, ldy, next_row, ch);
     return cudaGetLastError();
   }
   if (vec && d <= 1024) {
