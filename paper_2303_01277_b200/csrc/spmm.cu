@@ -341,10 +341,11 @@ cudaError_t launch_spmm(int nrows, const int64_t* row_ptr, const int32_t* col_id
         else if (window == 8) HB_S(2, 32, 8);
         else HB_S(2, 32, 4);
         break;
-      case 3:   // measured on Yelp-shaped rows: 1 row in flight beats 2 at 3 float4 per lane
-        if (window == 4) HB_S(3, 32, 4);
+      case 3:   // Yelp's 300-wide layer-1 operator: 4 nonzeros in flight 1.44 ms, 1 in flight 1.60
+                // (profiles/r2_kbench_yelp_rows.txt)
+        if (window == 1) HB_S(3, 32, 1);
         else if (window == 2) HB_S(3, 32, 2);
-        else HB_S(3, 32, 1);
+        else HB_S(3, 32, 4);
         break;
       case 4:
         if (window == 1) HB_S(4, 32, 1);
