@@ -1065,59 +1065,70 @@ dequant_b1_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int
     }
     const unsigned singles = __ballot_sync(0xffffffffu, my_single);
     const int n = min(32, num_dst - i0);
-    for (int j = 0; j < n; ++j) {
-      const int t = __shfl_sync(0xffffffffu, my_t, j);
-      float* out = dst + (int64_t)t * ld;
-      if (!((singles >> j) & 1u)) {
-        // zero or several received rows for this destination: chunk-wise f64 sum
-        const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
-        for (int c0 = 4 * lane; c0 < d; c0 += 128) {
-          double a4[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int k = k0; k < k1; ++k) {
-            const int q = src_rows[k];
-            const hb_segment_t& sg = segs_s[find_segment_smem(seg_begin, nseg, q)];
-            const int r = q - sg.row_begin;
-            const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
-            const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
-            const uint8_t* pay = blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
-            int code[4];
-            codes4(pay, rb, c0, 1, d, code);
+    // rows of a warp's batch are written U at a time: the payload bytes of all
+    // U rows are loaded before the first store, so the load latency is paid
+    // once per U rows (U = 1 for wide rows: the byte registers would spill)
+    constexpr int U = NCH <= 2 ? 4 : 1;
+    for (int j0 = 0; j0 < n; j0 += U) {
+      uint32_t bits[U][NCH];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, j & 31));
+        const bool ld_ok = j < n && ((singles >> (j & 31)) & 1u);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c0 = ch * 128 + 4 * lane;
+          bits[u][ch] = (ld_ok && c0 < d) ? (uint32_t)__ldg(pay + (c0 >> 3)) : 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        if (j >= n) break;
+        const int t = __shfl_sync(0xffffffffu, my_t, j);
+        float* out = dst + (int64_t)t * ld;
+        if (!((singles >> j) & 1u)) {
+          // zero or several received rows for this destination: chunk-wise f64 sum
+          const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
+          for (int c0 = 4 * lane; c0 < d; c0 += 128) {
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = k0; k < k1; ++k) {
+              const int q = src_rows[k];
+              const hb_segment_t& sg = segs_s[find_segment_smem(seg_begin, nseg, q)];
+              const int r = q - sg.row_begin;
+              const uint8_t* blk = reinterpret_cast<const uint8_t*>(sg.out);
+              const float* mp = reinterpret_cast<const float*>(blk + HB_HEADER_BYTES + 8 * (int64_t)r);
+              const uint8_t* pay = blk + HB_HEADER_BYTES + 8 * (int64_t)sg.num_rows + (int64_t)r * rb;
+              int code[4];
+              codes4(pay, rb, c0, 1, d, code);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                a4[e] = __dadd_rn(a4[e], __dadd_rn(__dmul_rn((double)mp[1], (double)code[e]), (double)mp[0]));
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              a4[e] = __dadd_rn(a4[e], __dadd_rn(__dmul_rn((double)mp[1], (double)code[e]), (double)mp[0]));
+              if (c0 + e < d) out[c0 + e] = __double2float_rn(a4[e]);
           }
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (c0 + e < d) out[c0 + e] = __double2float_rn(a4[e]);
+          continue;
         }
-        continue;
-      }
-      const float mn = __shfl_sync(0xffffffffu, my_mn, j);
-      const float one = __shfl_sync(0xffffffffu, my_one, j);
-      const uint8_t* pay = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, my_pay, j));
-      // all of the row's payload bytes are loaded before the first store (a
-      // byte pointer may alias the fp32 stores, so the compiler would
-      // otherwise serialise one load latency per 128-column chunk)
-      uint32_t bits[NCH];
+        const float mn = __shfl_sync(0xffffffffu, my_mn, j);
+        const float one = __shfl_sync(0xffffffffu, my_one, j);
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int c0 = ch * 128 + 4 * lane;
-        bits[ch] = c0 < d ? (uint32_t)__ldg(pay + (c0 >> 3)) : 0u;
-      }
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int c0 = ch * 128 + 4 * lane;
-        if (c0 >= d) continue;
-        const uint32_t nib = bits[ch] >> (c0 & 7);
-        const float4 v = make_float4((nib & 1u) ? one : mn, (nib & 2u) ? one : mn, (nib & 4u) ? one : mn,
-                                     (nib & 8u) ? one : mn);
-        if (vec && c0 + 3 < d) {
-          *reinterpret_cast<float4*>(out + c0) = v;
-        } else {
-          out[c0] = v.x;
-          if (c0 + 1 < d) out[c0 + 1] = v.y;
-          if (c0 + 2 < d) out[c0 + 2] = v.z;
-          if (c0 + 3 < d) out[c0 + 3] = v.w;
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int c0 = ch * 128 + 4 * lane;
+          if (c0 >= d) continue;
+          const uint32_t nib = bits[u][ch] >> (c0 & 7);
+          const float4 v = make_float4((nib & 1u) ? one : mn, (nib & 2u) ? one : mn, (nib & 4u) ? one : mn,
+                                       (nib & 8u) ? one : mn);
+          if (vec && c0 + 3 < d) {
+            *reinterpret_cast<float4*>(out + c0) = v;
+          } else {
+            out[c0] = v.x;
+            if (c0 + 1 < d) out[c0 + 1] = v.y;
+            if (c0 + 2 < d) out[c0 + 2] = v.z;
+            if (c0 + 3 < d) out[c0 + 3] = v.w;
+          }
         }
       }
     }
@@ -1680,9 +1691,16 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
     // one received row per destination, 1 bit, overwrite: the fp32 fast path
     if (!accumulate && bits == 1) {
       const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
-      const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
-#define HB_K2B(N) dequant_b1_batched_kernel<N><<<g32, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, \
-                                                                          src_rows, d, dst, ld)
+      // one wave: the resident CTAs per SM (register-limited) times the SMs
+      auto one_wave = [&](const void* f) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kQWarps * 32, 0) != cudaSuccess || per_sm < 1)
+          per_sm = 4;
+        const int cap = num_sms() * per_sm;
+        return want32 < cap ? want32 : cap;
+      };
+#define HB_K2B(N) dequant_b1_batched_kernel<N><<<one_wave((const void*)dequant_b1_batched_kernel<N>), kQWarps * 32, 0, \
+                                                 st>>>(segs, nseg, num_dst, dst_rows, src_ptr, src_rows, d, dst, ld)
       if (nch <= 1) HB_K2B(1);
       else if (nch <= 2) HB_K2B(2);
       else if (nch <= 4) HB_K2B(4);
@@ -1691,9 +1709,15 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
 #undef HB_K2B
     } else if (accumulate && bits == 1 && vec_dst) {
       const int want32 = (num_dst + 32 * kQWarps - 1) / (32 * kQWarps);
-      const int g32 = want32 < num_sms() * 8 ? want32 : num_sms() * 8;
-#define HB_K2A(N) dequant_b1_acc_kernel<N><<<g32, kQWarps * 32, 0, st>>>(segs, nseg, num_dst, dst_rows, src_ptr, \
-                                                                      src_rows, d, dst, ld)
+      auto one_wave = [&](const void* f) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kQWarps * 32, 0) != cudaSuccess || per_sm < 1)
+          per_sm = 4;
+        const int cap = num_sms() * per_sm;
+        return want32 < cap ? want32 : cap;
+      };
+#define HB_K2A(N) dequant_b1_acc_kernel<N><<<one_wave((const void*)dequant_b1_acc_kernel<N>), kQWarps * 32, 0, \
+                                             st>>>(segs, nseg, num_dst, dst_rows, src_ptr, src_rows, d, dst, ld)
       if (nch <= 1) HB_K2A(1);
       else if (nch <= 2) HB_K2A(2);
       else if (nch <= 4) HB_K2A(4);
