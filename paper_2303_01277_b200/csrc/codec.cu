@@ -1696,7 +1696,9 @@ cudaError_t launch_dequant_gather(const hb_segment_t* segs, int nseg, int num_ds
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kQWarps * 32, 0) != cudaSuccess || per_sm < 1)
           per_sm = 4;
-        const int cap = num_sms() * per_sm;
+        // one resident wave for the 4-rows-ahead layout (d <= 256); the wide
+        // rows measured faster with two (Reddit d = 602: 0.25 vs 0.27 ms)
+        const int cap = num_sms() * (nch <= 2 ? per_sm : 8);
         return want32 < cap ? want32 : cap;
       };
 #define HB_K2B(N) dequant_b1_batched_kernel<N><<<one_wave((const void*)dequant_b1_batched_kernel<N>), kQWarps * 32, 0, \
