@@ -58,7 +58,7 @@ def test_spmm_matches_reference_golden(algo, window, halo):
             assert np.all(np.abs(got - y) <= tol), (k, pad, np.abs(got - y).max())
 
 
-@pytest.mark.parametrize("d", [3, 8, 20, 44, 96, 128, 200, 300, 512, 1024, 1100])
+@pytest.mark.parametrize("d", [3, 8, 20, 44, 47, 65, 96, 101, 126, 128, 200, 300, 512, 1024, 1100])
 def test_spmm_random_power_law_rows(d):
     """Skewed row lengths (0 .. 2000 nonzeros) at every width class."""
     import scipy.sparse as sp
