@@ -1315,22 +1315,34 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         const int c0 = ch * 128 + 4 * lane;
-        nb[ch] = c0 < d ? (uint32_t)(__ldg(pay + (c0 >> 3)) >> (c0 & 7)) : 0u;
+        // the raw byte: shifting here would make the prefetch wait for its load
+        nb[ch] = c0 < d ? (uint32_t)__ldg(pay + (c0 >> 3)) : 0u;
       }
       return true;
     };
     uint32_t nib_cur[NCH];
     bool have_cur = first_bits(0, nib_cur);
+    // narrow rows (NCH <= 2) keep two rows in flight ahead of the one being
+    // accumulated (nxt = j + 1 loaded one iteration early, nn = j + 2)
+    constexpr bool kTwo = NCH <= 2;
+    float4 nxt[NCH];
+    uint32_t nib_nxt[NCH];
+    bool have_nxt = false;
+    if (kTwo && n > 1) {
+      load_row(__shfl_sync(0xffffffffu, my_t, 1), nxt);
+      have_nxt = first_bits(1, nib_nxt);
+    }
     for (int j = 0; j < n; ++j) {
       const int t = __shfl_sync(0xffffffffu, my_t, j);
-      const int tn = __shfl_sync(0xffffffffu, my_t, (j + 1) & 31);
       const int k0 = __shfl_sync(0xffffffffu, my_k0, j), k1 = __shfl_sync(0xffffffffu, my_k1, j);
-      float4 nxt[NCH];
-      uint32_t nib_nxt[NCH];
-      bool have_nxt = false;
-      if (j + 1 < n) {
-        load_row(tn, nxt);
-        have_nxt = first_bits(j + 1, nib_nxt);
+      const int ja = kTwo ? j + 2 : j + 1;                 // the row loaded this iteration
+      const int ta = __shfl_sync(0xffffffffu, my_t, ja & 31);
+      float4 nn[NCH];
+      uint32_t nib_nn[NCH];
+      bool have_nn = false;
+      if (ja < n) {
+        load_row(ta, nn);
+        have_nn = first_bits(ja, nib_nn);
       }
       double acc[NCH][4];
 #pragma unroll
@@ -1353,7 +1365,7 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
         for (int ch = 0; ch < NCH; ++ch) {
           const int c0 = ch * 128 + 4 * lane;
           if (c0 >= d) continue;
-          const uint32_t nib = pre ? nib_cur[ch] : (uint32_t)(pay[c0 >> 3] >> (c0 & 7));
+          const uint32_t nib = (pre ? nib_cur[ch] : (uint32_t)pay[c0 >> 3]) >> (c0 & 7);
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[ch][e] = __dadd_rn(acc[ch][e], ((nib >> e) & 1u) ? v1 : v0);
         }
@@ -1373,13 +1385,23 @@ dequant_b1_acc_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int num
           if (c0 + 2 < d) out[c0 + 2] = v.z;
         }
       }
-      if (j + 1 < n) {
+      if (kTwo) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           cur[ch] = nxt[ch];
           nib_cur[ch] = nib_nxt[ch];
+          nxt[ch] = nn[ch];
+          nib_nxt[ch] = nib_nn[ch];
         }
         have_cur = have_nxt;
+        have_nxt = have_nn;
+      } else if (j + 1 < n) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          cur[ch] = nn[ch];
+          nib_cur[ch] = nib_nn[ch];
+        }
+        have_cur = have_nn;
       }
     }
   }
