@@ -1068,7 +1068,7 @@ dequant_b1_batched_kernel(const hb_segment_t* __restrict__ segs_g, int nseg, int
     // rows of a warp's batch are written U at a time: the payload bytes of all
     // U rows are loaded before the first store, so the load latency is paid
     // once per U rows (U = 1 for wide rows: the byte registers would spill)
-    constexpr int U = NCH <= 2 ? 4 : 1;
+    constexpr int U = NCH <= 2 ? 4 : (NCH <= 5 ? 2 : 1);
     for (int j0 = 0; j0 < n; j0 += U) {
       uint32_t bits[U][NCH];
 #pragma unroll
